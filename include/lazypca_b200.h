@@ -1,0 +1,214 @@
+/* lazypca_b200 — C ABI of the B200-native Lazy SPCA / SPCA / RP reducer.
+ *
+ * Drop-in boundary for the reference C++ library `lazypca` (namespace lazypca,
+ * headers proj/core/include/lazypca/*.hpp, CMake target lazypca::core). Every
+ * entry point below names the reference interface it replaces; the header-only
+ * C++ shim include/lazypca_b200.hpp rebuilds the reference's value types and
+ * exception classes on top of these calls so existing callers relink unchanged.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no torch / CUDA types in any signature (streams
+ *    are passed as void*; NCCL unique ids as 128 opaque bytes).
+ *  - Matrices are described by lpca_matrix_view. Dense data may be row- or
+ *    column-major, fp32 or fp64, and live on the host or on the context's device.
+ *    CSC views (the reference's SparseMatrix) are densified on upload in this
+ *    release ("out of scope").
+ *  - Every call returns an lpca_status. Non-zero codes mirror the reference's
+ *    exception hierarchy (proj/core/include/lazypca/error.hpp:10-58); the message
+ *    and payload (index / last_gap / line) are available per thread through
+ *    lpca_last_error*().
+ *  - A context is bound to one device (one process per GPU). Calls on one
+ *    context are serialised by the caller; separate contexts are independent.
+ *  - There is no CPU fallback: if no sm_100 device is present every compute
+ *    entry point fails with LPCA_ERR_CUDA.
+ */
+#ifndef LAZYPCA_B200_H
+#define LAZYPCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPCA_ABI_VERSION 1
+
+typedef enum {
+  LPCA_OK = 0,
+  LPCA_ERR_DIMENSION = 1,          /* lazypca::DimensionError */
+  LPCA_ERR_INVALID_ARGUMENT = 2,   /* lazypca::InvalidArgumentError */
+  LPCA_ERR_RANK_DEFICIENCY = 3,    /* lazypca::RankDeficiencyError(index) */
+  LPCA_ERR_CONVERGENCE = 4,        /* lazypca::ConvergenceError(last_gap) */
+  LPCA_ERR_PARSE = 5,              /* lazypca::ParseError(line) */
+  LPCA_ERR_CUDA = 6,               /* device / driver failure (no reference analogue) */
+  LPCA_ERR_NCCL = 7,               /* collective failure (no reference analogue) */
+  LPCA_ERR_INTERNAL = 9
+} lpca_status;
+
+/* lazypca::ReducerMethod (proj/core/include/lazypca/reducer.hpp:12) */
+typedef enum { LPCA_RP = 0, LPCA_SPCA = 1, LPCA_LAZY_SPCA = 2 } lpca_method;
+/* lazypca::ProjectionKind (proj/core/include/lazypca/projection.hpp:12) */
+typedef enum { LPCA_GAUSSIAN = 0, LPCA_VERY_SPARSE = 1 } lpca_projection_kind;
+/* lazypca::DensityPolicy::Mode (proj/core/include/lazypca/projection.hpp:17-21) */
+typedef enum { LPCA_DENSITY_AGGRESSIVE = 0, LPCA_DENSITY_CONSERVATIVE = 1, LPCA_DENSITY_EXPLICIT = 2 } lpca_density_mode;
+
+typedef enum { LPCA_F32 = 4, LPCA_F64 = 8 } lpca_dtype;
+typedef enum { LPCA_HOST = 0, LPCA_DEVICE = 1 } lpca_location;
+typedef enum { LPCA_ROW_MAJOR = 0, LPCA_COL_MAJOR = 1, LPCA_CSC = 2 } lpca_layout;
+
+/* A matrix argument. Dense: data + ld (elements between consecutive rows for
+ * row-major, between consecutive columns for column-major; 0 = packed).
+ * CSC (lazypca::SparseMatrix, proj/core/include/lazypca/sparse_matrix.hpp:17-49):
+ * col_ptr (cols+1), row_idx (nnz), values (nnz, dtype) — host memory only. */
+typedef struct {
+  int32_t dtype;      /* lpca_dtype */
+  int32_t layout;     /* lpca_layout */
+  int32_t location;   /* lpca_location */
+  int32_t reserved;
+  int64_t rows, cols, ld;
+  const void* data;
+  const int64_t* col_ptr;
+  const int64_t* row_idx;
+  int64_t nnz;
+} lpca_matrix_view;
+
+/* lazypca::ReducerConfig + nested ProjectionSpec
+ * (proj/core/include/lazypca/reducer.hpp:20-33, projection.hpp:36-45). */
+typedef struct {
+  int32_t method;          /* lpca_method */
+  int32_t projection_kind; /* lpca_projection_kind */
+  int64_t k;
+  int64_t l;               /* 0 = same as k */
+  int64_t proj_n;          /* ProjectionSpec::n, 0 = from the data */
+  int64_t proj_l;          /* ProjectionSpec::l, 0 = l */
+  double density;          /* ProjectionSpec::density, in (0, 1] */
+  uint64_t seed;           /* ProjectionSpec::seed */
+  int64_t block_rows;      /* > 0 selects the streaming variants */
+  int32_t streaming;
+  int32_t deterministic;   /* accepted for manifest compatibility */
+  int32_t power_iters;     /* q >= 0. Builder extension, NOT in the reference
+                              (SPEC.md:371): q subspace steps Z = X^T U,
+                              Z <- orth(Z), U = X Z before F is formed. */
+  int32_t reserved;
+} lpca_config;
+
+/* lazypca::ReducerTimings (proj/core/include/lazypca/reducer.hpp:59-66),
+ * seconds, device-event timed; `power` and `transform` are extensions. */
+typedef struct {
+  double sketch, qr, f_form, svd, total;
+  double power, transform, h2d, d2h;
+} lpca_timings;
+
+typedef struct lpca_ctx lpca_ctx;
+typedef struct lpca_map lpca_map; /* device-resident lazypca::ReductionMap */
+
+/* ---- errors ------------------------------------------------------------- */
+const char* lpca_last_error(void);
+int64_t lpca_last_error_index(void);   /* RankDeficiencyError::index / ParseError::line, -1 if n/a */
+double lpca_last_error_gap(void);      /* ConvergenceError::last_gap */
+int32_t lpca_abi_version(void);
+
+/* ---- contexts (one per GPU) --------------------------------------------- */
+lpca_status lpca_ctx_create(int32_t device, lpca_ctx** out);
+/* Row-sharded data parallelism over NCCL: `rank` of `world`, all ranks pass the
+ * same 128-byte id from lpca_nccl_unique_id on rank 0. world == 1 needs no id. */
+lpca_status lpca_nccl_unique_id(void* out_128_bytes);
+lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
+                                 const void* nccl_id_128, lpca_ctx** out);
+lpca_status lpca_ctx_destroy(lpca_ctx* ctx);
+/* Launch everything on this cudaStream_t (default: the context's own stream). */
+lpca_status lpca_ctx_set_stream(lpca_ctx* ctx, void* cuda_stream);
+lpca_status lpca_ctx_synchronize(lpca_ctx* ctx);
+/* Kernel-path switch for A/B measurements: 0 = tcgen05 split-TF32 (fp32 data,
+ * default), 1 = SIMT FFMA/DFMA. Both are native sm_100a code. */
+lpca_status lpca_ctx_set_gemm_path(lpca_ctx* ctx, int32_t path);
+/* 1 = fp64 kernels use the reference's summation order (separate multiply and
+ * add, no split-K): results bitwise equal to the reference's spmm / gemm_t /
+ * dense_aat; slower. Kernel-level exports always run in this mode. */
+lpca_status lpca_ctx_set_exact_order(lpca_ctx* ctx, int32_t exact);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t lpca_ctx_launch_count(const lpca_ctx* ctx);
+
+/* ---- configuration ------------------------------------------------------ */
+/* ReducerConfig::resolved (proj/core/src/reducer.cpp:137-161). */
+lpca_status lpca_config_resolve(const lpca_config* in, int64_t data_cols, lpca_config* out);
+/* density_for (proj/core/src/projection.cpp:38-50). */
+lpca_status lpca_density_for(int32_t mode, int64_t k, double value, double* out);
+
+/* ---- projection --------------------------------------------------------- */
+/* regenerate / gen_gaussian / gen_very_sparse (proj/core/src/projection.cpp:71-130)
+ * Writes Omega dense column-major n x l (fp64; very sparse -> entries in
+ * {-1,0,+1}, unscaled) to `out` (host or device per `out_location`) and the
+ * variance constant c to *scale. Generated on the device. */
+lpca_status lpca_regenerate(lpca_ctx* ctx, int32_t kind, int64_t n, int64_t l, double density,
+                            uint64_t seed, void* out, int32_t out_location, double* scale);
+
+/* ---- reducers ----------------------------------------------------------- */
+/* reduce (proj/core/src/reducer.cpp:337-346) and, by method,
+ * reduce_rp / reduce_spca / reduce_lazy_spca (:171-234). For a distributed
+ * context X is this rank's row shard; the returned map is identical on all ranks. */
+lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_view* x,
+                     lpca_map** out_map, lpca_timings* timings);
+/* apply_map (proj/core/src/reducer.cpp:348-353): Y = X V, m x k.
+ * y_layout row- or column-major (the reference returns column-major), ldy 0 = packed. */
+lpca_status lpca_transform(lpca_ctx* ctx, const lpca_map* map, const lpca_matrix_view* x,
+                           void* y, int32_t y_dtype, int32_t y_layout, int32_t y_location,
+                           int64_t ldy, lpca_timings* timings);
+/* fit followed by transform of the same X, uploading a host X once. */
+lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_view* x,
+                               lpca_map** out_map, void* y, int32_t y_dtype, int32_t y_layout,
+                               int32_t y_location, int64_t ldy, lpca_timings* timings);
+
+/* ---- maps (lazypca::ReductionMap, proj/core/include/lazypca/reducer.hpp:47-57) */
+typedef struct {
+  int32_t method;
+  int32_t reserved;
+  int64_t k, l, n;
+  uint64_t seed;
+  double density;
+  double scale;
+  int32_t has_singular_values;
+  int32_t reserved2;
+} lpca_map_info;
+lpca_status lpca_map_info_get(const lpca_map* map, lpca_map_info* out);
+/* V: n x k column-major fp64; sigma: k fp64 (only when has_singular_values). */
+lpca_status lpca_map_copy_v(const lpca_map* map, double* v_out, int32_t out_location);
+lpca_status lpca_map_copy_sigma(const lpca_map* map, double* sigma_out);
+/* A map from host data (e.g. a loaded map file) for lpca_transform. */
+lpca_status lpca_map_create(lpca_ctx* ctx, const lpca_map_info* info, const double* v_host,
+                            const double* sigma_host, lpca_map** out);
+lpca_status lpca_map_destroy(lpca_map* map);
+
+/* ---- kernel-level exports (proj/core/include/lazypca/kernels.hpp:17-36,
+ *      truncated_svd.hpp:24, tridiag_eigh.hpp:8). Host or device operands; fp64
+ *      column-major unless stated; X views as above. ------------------------- */
+/* spmm(X, W): out m x w column-major fp64 (the sketch U = X Omega / apply). */
+lpca_status lpca_spmm(lpca_ctx* ctx, const lpca_matrix_view* x, const double* w, int64_t w_cols,
+                      int32_t w_location, double* out, int32_t out_location);
+/* gemm_t(U, X): U m x l column-major fp64, out l x n column-major fp64. */
+lpca_status lpca_gemm_t(lpca_ctx* ctx, const double* u, int64_t m, int64_t l, int32_t u_location,
+                        const lpca_matrix_view* x, double* out, int32_t out_location);
+/* dense_aat(F): F l x n, out l x l, bitwise symmetric. */
+lpca_status lpca_dense_aat(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
+                           int32_t location, double* out);
+/* Symmetric eigendecomposition (replaces tridiag_eigh / jacobi_eigh): eigenvalues
+ * descending, eigenvectors column-major. Parallel cyclic Jacobi on the device. */
+lpca_status lpca_eigh(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                      double* evecs);
+/* truncated_svd_via_gram(F, k): sigma (k), v (n x k), u_tilde (l x k, may be NULL). */
+lpca_status lpca_truncated_svd_via_gram(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
+                                        int64_t k, int32_t location, double* sigma, double* v,
+                                        double* u_tilde);
+
+/* ---- synthetic data (BASELINE generator; not part of the reference) -------
+ * X = G diag(rho^t) H + noise * E into device memory, row-major m x n, rows
+ * [row0, row0 + m) of the global matrix (so any row shard can be produced on any
+ * GPU). G, H, E are counter-based N(0,1) streams keyed by (seed, index). */
+lpca_status lpca_synth_lowrank(lpca_ctx* ctx, int64_t row0, int64_t m, int64_t n, int64_t r,
+                               double rho, double noise, uint64_t seed, int32_t dtype, void* x_dev,
+                               int64_t ldx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAZYPCA_B200_H */

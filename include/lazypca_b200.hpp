@@ -1,0 +1,375 @@
+// Header-only C++ shim: the reference `lazypca` API (namespace lazypca,
+// proj/core/include/lazypca/*.hpp) rebuilt over the lazypca_b200 C ABI, so a
+// caller of the reference recompiles against this header and links
+// liblazypca_b200.so instead of lazypca::core. Value types keep the reference's
+// layouts (column-major fp64 DenseMatrix, canonical CSC SparseMatrix) and the
+// C status codes are rethrown as the reference's exception classes
+// (proj/core/include/lazypca/error.hpp:10-58).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "lazypca_b200.h"
+
+namespace lazypca {
+
+using index_t = std::int64_t;
+
+// ---- errors (error.hpp) ---------------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+class DimensionError : public Error {
+ public:
+  explicit DimensionError(const std::string& w) : Error(w) {}
+};
+class InvalidArgumentError : public Error {
+ public:
+  explicit InvalidArgumentError(const std::string& w) : Error(w) {}
+};
+class RankDeficiencyError : public Error {
+ public:
+  RankDeficiencyError(const std::string& w, std::int64_t index = -1) : Error(w), index_(index) {}
+  std::int64_t index() const { return index_; }
+
+ private:
+  std::int64_t index_;
+};
+class ConvergenceError : public Error {
+ public:
+  ConvergenceError(const std::string& w, double gap = 0.0) : Error(w), gap_(gap) {}
+  double last_gap() const { return gap_; }
+
+ private:
+  double gap_;
+};
+class ParseError : public Error {
+ public:
+  ParseError(const std::string& w, std::int64_t line = 0) : Error(w), line_(line) {}
+  std::int64_t line() const { return line_; }
+
+ private:
+  std::int64_t line_;
+};
+// Device / collective failures have no reference analogue; they derive from Error.
+class DeviceError : public Error {
+ public:
+  explicit DeviceError(const std::string& w) : Error(w) {}
+};
+
+namespace detail {
+inline void check(lpca_status s) {
+  if (s == LPCA_OK) return;
+  const std::string msg = lpca_last_error();
+  switch (s) {
+    case LPCA_ERR_DIMENSION: throw DimensionError(msg);
+    case LPCA_ERR_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
+    case LPCA_ERR_RANK_DEFICIENCY: throw RankDeficiencyError(msg, lpca_last_error_index());
+    case LPCA_ERR_CONVERGENCE: throw ConvergenceError(msg, lpca_last_error_gap());
+    case LPCA_ERR_PARSE: throw ParseError(msg, lpca_last_error_index());
+    default: throw DeviceError(msg);
+  }
+}
+// One context per process-thread on device 0 unless the caller installs one.
+inline lpca_ctx*& current_ctx() {
+  static thread_local lpca_ctx* ctx = nullptr;
+  return ctx;
+}
+inline lpca_ctx* ctx() {
+  lpca_ctx*& c = current_ctx();
+  if (!c) check(lpca_ctx_create(0, &c));
+  return c;
+}
+}  // namespace detail
+
+// Installs a caller-owned context (e.g. one rank of a row-sharded NCCL group).
+inline void use_context(lpca_ctx* c) { detail::current_ctx() = c; }
+
+// threading.hpp:15-17 — accepted for compatibility; the GPU path has no host pool.
+inline void set_thread_count(int) {}
+inline int thread_count() { return 0; }
+
+// ---- value types (dense_matrix.hpp, sparse_matrix.hpp) ------------------------------
+class DenseMatrix {
+ public:
+  DenseMatrix() : rows_(0), cols_(0) {}
+  DenseMatrix(index_t r, index_t c) : rows_(r), cols_(c), data_(static_cast<std::size_t>(r * c), 0.0) {}
+  DenseMatrix(index_t r, index_t c, std::vector<double> cm) : rows_(r), cols_(c), data_(std::move(cm)) {}
+  static DenseMatrix identity(index_t n) {
+    DenseMatrix m(n, n);
+    for (index_t i = 0; i < n; ++i) m(i, i) = 1.0;
+    return m;
+  }
+  index_t rows() const { return rows_; }
+  index_t cols() const { return cols_; }
+  bool empty() const { return rows_ == 0 || cols_ == 0; }
+  double& operator()(index_t i, index_t j) { return data_[static_cast<std::size_t>(j * rows_ + i)]; }
+  double operator()(index_t i, index_t j) const { return data_[static_cast<std::size_t>(j * rows_ + i)]; }
+  double* col(index_t j) { return data_.data() + j * rows_; }
+  const double* col(index_t j) const { return data_.data() + j * rows_; }
+  double* data() { return data_.data(); }
+  const double* data() const { return data_.data(); }
+
+ private:
+  index_t rows_, cols_;
+  std::vector<double> data_;
+};
+
+class SparseMatrix {
+ public:
+  SparseMatrix() : rows_(0), cols_(0), col_ptr_{0} {}
+  static SparseMatrix from_csc(index_t rows, index_t cols, std::vector<index_t> col_ptr,
+                               std::vector<index_t> row_idx, std::vector<double> values) {
+    SparseMatrix s;
+    s.rows_ = rows;
+    s.cols_ = cols;
+    s.col_ptr_ = std::move(col_ptr);
+    s.row_idx_ = std::move(row_idx);
+    s.values_ = std::move(values);
+    return s;  // canonical-form validation happens in the library on use
+  }
+  index_t rows() const { return rows_; }
+  index_t cols() const { return cols_; }
+  index_t nnz() const { return static_cast<index_t>(values_.size()); }
+  const std::vector<index_t>& col_ptr() const { return col_ptr_; }
+  const std::vector<index_t>& row_idx() const { return row_idx_; }
+  const std::vector<double>& values() const { return values_; }
+  lpca_matrix_view view() const {
+    lpca_matrix_view v{};
+    v.dtype = LPCA_F64;
+    v.layout = LPCA_CSC;
+    v.location = LPCA_HOST;
+    v.rows = rows_;
+    v.cols = cols_;
+    v.data = values_.data();
+    v.col_ptr = col_ptr_.data();
+    v.row_idx = row_idx_.data();
+    v.nnz = nnz();
+    return v;
+  }
+
+ private:
+  index_t rows_, cols_;
+  std::vector<index_t> col_ptr_, row_idx_;
+  std::vector<double> values_;
+};
+
+// ---- configuration (projection.hpp, reducer.hpp) -------------------------------------
+enum class ProjectionKind { gaussian = LPCA_GAUSSIAN, very_sparse = LPCA_VERY_SPARSE };
+enum class ReducerMethod { rp = LPCA_RP, spca = LPCA_SPCA, lazy_spca = LPCA_LAZY_SPCA };
+
+inline std::string to_string(ReducerMethod m) {
+  return m == ReducerMethod::rp ? "rp" : m == ReducerMethod::spca ? "spca" : "lazy_spca";
+}
+inline ReducerMethod reducer_method_from_string(const std::string& t) {
+  if (t == "rp") return ReducerMethod::rp;
+  if (t == "spca") return ReducerMethod::spca;
+  if (t == "lazy_spca") return ReducerMethod::lazy_spca;
+  throw InvalidArgumentError("unknown method '" + t + "' (expected rp, spca, or lazy_spca)");
+}
+
+struct DensityPolicy {
+  enum class Mode { aggressive, conservative, explicit_value };
+  Mode mode = Mode::conservative;
+  double value = 0.0;
+  static DensityPolicy aggressive() { return {Mode::aggressive, 0.0}; }
+  static DensityPolicy conservative() { return {Mode::conservative, 0.0}; }
+  static DensityPolicy explicit_value(double v) { return {Mode::explicit_value, v}; }
+};
+
+inline double density_for(const DensityPolicy& p, index_t k) {
+  double out = 0.0;
+  detail::check(lpca_density_for(static_cast<int32_t>(p.mode), k, p.value, &out));
+  return out;
+}
+
+struct ProjectionSpec {
+  ProjectionKind kind = ProjectionKind::gaussian;
+  index_t n = 0;
+  index_t l = 0;
+  double density = 1.0;
+  std::uint64_t seed = 0;
+};
+
+struct ReducerConfig {
+  ReducerMethod method = ReducerMethod::spca;
+  index_t k = 0;
+  index_t l = 0;
+  ProjectionSpec projection;
+  index_t block_rows = 0;
+  bool streaming = false;
+  bool deterministic = true;
+  int power_iters = 0;  // extension (not in the reference)
+
+  lpca_config c_config() const {
+    lpca_config c{};
+    c.method = static_cast<int32_t>(method);
+    c.projection_kind = static_cast<int32_t>(projection.kind);
+    c.k = k;
+    c.l = l;
+    c.proj_n = projection.n;
+    c.proj_l = projection.l;
+    c.density = projection.density;
+    c.seed = projection.seed;
+    c.block_rows = block_rows;
+    c.streaming = streaming;
+    c.deterministic = deterministic;
+    c.power_iters = power_iters;
+    return c;
+  }
+  ReducerConfig resolved(index_t data_cols) const {
+    const lpca_config in = c_config();
+    lpca_config out{};
+    detail::check(lpca_config_resolve(&in, data_cols, &out));
+    ReducerConfig r = *this;
+    r.l = out.l;
+    r.projection.n = out.proj_n;
+    r.projection.l = out.proj_l;
+    r.streaming = out.streaming != 0;
+    return r;
+  }
+};
+
+struct ReducerTimings {
+  double sketch = 0.0, qr = 0.0, f_form = 0.0, svd = 0.0, total = 0.0;
+};
+
+struct ReductionMap {
+  std::string method;
+  index_t k = 0, l = 0, n = 0;
+  std::uint64_t seed = 0;
+  double density = 1.0;
+  double scale = 1.0;
+  DenseMatrix v;
+  std::vector<double> singular_values;
+};
+
+namespace detail {
+inline ReductionMap to_host(lpca_map* m) {
+  std::unique_ptr<lpca_map, lpca_status (*)(lpca_map*)> guard(m, lpca_map_destroy);
+  lpca_map_info info{};
+  check(lpca_map_info_get(m, &info));
+  ReductionMap out;
+  out.method = to_string(static_cast<ReducerMethod>(info.method));
+  out.k = info.k;
+  out.l = info.l;
+  out.n = info.n;
+  out.seed = info.seed;
+  out.density = info.density;
+  out.scale = info.scale;
+  out.v = DenseMatrix(info.n, info.k);
+  if (info.n * info.k > 0) check(lpca_map_copy_v(m, out.v.data(), LPCA_HOST));
+  if (info.has_singular_values) {
+    out.singular_values.resize(static_cast<std::size_t>(info.k));
+    check(lpca_map_copy_sigma(m, out.singular_values.data()));
+  }
+  return out;
+}
+inline ReductionMap fit(const SparseMatrix& x, ReducerConfig cfg, ReducerMethod m, ReducerTimings* t) {
+  cfg.method = m;
+  const lpca_config c = cfg.c_config();
+  const lpca_matrix_view v = x.view();
+  lpca_map* out = nullptr;
+  lpca_timings tm{};
+  check(lpca_fit(ctx(), &c, &v, &out, &tm));
+  if (t) {
+    t->sketch += tm.sketch + tm.power;
+    t->qr += tm.qr;
+    t->f_form += tm.f_form;
+    t->svd += tm.svd;
+    t->total += tm.total + tm.h2d;
+  }
+  return to_host(out);
+}
+}  // namespace detail
+
+// reducer.hpp:69-92
+inline ReductionMap reduce_rp(const SparseMatrix& x, const ReducerConfig& c, ReducerTimings* t = nullptr) {
+  return detail::fit(x, c, ReducerMethod::rp, t);
+}
+inline ReductionMap reduce_spca(const SparseMatrix& x, const ReducerConfig& c, ReducerTimings* t = nullptr) {
+  return detail::fit(x, c, ReducerMethod::spca, t);
+}
+inline ReductionMap reduce_lazy_spca(const SparseMatrix& x, const ReducerConfig& c,
+                                     ReducerTimings* t = nullptr) {
+  return detail::fit(x, c, ReducerMethod::lazy_spca, t);
+}
+inline ReductionMap reduce(const SparseMatrix& x, const ReducerConfig& c, ReducerTimings* t = nullptr) {
+  return detail::fit(x, c, c.method, t);
+}
+
+inline DenseMatrix apply_map(const ReductionMap& map, const SparseMatrix& x) {
+  lpca_map_info info{};
+  info.method = static_cast<int32_t>(reducer_method_from_string(map.method));
+  info.k = map.k;
+  info.l = map.l;
+  info.n = map.n;
+  info.seed = map.seed;
+  info.density = map.density;
+  info.scale = map.scale;
+  lpca_map* m = nullptr;
+  detail::check(lpca_map_create(detail::ctx(), &info, map.v.data(), nullptr, &m));
+  std::unique_ptr<lpca_map, lpca_status (*)(lpca_map*)> guard(m, lpca_map_destroy);
+  DenseMatrix y(x.rows(), map.k);
+  const lpca_matrix_view v = x.view();
+  detail::check(lpca_transform(detail::ctx(), m, &v, y.data(), LPCA_F64, LPCA_COL_MAJOR, LPCA_HOST, 0, nullptr));
+  return y;
+}
+
+// projection.hpp:48-72 (dense representation of either family)
+struct ProjectionMatrix {
+  ProjectionSpec spec;
+  double scale = 1.0;
+  DenseMatrix omega;
+};
+inline ProjectionMatrix regenerate(const ProjectionSpec& s) {
+  ProjectionMatrix p;
+  p.spec = s;
+  p.omega = DenseMatrix(s.n, s.l);
+  detail::check(lpca_regenerate(detail::ctx(), static_cast<int32_t>(s.kind), s.n, s.l, s.density, s.seed,
+                                p.omega.data(), LPCA_HOST, &p.scale));
+  return p;
+}
+
+// kernels.hpp:17-36 (fp64, reference summation order)
+inline DenseMatrix spmm(const SparseMatrix& a, const DenseMatrix& b) {
+  DenseMatrix out(a.rows(), b.cols());
+  const lpca_matrix_view v = a.view();
+  detail::check(lpca_spmm(detail::ctx(), &v, b.data(), b.cols(), LPCA_HOST, out.data(), LPCA_HOST));
+  return out;
+}
+inline DenseMatrix gemm_t(const DenseMatrix& u, const SparseMatrix& x) {
+  DenseMatrix out(u.cols(), x.cols());
+  const lpca_matrix_view v = x.view();
+  detail::check(lpca_gemm_t(detail::ctx(), u.data(), u.rows(), u.cols(), LPCA_HOST, &v, out.data(), LPCA_HOST));
+  return out;
+}
+inline DenseMatrix dense_aat(const DenseMatrix& f) {
+  DenseMatrix out(f.rows(), f.rows());
+  detail::check(lpca_dense_aat(detail::ctx(), f.data(), f.rows(), f.cols(), LPCA_HOST, out.data()));
+  return out;
+}
+
+struct TruncatedSVD {
+  DenseMatrix u_tilde;
+  std::vector<double> singular_values;
+  DenseMatrix v;
+};
+inline TruncatedSVD truncated_svd_via_gram(const DenseMatrix& f, index_t k) {
+  TruncatedSVD s;
+  s.singular_values.resize(static_cast<std::size_t>(k > 0 ? k : 0));
+  s.v = DenseMatrix(f.cols(), k);
+  s.u_tilde = DenseMatrix(f.rows(), k);
+  detail::check(lpca_truncated_svd_via_gram(detail::ctx(), f.data(), f.rows(), f.cols(), k, LPCA_HOST,
+                                            s.singular_values.data(), s.v.data(), s.u_tilde.data()));
+  return s;
+}
+
+}  // namespace lazypca

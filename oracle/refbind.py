@@ -1,0 +1,196 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes binding of oracle/_ref/liblazypca_ref.so.
+
+That library is the unmodified reference core (/root/reference/proj/core/src,
+built by oracle/Makefile) behind the flat wrapper oracle/ref_capi.cpp. Only
+tests/, __graft_entry__.smoke() and bench.py's CPU legs use it, as the checker
+or the timed reference; the product never loads it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "_ref" / "liblazypca_ref.so"
+REF_SRC = Path("/root/reference/proj/core")
+
+_lib = None
+
+
+class RefError(RuntimeError):
+    def __init__(self, code: int, msg: str, index: int):
+        super().__init__(msg)
+        self.code, self.index = code, index
+
+
+def build_if_possible() -> bool:
+    """Builds _ref from the reference sources when they are present (here, not on the GPU box)."""
+    if REF_SRC.exists():
+        r = subprocess.run(["make", "-s", "-j8", "-C", str(HERE)], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"oracle/_ref build failed:\n{r.stdout}\n{r.stderr}")
+    return LIB.exists()
+
+
+def available() -> bool:
+    return LIB.exists()
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            raise RuntimeError(f"{LIB} missing; build it with `make -C oracle` where /root/reference exists")
+        lib = C.CDLL(str(LIB))
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_last_error_index.restype = C.c_int64
+        _lib = lib
+    return _lib
+
+
+def _chk(code: int) -> None:
+    if code != 0:
+        lib = load()
+        raise RefError(code, lib.ref_last_error().decode(), int(lib.ref_last_error_index()))
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+def set_threads(n: int) -> None:
+    load().ref_set_thread_count(C.c_int(n))
+
+
+def regenerate(kind: int, n: int, l: int, density: float, seed: int):
+    out = np.zeros((n, l), order="F")
+    sc = C.c_double()
+    _chk(load().ref_regenerate(C.c_int(kind), C.c_int64(n), C.c_int64(l), C.c_double(density),
+                               C.c_uint64(seed), _p(out), C.byref(sc)))
+    return out, sc.value
+
+
+def density_for(mode: int, k: int, value: float = 0.0) -> float:
+    out = C.c_double()
+    _chk(load().ref_density_for(C.c_int(mode), C.c_int64(k), C.c_double(value), C.byref(out)))
+    return out.value
+
+
+def _x(x: np.ndarray):
+    x = np.ascontiguousarray(x)
+    dt = 4 if x.dtype == np.float32 else 8
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    return x, dt
+
+
+def reduce(method: int, x: np.ndarray, k: int, l: int, seed: int, kind: int = 0, density: float = 1.0,
+           block_rows: int = 0):
+    """reduce() on dense row-major X. Returns (V n x k, sigma, scale, timings[5])."""
+    x, dt = _x(x)
+    m, n = x.shape
+    v = np.zeros((n, k), order="F")
+    sig = np.zeros(k)
+    sc = C.c_double()
+    t = np.zeros(5)
+    _chk(load().ref_reduce(C.c_int(method), _p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n), C.c_int64(k),
+                           C.c_int64(l), C.c_uint64(seed), C.c_int(kind), C.c_double(density),
+                           C.c_int64(block_rows), _p(v), _p(sig), C.byref(sc), _p(t)))
+    return v, sig, sc.value, t
+
+
+def fit_transform(method: int, x: np.ndarray, k: int, l: int, seed: int, kind: int = 0,
+                  density: float = 1.0, want_y: bool = True):
+    """reduce + apply_map, timed inside the reference call (CSC build excluded)."""
+    x, dt = _x(x)
+    m, n = x.shape
+    y = np.zeros((m, k), order="F") if want_y else None
+    v = np.zeros((n, k), order="F")
+    sig = np.zeros(k)
+    secs = C.c_double()
+    _chk(load().ref_fit_transform(C.c_int(method), _p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n),
+                                  C.c_int64(k), C.c_int64(l), C.c_uint64(seed), C.c_int(kind),
+                                  C.c_double(density), _p(y), _p(v), _p(sig), C.byref(secs)))
+    return y, v, sig, secs.value
+
+
+def apply_map(x: np.ndarray, v: np.ndarray):
+    x, dt = _x(x)
+    v = np.asfortranarray(v, dtype=np.float64)
+    m, n = x.shape
+    y = np.zeros((m, v.shape[1]), order="F")
+    _chk(load().ref_apply_map(_p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n), _p(v), C.c_int64(v.shape[1]),
+                              _p(y)))
+    return y
+
+
+def spmm(x: np.ndarray, w: np.ndarray):
+    x, dt = _x(x)
+    w = np.asfortranarray(w, dtype=np.float64)
+    m, n = x.shape
+    out = np.zeros((m, w.shape[1]), order="F")
+    _chk(load().ref_spmm(_p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n), _p(w), C.c_int64(w.shape[1]),
+                         _p(out)))
+    return out
+
+
+def gemm_t(u: np.ndarray, x: np.ndarray):
+    x, dt = _x(x)
+    u = np.asfortranarray(u, dtype=np.float64)
+    m, l = u.shape
+    n = x.shape[1]
+    out = np.zeros((l, n), order="F")
+    _chk(load().ref_gemm_t(_p(u), C.c_int64(m), C.c_int64(l), _p(x), C.c_int(dt), C.c_int64(n), _p(out)))
+    return out
+
+
+def dense_aat(f: np.ndarray):
+    f = np.asfortranarray(f, dtype=np.float64)
+    l, n = f.shape
+    out = np.zeros((l, l), order="F")
+    _chk(load().ref_dense_aat(_p(f), C.c_int64(l), C.c_int64(n), _p(out)))
+    return out
+
+
+def eigh(a: np.ndarray, which: str = "tridiag"):
+    a = np.asfortranarray(a, dtype=np.float64)
+    l = a.shape[0]
+    ev = np.zeros(l)
+    vec = np.zeros((l, l), order="F")
+    _chk(load().ref_eigh(C.c_int(0 if which == "tridiag" else 1), _p(a), C.c_int64(l), _p(ev), _p(vec)))
+    return ev, vec
+
+
+def truncated_svd(f: np.ndarray, k: int):
+    f = np.asfortranarray(f, dtype=np.float64)
+    l, n = f.shape
+    sig = np.zeros(k)
+    v = np.zeros((n, k), order="F")
+    ut = np.zeros((l, k), order="F")
+    _chk(load().ref_truncated_svd(_p(f), C.c_int64(l), C.c_int64(n), C.c_int64(k), _p(sig), _p(v), _p(ut)))
+    return sig, v, ut
+
+
+def householder_qr(a: np.ndarray):
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, l = a.shape
+    q = np.zeros((m, l), order="F")
+    r = np.zeros((l, l), order="F")
+    _chk(load().ref_householder_qr(_p(a), C.c_int64(m), C.c_int64(l), _p(q), _p(r)))
+    return q, r
+
+
+def chordal(v1: np.ndarray, v2: np.ndarray) -> float:
+    v1 = np.asfortranarray(v1, dtype=np.float64)
+    v2 = np.asfortranarray(v2, dtype=np.float64)
+    out = C.c_double()
+    _chk(load().ref_chordal(_p(v1), _p(v2), C.c_int64(v1.shape[0]), C.c_int64(v1.shape[1]), C.byref(out)))
+    return out.value
+
+
+def cpu_threads() -> int:
+    return len(os.sched_getaffinity(0))

@@ -1,0 +1,67 @@
+"""Builds the product library liblazypca_b200.so in-tree with nvcc for sm_100a.
+
+The library is self-contained C ABI (include/lazypca_b200.h): static cudart,
+NCCL from the system (same soname as torch's bundled copy), no torch types.
+Usage: python -m paper_1709_07175_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
+LIB = PKG / "liblazypca_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I", str(ROOT / "include"), "-I", str(CSRC)]
+SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu"]
+
+
+def _obj(src: str) -> Path:
+    return BUILD / (Path(src).stem + ".o")
+
+
+def _needs(src: Path, obj: Path) -> bool:
+    if not obj.exists():
+        return True
+    deps = [src, *CSRC.glob("*.cuh"), ROOT / "include" / "lazypca_b200.h"]
+    return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
+
+
+def _compile(src: str, verbose: bool) -> None:
+    obj = _obj(src)
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    if verbose and r.stderr:
+        print(r.stderr)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    todo = [s for s in SOURCES if force or _needs(CSRC / s, _obj(s))]
+    with ThreadPoolExecutor(max_workers=min(8, max(1, len(todo)))) as ex:
+        list(ex.map(lambda s: _compile(s, verbose), todo))
+    objs = [str(_obj(s)) for s in SOURCES]
+    if todo or not LIB.exists() or force:
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-Xlinker", "-z,defs",
+               "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,256 @@
+// SIMT tall-skinny GEMMs (FFMA for fp32 data, DFMA for fp64 data).
+//
+// These are the exact-order / fp64 path and the A/B baseline for the tcgen05
+// split-TF32 kernels in gemm_tc.cu. Accumulation order is a fixed function of
+// the shapes (CTA tiles own disjoint outputs; K is walked in ascending order),
+// so results are bitwise reproducible run to run — the reference's determinism
+// contract (proj/core/include/lazypca/kernels.hpp:5-9). In `exact` mode the fp64
+// kernels use separate multiply and add in the reference's summation order,
+// which reproduces the reference's spmm / gemm_t bit for bit on dense input.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace lpca {
+
+namespace {
+
+constexpr int kBM = 64, kBN = 64, kBK = 16, kThreads = 256;
+constexpr int kFlushK = 256;  // fp32 partial sums span at most this many products
+
+template <typename T, bool kExact>
+struct Acc;
+
+template <bool kExact>
+struct Acc<double, kExact> {
+  double v[4][4];
+  __device__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[a][b] = 0.0;
+  }
+  __device__ __forceinline__ void add(int a, int b, double x, double y) {
+    if constexpr (kExact)
+      v[a][b] = __dadd_rn(v[a][b], __dmul_rn(x, y));
+    else
+      v[a][b] = fma(x, y, v[a][b]);
+  }
+  __device__ __forceinline__ void flush() {}
+  __device__ __forceinline__ double get(int a, int b) const { return v[a][b]; }
+};
+
+template <bool kExact>
+struct Acc<float, kExact> {
+  float f[4][4];
+  double d[4][4];
+  __device__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        f[a][b] = 0.f;
+        d[a][b] = 0.0;
+      }
+  }
+  __device__ __forceinline__ void add(int a, int b, float x, float y) { f[a][b] = fmaf(x, y, f[a][b]); }
+  __device__ __forceinline__ void flush() {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        d[a][b] += static_cast<double>(f[a][b]);
+        f[a][b] = 0.f;
+      }
+  }
+  __device__ __forceinline__ double get(int a, int b) const { return d[a][b]; }
+};
+
+// out[i*ors + c*ocs] = sum_j X[i, j] W[c, j]; CTA tile 64 rows x 64 columns.
+template <typename T, typename TO, bool kExact>
+__global__ void __launch_bounds__(kThreads) xw_simt_kernel(const T* __restrict__ x, index_t m,
+                                                           index_t n, index_t ldx,
+                                                           const T* __restrict__ w, index_t wc,
+                                                           index_t ldw, TO* __restrict__ out,
+                                                           index_t ors, index_t ocs) {
+  __shared__ T As[kBK][kBM + 1];
+  __shared__ T Bs[kBK][kBN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const index_t i0 = static_cast<index_t>(blockIdx.x) * kBM;
+  const index_t c0 = static_cast<index_t>(blockIdx.y) * kBN;
+  Acc<T, kExact> acc;
+  acc.zero();
+  int since_flush = 0;
+  for (index_t k0 = 0; k0 < n; k0 += kBK) {
+    for (int e = threadIdx.x; e < kBM * kBK; e += kThreads) {
+      const int r = e / kBK, kk = e % kBK;
+      const index_t gi = i0 + r, gk = k0 + kk;
+      As[kk][r] = (gi < m && gk < n) ? x[gi * ldx + gk] : T(0);
+    }
+    for (int e = threadIdx.x; e < kBN * kBK; e += kThreads) {
+      const int c = e / kBK, kk = e % kBK;
+      const index_t gc = c0 + c, gk = k0 + kk;
+      Bs[kk][c] = (gc < wc && gk < n) ? w[gc * ldw + gk] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc.add(a, b, av[a], bv[b]);
+    }
+    since_flush += kBK;
+    if (since_flush >= kFlushK) {
+      acc.flush();
+      since_flush = 0;
+    }
+    __syncthreads();
+  }
+  acc.flush();
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const index_t gi = i0 + ty + 16 * a;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const index_t gc = c0 + tx + 16 * b;
+      if (gc < wc) out[gi * ors + gc * ocs] = static_cast<TO>(acc.get(a, b));
+    }
+  }
+}
+
+// part[c][j*l + r] = sum_{i in chunk c} U[i, r] X[i, j]; CTA tile 64 (r) x 64 (j).
+template <typename T, bool kExact>
+__global__ void __launch_bounds__(kThreads) utx_simt_kernel(const T* __restrict__ u, index_t ldu,
+                                                            const T* __restrict__ x, index_t ldx,
+                                                            index_t m, index_t l, index_t n,
+                                                            index_t chunk_rows,
+                                                            double* __restrict__ part) {
+  __shared__ T Us[kBK][kBM + 1];
+  __shared__ T Xs[kBK][kBN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const index_t j0 = static_cast<index_t>(blockIdx.x) * kBN;
+  const index_t r0 = static_cast<index_t>(blockIdx.y) * kBM;
+  const index_t chunk = blockIdx.z;
+  const index_t row_begin = chunk * chunk_rows;
+  const index_t row_end = row_begin + chunk_rows < m ? row_begin + chunk_rows : m;
+  Acc<T, kExact> acc;
+  acc.zero();
+  int since_flush = 0;
+  for (index_t i0 = row_begin; i0 < row_end; i0 += kBK) {
+    for (int e = threadIdx.x; e < kBM * kBK; e += kThreads) {
+      const int kk = e / kBM, rr = e % kBM;
+      const index_t gi = i0 + kk, gr = r0 + rr;
+      Us[kk][rr] = (gi < row_end && gr < l) ? u[gi * ldu + gr] : T(0);
+    }
+    for (int e = threadIdx.x; e < kBN * kBK; e += kThreads) {
+      const int kk = e / kBN, jj = e % kBN;
+      const index_t gi = i0 + kk, gj = j0 + jj;
+      Xs[kk][jj] = (gi < row_end && gj < n) ? x[gi * ldx + gj] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      T uv[4], xv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) uv[a] = Us[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) xv[b] = Xs[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc.add(a, b, xv[b], uv[a]);
+    }
+    since_flush += kBK;
+    if (since_flush >= kFlushK) {
+      acc.flush();
+      since_flush = 0;
+    }
+    __syncthreads();
+  }
+  acc.flush();
+  double* dst = part + chunk * l * n;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const index_t gr = r0 + ty + 16 * a;
+    if (gr >= l) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const index_t gj = j0 + tx + 16 * b;
+      if (gj < n) dst[gj * l + gr] = acc.get(a, b);
+    }
+  }
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ part, index_t nparts,
+                                       index_t count, double* __restrict__ out) {
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    double s = part[e];
+    for (index_t c = 1; c < nparts; ++c) s += part[c * count + e];
+    out[e] = s;
+  }
+}
+
+}  // namespace
+
+template <typename T, typename TO>
+void launch_xw_simt(cudaStream_t s, const T* x, index_t m, index_t n, index_t ldx, const T* w,
+                    index_t wc, index_t ldw, TO* out, index_t ors, index_t ocs, bool exact) {
+  if (m <= 0 || wc <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(m, kBM)), static_cast<unsigned>(ceil_div(wc, kBN)));
+  if (exact)
+    xw_simt_kernel<T, TO, true><<<grid, kThreads, 0, s>>>(x, m, n, ldx, w, wc, ldw, out, ors, ocs);
+  else
+    xw_simt_kernel<T, TO, false><<<grid, kThreads, 0, s>>>(x, m, n, ldx, w, wc, ldw, out, ors, ocs);
+}
+
+template <typename T>
+void launch_utx_simt(cudaStream_t s, const T* u, index_t ldu, const T* x, index_t ldx, index_t m,
+                     index_t l, index_t n, index_t chunk_rows, double* part, bool exact) {
+  const index_t chunks = ceil_div(m, chunk_rows);
+  dim3 grid(static_cast<unsigned>(ceil_div(n, kBN)), static_cast<unsigned>(ceil_div(l, kBM)),
+            static_cast<unsigned>(chunks));
+  if (exact)
+    utx_simt_kernel<T, true><<<grid, kThreads, 0, s>>>(u, ldu, x, ldx, m, l, n, chunk_rows, part);
+  else
+    utx_simt_kernel<T, false><<<grid, kThreads, 0, s>>>(u, ldu, x, ldx, m, l, n, chunk_rows, part);
+}
+
+template <typename T>
+void launch_syrk_partials(cudaStream_t s, const T* u, index_t ldu, index_t m, index_t l,
+                          index_t chunk_rows, double* part) {
+  launch_utx_simt<T>(s, u, ldu, u, ldu, m, l, l, chunk_rows, part, false);
+}
+
+void launch_reduce_partials(cudaStream_t s, const double* part, index_t nparts, index_t count,
+                            double* out) {
+  index_t g = ceil_div(count, 256);
+  if (g > 148 * 8) g = 148 * 8;
+  reduce_partials_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(part, nparts, count, out);
+}
+
+template void launch_xw_simt<float, float>(cudaStream_t, const float*, index_t, index_t, index_t,
+                                           const float*, index_t, index_t, float*, index_t, index_t, bool);
+template void launch_xw_simt<float, double>(cudaStream_t, const float*, index_t, index_t, index_t,
+                                            const float*, index_t, index_t, double*, index_t, index_t, bool);
+template void launch_xw_simt<double, double>(cudaStream_t, const double*, index_t, index_t, index_t,
+                                             const double*, index_t, index_t, double*, index_t, index_t, bool);
+template void launch_xw_simt<double, float>(cudaStream_t, const double*, index_t, index_t, index_t,
+                                            const double*, index_t, index_t, float*, index_t, index_t, bool);
+template void launch_utx_simt<float>(cudaStream_t, const float*, index_t, const float*, index_t,
+                                     index_t, index_t, index_t, index_t, double*, bool);
+template void launch_utx_simt<double>(cudaStream_t, const double*, index_t, const double*, index_t,
+                                      index_t, index_t, index_t, index_t, double*, bool);
+template void launch_syrk_partials<float>(cudaStream_t, const float*, index_t, index_t, index_t,
+                                          index_t, double*);
+template void launch_syrk_partials<double>(cudaStream_t, const double*, index_t, index_t, index_t,
+                                           index_t, double*);
+
+}  // namespace lpca

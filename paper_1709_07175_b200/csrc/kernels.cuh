@@ -1,0 +1,101 @@
+// Kernel launchers of lazypca_b200 (all sm_100a). Each names the reference
+// routine whose semantics it implements.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace lpca {
+
+// ---- projection (proj/core/src/projection.cpp:71-126) --------------------
+// Omega dense column-major n x l (ld >= n), fp64, exactly the reference's
+// per-column xoshiro256** streams.
+void launch_omega_gaussian(cudaStream_t s, index_t n, index_t l, std::uint64_t seed, double* out,
+                           index_t ld);
+// {-1, 0, +1} pattern of gen_very_sparse, dense column-major, unscaled.
+void launch_omega_very_sparse(cudaStream_t s, index_t n, index_t l, double density,
+                              std::uint64_t seed, double* out, index_t ld);
+
+// ---- synthetic data --------------------------------------------------------
+// Rows [row0, row0+m) of X = G diag(rho^t) H + noise E, row-major, dtype 4/8.
+// `sigma` holds r fp64 scale factors; scratch needs (rows_per_batch*r + r*n) doubles.
+void launch_synth_lowrank(cudaStream_t s, index_t row0, index_t m, index_t n, index_t r,
+                          const double* sigma_dev, double noise, std::uint64_t seed, int dtype,
+                          void* x, index_t ldx, double* scratch, index_t scratch_elems);
+
+// ---- elementwise / layout helpers -----------------------------------------
+// dst[c*ldd + i] = (TO) (scale * src[c*lds + i]) for i < rows, c < cols (column-major copy/convert).
+void launch_convert_f64_to_f32(cudaStream_t s, const double* src, index_t lds, float* dst,
+                               index_t ldd, index_t rows, index_t cols, double scale);
+void launch_scale_f64(cudaStream_t s, const double* src, double* dst, index_t count, double inv);
+// Split fp64 column-major W (n x w) into tf32-exact hi/lo fp32 planes [wpad][ldd]
+// (rows >= w zero-filled): hi = tf32(W), lo = tf32(W - hi).
+void launch_split_tf32_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc,
+                         index_t wpad, float* hi, float* lo, index_t ldd);
+// Densify a CSC matrix (device arrays) into row-major dtype storage.
+void launch_csc_to_dense(cudaStream_t s, index_t m, index_t n, const std::int64_t* col_ptr,
+                         const std::int64_t* row_idx, const double* vals, int dtype, void* x,
+                         index_t ldx);
+// Transpose a column-major dtype matrix into row-major.
+void launch_transpose(cudaStream_t s, int dtype, const void* src, index_t lds, index_t rows,
+                      index_t cols, void* dst, index_t ldd);
+void launch_zero(cudaStream_t s, void* p, std::size_t bytes);
+// dst (fp64, packed row-major m x n) = src (fp32 row-major, ld lds), exact widening.
+void launch_widen_f32(cudaStream_t s, const float* src, index_t lds, index_t m, index_t n, double* dst);
+
+// ---- SIMT GEMMs (FFMA / DFMA) ------------------------------------------------
+// out[i*ors + c*ocs] = sum_j X[i*ldx + j] * W[c*ldw + j]  (spmm, kernels.cpp:30-47)
+// T = float: fp32 products, fp32 sums over 256-wide K blocks, fp64 across blocks.
+// T = double, exact: mul+add in ascending j (the reference's rounding sequence).
+template <typename T, typename TO>
+void launch_xw_simt(cudaStream_t s, const T* x, index_t m, index_t n, index_t ldx, const T* w,
+                    index_t wc, index_t ldw, TO* out, index_t ors, index_t ocs, bool exact);
+// part[c][j*l + r] = sum_{i in chunk c} U[i*ldu + r] * X[i*ldx + j]  (gemm_t, kernels.cpp:70-113)
+template <typename T>
+void launch_utx_simt(cudaStream_t s, const T* u, index_t ldu, const T* x, index_t ldx, index_t m,
+                     index_t l, index_t n, index_t chunk_rows, double* part, bool exact);
+// out[idx] = sum_c part[c][idx], c ascending (fixed order; no float atomics).
+void launch_reduce_partials(cudaStream_t s, const double* part, index_t nparts, index_t count,
+                            double* out);
+
+// ---- tcgen05 split-TF32 GEMMs (fp32 data) -------------------------------------
+// out (fp32, row-major [m][ldo]) = X (fp32 row-major) * W, with W given as tf32
+// hi/lo planes [wpad][ldw]: X_hi*W_hi + X_lo*W_hi + X_hi*W_lo accumulated in TMEM.
+bool tc_xw_supported(index_t n, index_t wpad);
+void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
+                  const float* w_hi, const float* w_lo, index_t wpad, index_t ldw, float* out,
+                  index_t ldo, int num_sms);
+// part[c][j*l + r] for r < l: U^T X over row chunks with the same 3-term split.
+bool tc_utx_supported(index_t l, index_t n);
+void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, index_t ldx,
+                   index_t m, index_t l, index_t n, index_t chunk_rows, double* part,
+                   int num_sms);
+
+// ---- small fp64 kernels (the l x l step) ----------------------------------------
+// G = F F^T, F l x n column-major, bitwise symmetric (dense_aat, kernels.cpp:148-172).
+void launch_gram(cudaStream_t s, const double* f, index_t l, index_t n, double* g);
+// U^T U for tall U (m x l row-major) into chunk partials part[c][a + b*l] (full square).
+template <typename T>
+void launch_syrk_partials(cudaStream_t s, const T* u, index_t ldu, index_t m, index_t l,
+                          index_t chunk_rows, double* part);
+// Cyclic parallel Jacobi (round-robin schedule of jacobi.cpp:18-33).
+// a: l x l column-major (overwritten); evals descending; evecs column-major.
+// status[0] = 0 ok / 1 no convergence; gap[0] = last max off-diagonal.
+void launch_jacobi_eigh(cudaStream_t s, double* a, index_t l, double* evals, double* evecs,
+                        double* work, int* status, double* gap);
+// V(j,r) = (sum_i F(i,j) Ut(i,r)) / sigma_r  (truncated_svd.cpp:52-62), then the
+// canonical sign flip (truncated_svd.cpp:64-80) applied to V and Ut.
+void launch_vform(cudaStream_t s, const double* f, index_t l, index_t n, const double* ut,
+                  const double* evals, index_t k, double* sigma, double* v);
+void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* ut, index_t l);
+// Cholesky of an SPD l x l (lower L, column-major), then R^{-1} = L^{-T} (upper).
+// status[0] = pivot index + 1 on failure (pivot tol 1e-14 * max diag,
+// lazy_projector.cpp:12-37).
+void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
+                         int* status);
+// F <- L^{-1} F  ==  (Z R^{-1})^T for Z = F^T; rinv = L^{-T} upper, F l x n col-major.
+void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
+                         double* tmp);
+
+}  // namespace lpca

@@ -1,0 +1,1126 @@
+// Host orchestration and C ABI of lazypca_b200.
+//
+// The reducers below mirror proj/core/src/reducer.cpp step for step — config
+// resolution (:137-161), Omega regeneration (:128-130), sketch (:163-169),
+// F formation (:216-234 Lazy, :192-214 SPCA), finish_spectral (:75-90) with
+// truncated_svd_via_gram (truncated_svd.cpp:13-82), apply_map (:348-353) —
+// with every numeric phase a device kernel on the context's stream and the
+// row-sharded exchange (q+1 fp64 allreduces of n x l) done with NCCL.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/lazypca_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using lpca::Error;
+using lpca::index_t;
+
+namespace {
+
+thread_local std::string g_err_msg;
+thread_local std::int64_t g_err_index = -1;
+thread_local double g_err_gap = 0.0;
+
+template <typename F>
+lpca_status guarded(F&& fn) {
+  try {
+    fn();
+    return LPCA_OK;
+  } catch (const Error& e) {
+    g_err_msg = e.what();
+    g_err_index = e.index;
+    g_err_gap = e.gap;
+    return static_cast<lpca_status>(e.code);
+  } catch (const std::exception& e) {
+    g_err_msg = e.what();
+    g_err_index = -1;
+    return LPCA_ERR_INTERNAL;
+  }
+}
+
+// NCCL is resolved at run time, only when a context spans more than one rank:
+// the process may already hold torch's bundled libnccl.so.2 (same soname,
+// newer symbols), which must win over the system copy. Types come from nccl.h.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  if (loaded) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h && std::getenv("LPCA_NCCL_PATH")) h = dlopen(std::getenv("LPCA_NCCL_PATH"), RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+  if (!h) throw Error(lpca::kNccl, std::string("cannot load libnccl.so.2: ") + dlerror());
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy || !api.error_string)
+    throw Error(lpca::kNccl, "libnccl.so.2 lacks a required symbol");
+  loaded = true;
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(lpca::kNccl, std::string(what) + ": " + nccl().error_string(r));
+}
+
+std::string S(index_t v) { return std::to_string(v); }
+
+}  // namespace
+
+struct lpca_ctx {
+  int device = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  int gemm_path = 0;  // 0 = tcgen05 split-TF32 for fp32 data, 1 = SIMT
+  int exact = 0;      // fp64 reference summation order (tests)
+  std::int64_t launches = 0;
+  std::unordered_map<std::string, std::pair<void*, std::size_t>> ws;
+  cudaEvent_t ev[12] = {};
+
+  void note_launch(int n = 1) { launches += n; }
+
+  void* buf(const std::string& name, std::size_t bytes) {
+    auto it = ws.find(name);
+    if (it != ws.end() && it->second.second >= bytes) return it->second.first;
+    if (it != ws.end()) {
+      LPCA_CUDA(cudaStreamSynchronize(stream));
+      LPCA_CUDA(cudaFree(it->second.first));
+      ws.erase(it);
+    }
+    void* p = nullptr;
+    LPCA_CUDA(cudaMalloc(&p, bytes < 256 ? 256 : bytes));
+    ws[name] = {p, bytes};
+    return p;
+  }
+  template <typename T>
+  T* get(const std::string& name, std::size_t count) {
+    return static_cast<T*>(buf(name, count * sizeof(T)));
+  }
+  void allreduce(double* p, index_t count) {
+    if (world <= 1) return;
+    nccl_check(nccl().all_reduce(p, p, static_cast<std::size_t>(count), ncclDouble, ncclSum, comm, stream),
+               "ncclAllReduce");
+  }
+};
+
+struct lpca_map {
+  int device = 0;
+  int method = LPCA_LAZY_SPCA;
+  index_t k = 0, l = 0, n = 0;
+  std::uint64_t seed = 0;
+  double density = 1.0, scale = 1.0;
+  double* v = nullptr;  // device, n x k column-major fp64
+  std::vector<double> sigma;
+  ~lpca_map() {
+    if (v) cudaFree(v);
+  }
+};
+
+namespace {
+
+using namespace lpca;
+
+// ---- configuration (ReducerConfig::resolved, reducer.cpp:137-161;
+//      ProjectionSpec::validate, projection.cpp:52-60) ----------------------
+lpca_config resolve(const lpca_config& in, index_t data_cols) {
+  lpca_config out = in;
+  if (out.k < 1) throw Error(kInvalidArgument, "reducer: k must be at least 1, got " + S(out.k));
+  if (out.l == 0) out.l = out.k;
+  if (out.k > out.l)
+    throw Error(kInvalidArgument,
+                "reducer: k = " + S(out.k) + " exceeds sketch width l = " + S(out.l));
+  if (out.method == LPCA_RP && out.k != out.l)
+    throw Error(kInvalidArgument,
+                "reducer: random projection reduces straight to k dimensions; l must equal k");
+  if (out.block_rows > 0) out.streaming = 1;
+  if (out.streaming && out.block_rows < 1)
+    throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
+  if (out.proj_n == 0) out.proj_n = data_cols;
+  if (out.proj_l == 0) out.proj_l = out.l;
+  if (out.proj_n != data_cols)
+    throw Error(kDimension, "reducer: projection is built for n = " + S(out.proj_n) +
+                                " but the data has " + S(data_cols) + " columns");
+  if (out.proj_l != out.l)
+    throw Error(kDimension, "reducer: projection width " + S(out.proj_l) +
+                                " does not match l = " + S(out.l));
+  if (out.proj_l < 2)
+    throw Error(kInvalidArgument,
+                "projection: sketch width l must be at least 2, got " + S(out.proj_l));
+  if (out.proj_l > out.proj_n)
+    throw Error(kInvalidArgument, "projection: sketch width l = " + S(out.proj_l) +
+                                      " exceeds data dimensionality n = " + S(out.proj_n));
+  if (!(out.density > 0.0) || out.density > 1.0)
+    throw Error(kInvalidArgument,
+                "projection: density must lie in (0, 1], got " + std::to_string(out.density));
+  if (out.power_iters < 0) throw Error(kInvalidArgument, "reducer: power_iters must be >= 0");
+  if (out.method != LPCA_RP && out.method != LPCA_SPCA && out.method != LPCA_LAZY_SPCA)
+    throw Error(kInvalidArgument, "unknown method");
+  return out;
+}
+
+double projection_scale(const lpca_config& c) {
+  return c.projection_kind == LPCA_GAUSSIAN ? std::sqrt(static_cast<double>(c.proj_l))
+                                            : std::sqrt(static_cast<double>(c.proj_l) * c.density);
+}
+
+void check_ctx(lpca_ctx* ctx) {
+  if (!ctx) throw Error(kInvalidArgument, "null context");
+  LPCA_CUDA(cudaSetDevice(ctx->device));
+}
+
+// ---- device-resident X ------------------------------------------------------
+struct DevX {
+  const void* p = nullptr;
+  int dtype = 8;
+  index_t m = 0, n = 0, ld = 0;
+};
+
+std::size_t dsize(int dtype) { return dtype == 4 ? 4 : 8; }
+
+void check_view(const lpca_matrix_view* x) {
+  if (!x) throw Error(kInvalidArgument, "null matrix view");
+  if (x->dtype != LPCA_F32 && x->dtype != LPCA_F64)
+    throw Error(kInvalidArgument, "matrix view: dtype must be LPCA_F32 or LPCA_F64");
+  if (x->rows < 0 || x->cols < 0)
+    throw Error(kInvalidArgument, "sparse matrix dimensions must be non-negative");
+  if (x->layout == LPCA_CSC) {
+    if (x->location != LPCA_HOST) throw Error(kInvalidArgument, "CSC views must be host memory");
+    if (!x->col_ptr || (x->nnz > 0 && (!x->row_idx || !x->data)))
+      throw Error(kInvalidArgument, "CSC view: missing arrays");
+  } else if (x->layout != LPCA_ROW_MAJOR && x->layout != LPCA_COL_MAJOR) {
+    throw Error(kInvalidArgument, "matrix view: unknown layout");
+  } else if (!x->data && x->rows * x->cols > 0) {
+    throw Error(kInvalidArgument, "matrix view: null data");
+  }
+}
+
+// Brings any view to a row-major device matrix of its own dtype. Host data is
+// copied with one cudaMemcpyAsync per contiguous range; a column-major or CSC
+// view is transposed / densified by a kernel after upload.
+DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes) {
+  check_view(x);
+  DevX d;
+  d.m = x->rows;
+  d.n = x->cols;
+  d.dtype = x->dtype;
+  const std::size_t es = dsize(x->dtype);
+  if (d.m == 0 || d.n == 0) {
+    d.p = ctx.buf(slot, es);
+    d.ld = d.n > 0 ? d.n : 1;
+    return d;
+  }
+  if (x->layout == LPCA_CSC) {
+    const index_t nnz = x->nnz;
+    // canonical-form checks of SparseMatrix::from_csc (sparse_matrix.cpp:50-80)
+    if (x->col_ptr[0] != 0) throw Error(kInvalidArgument, "csc: col_ptr[0] must be 0");
+    if (x->col_ptr[x->cols] != nnz) throw Error(kDimension, "csc: col_ptr[cols] must equal nnz");
+    std::vector<double> vals(static_cast<std::size_t>(nnz));
+    for (index_t j = 0; j < x->cols; ++j) {
+      const index_t lo = x->col_ptr[j], hi = x->col_ptr[j + 1];
+      if (hi < lo) throw Error(kInvalidArgument, "csc: col_ptr must be non-decreasing");
+      for (index_t p = lo; p < hi; ++p) {
+        const index_t r = x->row_idx[p];
+        if (r < 0 || r >= x->rows)
+          throw Error(kDimension, "csc: row index out of range in column " + S(j));
+        if (p > lo && r <= x->row_idx[p - 1])
+          throw Error(kInvalidArgument, "csc: row indices must be strictly increasing in column " + S(j));
+        const double v = x->dtype == 4 ? static_cast<const float*>(x->data)[p]
+                                       : static_cast<const double*>(x->data)[p];
+        if (v == 0.0) throw Error(kInvalidArgument, "csc: explicit zero stored in column " + S(j));
+        if (!std::isfinite(v)) throw Error(kInvalidArgument, "csc: non-finite value in column " + S(j));
+        vals[static_cast<std::size_t>(p)] = v;
+      }
+    }
+    auto* cp = ctx.get<std::int64_t>(std::string(slot) + ".ptr", x->cols + 1);
+    auto* ri = ctx.get<std::int64_t>(std::string(slot) + ".idx", nnz > 0 ? nnz : 1);
+    auto* vv = ctx.get<double>(std::string(slot) + ".val", nnz > 0 ? nnz : 1);
+    LPCA_CUDA(cudaMemcpyAsync(cp, x->col_ptr, sizeof(std::int64_t) * (x->cols + 1),
+                              cudaMemcpyHostToDevice, ctx.stream));
+    if (nnz > 0) {
+      LPCA_CUDA(cudaMemcpyAsync(ri, x->row_idx, sizeof(std::int64_t) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+      LPCA_CUDA(cudaMemcpyAsync(vv, vals.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+    }
+    void* dst = ctx.buf(slot, es * d.m * d.n);
+    launch_zero(ctx.stream, dst, es * d.m * d.n);
+    launch_csc_to_dense(ctx.stream, d.m, d.n, cp, ri, vv, d.dtype, dst, d.n);
+    LPCA_LAUNCHED(ctx);
+    // the staged host vectors must outlive the async copies
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz * (8 + 8) + (x->cols + 1) * 8);
+    d.p = dst;
+    d.ld = d.n;
+    return d;
+  }
+  const bool row = x->layout == LPCA_ROW_MAJOR;
+  const index_t ld = x->ld > 0 ? x->ld : (row ? x->cols : x->rows);
+  if (x->location == LPCA_DEVICE && row) {
+    d.p = x->data;
+    d.ld = ld;
+    return d;
+  }
+  const void* src_dev = x->data;
+  index_t src_ld = ld;
+  if (x->location == LPCA_HOST) {
+    const index_t outer = row ? x->rows : x->cols, inner = row ? x->cols : x->rows;
+    void* dst = ctx.buf(row ? std::string(slot) : std::string(slot) + ".cm", es * outer * inner);
+    LPCA_CUDA(cudaMemcpy2DAsync(dst, es * inner, x->data, es * ld, es * inner, outer,
+                                cudaMemcpyHostToDevice, ctx.stream));
+    if (h2d_bytes) *h2d_bytes += static_cast<double>(es * outer * inner);
+    if (row) {
+      d.p = dst;
+      d.ld = inner;
+      return d;
+    }
+    src_dev = dst;
+    src_ld = inner;
+  }
+  void* dst = ctx.buf(slot, es * d.m * d.n);
+  launch_transpose(ctx.stream, d.dtype, src_dev, src_ld, d.m, d.n, dst, d.n);
+  LPCA_LAUNCHED(ctx);
+  d.p = dst;
+  d.ld = d.n;
+  return d;
+}
+
+// ---- GEMM dispatch ------------------------------------------------------------
+// Which engine runs an fp32 X-pass: tcgen05 split-TF32 when the path is
+// selected and the shape is supported, SIMT FFMA otherwise.
+bool use_tc(const lpca_ctx& ctx, const DevX& x, index_t w) {
+  return ctx.gemm_path == 0 && x.dtype == 4 && tc_xw_supported(x.n, round_up(w, 16)) &&
+         x.ld % 4 == 0;
+}
+
+// out (T row-major [m][ldo]) = X W, W fp64 column-major (n x wc, ld ldw).
+// For fp32 X the operand is prepared once per call (rounded, or tf32 hi/lo).
+void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, void* out,
+             index_t ldo, bool exact) {
+  const index_t m = x.m, n = x.n;
+  if (x.dtype == 8) {
+    launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, w, wc,
+                                   ldw, static_cast<double*>(out), ldo, 1, exact);
+    LPCA_LAUNCHED(ctx);
+    return;
+  }
+  if (use_tc(ctx, x, wc)) {
+    const index_t wpad = round_up(wc, 16);
+    float* hi = ctx.get<float>("w.hi", wpad * n);
+    float* lo = ctx.get<float>("w.lo", wpad * n);
+    launch_split_tf32_w(ctx.stream, w, ldw, n, wc, wpad, hi, lo, n);
+    LPCA_LAUNCHED(ctx);
+    launch_xw_tc(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, hi, lo, wpad, n,
+                 static_cast<float*>(out), ldo, ctx.num_sms);
+    LPCA_LAUNCHED(ctx);
+    return;
+  }
+  float* w32 = ctx.get<float>("w.f32", wc * n);
+  launch_convert_f64_to_f32(ctx.stream, w, ldw, w32, n, n, wc, 1.0);
+  LPCA_LAUNCHED(ctx);
+  launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, w32, wc, n,
+                               static_cast<float*>(out), ldo, 1, false);
+  LPCA_LAUNCHED(ctx);
+}
+
+index_t pick_chunks(const lpca_ctx& ctx, index_t m, index_t tiles, bool exact) {
+  if (exact || m <= 0) return 1;
+  index_t chunks = ceil_div(4 * ctx.num_sms, tiles > 0 ? tiles : 1);
+  const index_t max_chunks = ceil_div(m, 2048);
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  return chunks;
+}
+
+// F (l x n column-major fp64) = U^T X summed over this rank's rows, then
+// allreduced over ranks. U is T row-major [m][ldu].
+void utx_pass(lpca_ctx& ctx, const DevX& x, const void* u, index_t ldu, index_t l, double* f,
+              bool exact) {
+  const index_t m = x.m, n = x.n;
+  if (m == 0) {
+    launch_zero(ctx.stream, f, sizeof(double) * l * n);
+    ctx.allreduce(f, l * n);
+    return;
+  }
+  const bool tc = x.dtype == 4 && ctx.gemm_path == 0 && tc_utx_supported(l, n) && ldu % 4 == 0 &&
+                  x.ld % 4 == 0;
+  const index_t tiles = tc ? ceil_div(n, 256) : ceil_div(n, 64) * ceil_div(l, 64);
+  index_t chunks = pick_chunks(ctx, m, tiles, exact);
+  index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
+  chunks = ceil_div(m, chunk_rows);
+  double* part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+  if (tc) {
+    launch_utx_tc(ctx.stream, static_cast<const float*>(u), ldu, static_cast<const float*>(x.p),
+                  x.ld, m, l, n, chunk_rows, part, ctx.num_sms);
+  } else if (x.dtype == 4) {
+    launch_utx_simt<float>(ctx.stream, static_cast<const float*>(u), ldu,
+                           static_cast<const float*>(x.p), x.ld, m, l, n, chunk_rows, part, false);
+  } else {
+    launch_utx_simt<double>(ctx.stream, static_cast<const double*>(u), ldu,
+                            static_cast<const double*>(x.p), x.ld, m, l, n, chunk_rows, part, exact);
+  }
+  LPCA_LAUNCHED(ctx);
+  if (chunks > 1) {
+    launch_reduce_partials(ctx.stream, part, chunks, l * n, f);
+    LPCA_LAUNCHED(ctx);
+  }
+  ctx.allreduce(f, l * n);
+}
+
+// CholeskyQR step on a wide F (l x n, F = Z^T): F <- L^{-1} F with
+// L L^T = F F^T. Returns the failing pivot (+1) or 0.
+void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
+  double* g = ctx.get<double>("orth.g", l * l);
+  double* w = ctx.get<double>("orth.w", l * l);
+  double* lm = ctx.get<double>("orth.l", l * l);
+  double* tmp = ctx.get<double>("orth.tmp", l * n);
+  int* st = ctx.get<int>("orth.status", 1);
+  for (int pass = 0; pass < 2; ++pass) {
+    launch_gram(ctx.stream, f, l, n, g);
+    LPCA_LAUNCHED(ctx);
+    launch_chol_inverse(ctx.stream, g, l, w, lm, st);
+    LPCA_LAUNCHED(ctx);
+    int h = 0;
+    LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (h != 0)
+      throw Error(kRankDeficiency, "power iteration: cholesky pivot " + S(h - 1) +
+                                       " is not positive definite", h - 1);
+    launch_apply_rinv_t(ctx.stream, w, l, f, n, tmp);
+    LPCA_LAUNCHED(ctx);
+  }
+}
+
+struct PhaseEvents {
+  lpca_ctx& ctx;
+  explicit PhaseEvents(lpca_ctx& c) : ctx(c) {
+    for (auto& e : ctx.ev)
+      if (!e) LPCA_CUDA(cudaEventCreate(&e));
+  }
+  void mark(int i) { LPCA_CUDA(cudaEventRecord(ctx.ev[i], ctx.stream)); }
+  double secs(int a, int b) {
+    float ms = 0.f;
+    LPCA_CUDA(cudaEventElapsedTime(&ms, ctx.ev[a], ctx.ev[b]));
+    return ms * 1e-3;
+  }
+};
+
+void regenerate_dev(lpca_ctx& ctx, const lpca_config& c, double* omega) {
+  if (c.projection_kind == LPCA_GAUSSIAN)
+    launch_omega_gaussian(ctx.stream, c.proj_n, c.proj_l, c.seed, omega, c.proj_n);
+  else
+    launch_omega_very_sparse(ctx.stream, c.proj_n, c.proj_l, c.density, c.seed, omega, c.proj_n);
+  LPCA_LAUNCHED(ctx);
+}
+
+// truncated_svd_via_gram on a device F (l x n). Fills v (n x k), sigma (host),
+// and optionally u~ (device, l x k). Throws the reference's errors.
+void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index_t k, double* v,
+                     std::vector<double>& sigma, double* ut_out) {
+  if (l > n)
+    throw Error(kDimension, "truncated_svd_via_gram: F must be wide (l <= n), got " + S(l) + "x" + S(n));
+  if (k < 1 || k > l)
+    throw Error(kInvalidArgument, "truncated_svd_via_gram: need 1 <= k <= l, got k = " + S(k));
+  double* g = ctx.get<double>("svd.g", l * l);
+  double* evals = ctx.get<double>("svd.evals", l);
+  double* evecs = ctx.get<double>("svd.evecs", l * l);
+  double* work = ctx.get<double>("svd.work", 2 * l * l);
+  int* st = ctx.get<int>("svd.status", 2);
+  double* gap = ctx.get<double>("svd.gap", 1);
+  launch_gram(ctx.stream, f, l, n, g);
+  LPCA_LAUNCHED(ctx);
+  launch_jacobi_eigh(ctx.stream, g, l, evals, evecs, work, st, gap);
+  LPCA_LAUNCHED(ctx);
+  launch_vform(ctx.stream, f, l, n, evecs, evals, k, nullptr, v);
+  LPCA_LAUNCHED(ctx);
+  launch_sign_canon(ctx.stream, v, n, k, evecs, l);
+  LPCA_LAUNCHED(ctx);
+  if (ut_out) {
+    LPCA_CUDA(cudaMemcpyAsync(ut_out, evecs, sizeof(double) * l * k, cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+  std::vector<double> lam(static_cast<std::size_t>(l));
+  int hst = 0;
+  double hgap = 0.0;
+  LPCA_CUDA(cudaMemcpyAsync(lam.data(), evals, sizeof(double) * l, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaMemcpyAsync(&hgap, gap, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (hst == 2)
+    throw Error(kInvalidArgument, "eigh: input is not symmetric (max |a_ij - a_ji| = " +
+                                      std::to_string(hgap) + ")");
+  if (hst == 1)
+    throw Error(kConvergence, "eigh: Jacobi off-diagonal " + std::to_string(hgap) +
+                                  " still above tolerance after 50 sweeps", -1, hgap);
+  // rank floor (truncated_svd.cpp:28-39)
+  const double lambda_max = lam.front();
+  const double floor = 1e-12 * (lambda_max > 0.0 ? lambda_max : 0.0);
+  index_t safe = 0;
+  while (safe < l && lam[static_cast<std::size_t>(safe)] > floor && lam[static_cast<std::size_t>(safe)] > 0.0)
+    ++safe;
+  if (k > safe)
+    throw Error(kRankDeficiency, "truncated_svd_via_gram: requested rank " + S(k) +
+                                     " exceeds the numerical rank; largest safe k = " + S(safe),
+                safe);
+  sigma.resize(static_cast<std::size_t>(k));
+  for (index_t r = 0; r < k; ++r) sigma[static_cast<std::size_t>(r)] = std::sqrt(lam[static_cast<std::size_t>(r)]);
+}
+
+struct FitResult {
+  lpca_map* map = nullptr;
+};
+
+// The fit pipeline on a device-resident X (this rank's rows).
+lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_timings* t) {
+  const lpca_config c = resolve(cfg_in, x.n);
+  if (c.streaming)
+    throw Error(kInvalidArgument,
+                "streaming reducers take a row-block stream; use block_rows = 0 for in-core data");
+  PhaseEvents ev(ctx);
+  ev.mark(0);
+  const index_t n = x.n, l = c.l, k = c.k, m = x.m;
+  auto map = new lpca_map();
+  map->device = ctx.device;
+  map->method = c.method;
+  map->k = k;
+  map->l = l;
+  map->n = n;
+  map->seed = c.seed;
+  map->density = c.density;
+  map->scale = projection_scale(c);
+  try {
+    LPCA_CUDA(cudaMalloc(&map->v, sizeof(double) * (n * k > 0 ? n * k : 1)));
+    double* omega = ctx.get<double>("omega", n * l);
+    regenerate_dev(ctx, c, omega);
+    if (c.method == LPCA_RP) {
+      launch_scale_f64(ctx.stream, omega, map->v, n * k, 1.0 / map->scale);
+      LPCA_LAUNCHED(ctx);
+      ev.mark(1);
+      LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+      if (t) {
+        t->sketch += ev.secs(0, 1);
+        t->total += ev.secs(0, 1);
+      }
+      return map;
+    }
+    const bool exact = ctx.exact != 0 && x.dtype == 8;
+    const index_t ldu = round_up(l, 16);
+    void* u = ctx.buf("u", dsize(x.dtype) * (m > 0 ? m : 1) * ldu);
+    // sketch U = X Omega (reducer.cpp:163-169)
+    if (m > 0) xw_pass(ctx, x, omega, l, n, u, ldu, exact);
+    ev.mark(1);
+    // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
+    double* f = ctx.get<double>("f", l * n);
+    if (c.power_iters > 0) {
+      double* z = ctx.get<double>("z.w", l * n);
+      for (int it = 0; it < c.power_iters; ++it) {
+        utx_pass(ctx, x, u, ldu, l, f, exact);       // F = U^T X  (= Z^T)
+        orth_rows(ctx, f, l, n);                     // Z <- orth(Z)
+        launch_transpose(ctx.stream, 8, f, l, l, n, z, n);  // W = Z as n x l column-major
+        LPCA_LAUNCHED(ctx);
+        if (m > 0) xw_pass(ctx, x, z, l, n, u, ldu, exact);  // U = X Z
+      }
+    }
+    ev.mark(2);
+    if (c.method == LPCA_SPCA) {
+      // CholeskyQR2 of U (the reference uses Householder QR, qr.cpp:104-132;
+      // Q is the same up to roundoff once R's diagonal is made positive).
+      double* gpart = nullptr;
+      double* gu = ctx.get<double>("spca.g", l * l);
+      double* w = ctx.get<double>("spca.w", l * l);
+      double* lm = ctx.get<double>("spca.l", l * l);
+      int* st = ctx.get<int>("spca.status", 1);
+      for (int pass = 0; pass < 2; ++pass) {
+        if (m > 0) {
+          index_t chunks = pick_chunks(ctx, m, ceil_div(l, 64) * ceil_div(l, 64), exact);
+          index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
+          chunks = ceil_div(m, chunk_rows);
+          gpart = chunks == 1 ? gu : ctx.get<double>("spca.gpart", chunks * l * l);
+          if (x.dtype == 4)
+            launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u), ldu, m, l, chunk_rows, gpart);
+          else
+            launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u), ldu, m, l, chunk_rows, gpart);
+          LPCA_LAUNCHED(ctx);
+          if (chunks > 1) {
+            launch_reduce_partials(ctx.stream, gpart, chunks, l * l, gu);
+            LPCA_LAUNCHED(ctx);
+          }
+        } else {
+          launch_zero(ctx.stream, gu, sizeof(double) * l * l);
+        }
+        ctx.allreduce(gu, l * l);
+        launch_chol_inverse(ctx.stream, gu, l, w, lm, st);
+        LPCA_LAUNCHED(ctx);
+        int h = 0;
+        LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (h != 0)
+          throw Error(kRankDeficiency, "qr: column " + S(h - 1) +
+                                           " is numerically dependent on earlier columns", h - 1);
+        if (m > 0) {
+          // Q = U R^{-1}: the sketch GEMM with X := U (m x l) and W := R^{-1}
+          DevX ux{u, x.dtype, m, l, ldu};
+          void* q = ctx.buf("q", dsize(x.dtype) * m * ldu);
+          if (x.dtype == 8) {
+            launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(u), m, l, ldu, w,
+                                           l, l, static_cast<double*>(q), ldu, 1, exact);
+          } else {
+            float* w32 = ctx.get<float>("spca.w32", l * l);
+            launch_convert_f64_to_f32(ctx.stream, w, l, w32, l, l, l, 1.0);
+            LPCA_LAUNCHED(ctx);
+            launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(u), m, l, ldu, w32,
+                                         l, l, static_cast<float*>(q), ldu, 1, false);
+          }
+          LPCA_LAUNCHED(ctx);
+          (void)ux;
+          LPCA_CUDA(cudaMemcpyAsync(u, q, dsize(x.dtype) * m * ldu, cudaMemcpyDeviceToDevice, ctx.stream));
+        }
+      }
+    }
+    ev.mark(3);
+    utx_pass(ctx, x, u, ldu, l, f, exact);  // F = U^T X (or Q^T X)
+    ev.mark(4);
+    finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
+    ev.mark(5);
+    LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
+    if (t) {
+      t->sketch += ev.secs(0, 1);
+      t->power += ev.secs(1, 2);
+      t->qr += ev.secs(2, 3);
+      t->f_form += ev.secs(3, 4);
+      t->svd += ev.secs(4, 5);
+      t->total += ev.secs(0, 5);
+    }
+    return map;
+  } catch (...) {
+    delete map;
+    throw;
+  }
+}
+
+// Y = X V into a caller buffer (apply_map, reducer.cpp:348-353).
+void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, int y_dtype,
+                   int y_layout, int y_location, index_t ldy, lpca_timings* t, double* d2h) {
+  if (x.n != map.n)
+    throw Error(kDimension, "apply_map: data has " + S(x.n) + " columns but the map expects " + S(map.n));
+  if (y_dtype != LPCA_F32 && y_dtype != LPCA_F64) throw Error(kInvalidArgument, "transform: bad y dtype");
+  if (y_layout != LPCA_ROW_MAJOR && y_layout != LPCA_COL_MAJOR)
+    throw Error(kInvalidArgument, "transform: bad y layout");
+  const index_t m = x.m, k = map.k;
+  const bool row = y_layout == LPCA_ROW_MAJOR;
+  if (ldy <= 0) ldy = row ? k : m;
+  PhaseEvents ev(ctx);
+  ev.mark(6);
+  if (m > 0 && k > 0) {
+    const std::size_t ybytes = dsize(y_dtype) * static_cast<std::size_t>(row ? m * ldy : k * ldy);
+    void* ydev = y_location == LPCA_DEVICE ? y : ctx.buf("y", ybytes);
+    const index_t ors = row ? ldy : 1, ocs = row ? 1 : ldy;
+    if (x.dtype == 8) {
+      if (y_dtype == 8)
+        launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
+                                       map.v, k, map.n, static_cast<double*>(ydev), ors, ocs, ctx.exact != 0);
+      else
+        launch_xw_simt<double, float>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
+                                      map.v, k, map.n, static_cast<float*>(ydev), ors, ocs, ctx.exact != 0);
+      LPCA_LAUNCHED(ctx);
+    } else if (row && y_dtype == 4 && use_tc(ctx, x, k)) {
+      xw_pass(ctx, x, map.v, k, map.n, ydev, ldy, false);
+    } else {
+      float* w32 = ctx.get<float>("v.f32", k * x.n);
+      launch_convert_f64_to_f32(ctx.stream, map.v, map.n, w32, x.n, x.n, k, 1.0);
+      LPCA_LAUNCHED(ctx);
+      if (y_dtype == 4)
+        launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(x.p), m, x.n, x.ld, w32,
+                                     k, x.n, static_cast<float*>(ydev), ors, ocs, false);
+      else
+        launch_xw_simt<float, double>(ctx.stream, static_cast<const float*>(x.p), m, x.n, x.ld, w32,
+                                      k, x.n, static_cast<double*>(ydev), ors, ocs, false);
+      LPCA_LAUNCHED(ctx);
+    }
+    ev.mark(7);
+    if (y_location == LPCA_HOST) {
+      LPCA_CUDA(cudaMemcpyAsync(y, ydev, ybytes, cudaMemcpyDeviceToHost, ctx.stream));
+      if (d2h) *d2h += static_cast<double>(ybytes);
+    }
+  } else {
+    ev.mark(7);
+  }
+  ev.mark(8);
+  LPCA_CUDA(cudaEventSynchronize(ctx.ev[8]));
+  if (t) {
+    t->transform += ev.secs(6, 7);
+    t->d2h += ev.secs(7, 8);
+  }
+}
+
+int num_sms_of(int device) {
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
+}
+
+}  // namespace
+
+// ============================== C ABI =========================================
+extern "C" {
+
+const char* lpca_last_error(void) { return g_err_msg.c_str(); }
+int64_t lpca_last_error_index(void) { return g_err_index; }
+double lpca_last_error_gap(void) { return g_err_gap; }
+int32_t lpca_abi_version(void) { return LPCA_ABI_VERSION; }
+
+lpca_status lpca_ctx_create(int32_t device, lpca_ctx** out) {
+  return lpca_ctx_create_dist(device, 0, 1, nullptr, out);
+}
+
+lpca_status lpca_nccl_unique_id(void* out_128_bytes) {
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(out_128_bytes, &id, sizeof(id));
+  });
+}
+
+lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
+                                 const void* nccl_id_128, lpca_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalidArgument, "null output");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) throw Error(kInvalidArgument, "bad rank/world");
+    int count = 0;
+    LPCA_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      throw Error(kCuda, "device " + std::to_string(device) + " not present (" + std::to_string(count) + " visible)");
+    cudaDeviceProp prop;
+    LPCA_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw Error(kCuda, "lazypca_b200 needs an sm_100 (B200) device; found sm_" +
+                             std::to_string(prop.major) + std::to_string(prop.minor));
+    LPCA_CUDA(cudaSetDevice(device));
+    auto ctx = new lpca_ctx();
+    ctx->device = device;
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->num_sms = num_sms_of(device);
+    const char* path = std::getenv("LPCA_GEMM_PATH");
+    if (path && std::string(path) == "simt") ctx->gemm_path = 1;
+    try {
+      LPCA_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+      ctx->stream = ctx->own_stream;
+      if (world > 1) {
+        if (!nccl_id_128) throw Error(kInvalidArgument, "world > 1 needs an NCCL unique id");
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id_128, sizeof(id));
+        nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+      }
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+lpca_status lpca_ctx_destroy(lpca_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->ws) cudaFree(kv.second.first);
+    for (auto& e : ctx->ev)
+      if (e) cudaEventDestroy(e);
+    if (ctx->comm) nccl().comm_destroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+lpca_status lpca_ctx_set_stream(lpca_ctx* ctx, void* cuda_stream) {
+  return guarded([&] {
+    check_ctx(ctx);
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  });
+}
+
+lpca_status lpca_ctx_synchronize(lpca_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lpca_status lpca_ctx_set_gemm_path(lpca_ctx* ctx, int32_t path) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (path != 0 && path != 1) throw Error(kInvalidArgument, "gemm path must be 0 (tcgen05) or 1 (simt)");
+    ctx->gemm_path = path;
+  });
+}
+
+lpca_status lpca_ctx_set_exact_order(lpca_ctx* ctx, int32_t exact) {
+  return guarded([&] {
+    check_ctx(ctx);
+    ctx->exact = exact != 0;
+  });
+}
+
+int64_t lpca_ctx_launch_count(const lpca_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+lpca_status lpca_config_resolve(const lpca_config* in, int64_t data_cols, lpca_config* out) {
+  return guarded([&] {
+    if (!in || !out) throw Error(kInvalidArgument, "null config");
+    *out = resolve(*in, data_cols);
+  });
+}
+
+lpca_status lpca_density_for(int32_t mode, int64_t k, double value, double* out) {
+  return guarded([&] {
+    if (k < 2) throw Error(kInvalidArgument, "density policy: k must be at least 2, got " + S(k));
+    double d;
+    switch (mode) {
+      case LPCA_DENSITY_AGGRESSIVE: d = std::log(static_cast<double>(k)) / static_cast<double>(k); break;
+      case LPCA_DENSITY_CONSERVATIVE: d = 1.0 / std::sqrt(static_cast<double>(k)); break;
+      case LPCA_DENSITY_EXPLICIT: d = value; break;
+      default: d = 1.0;
+    }
+    if (d > 1.0) d = 1.0;
+    if (!(d > 0.0)) throw Error(kInvalidArgument, "density policy: derived density is not positive");
+    *out = d;
+  });
+}
+
+lpca_status lpca_regenerate(lpca_ctx* ctx, int32_t kind, int64_t n, int64_t l, double density,
+                            uint64_t seed, void* out, int32_t out_location, double* scale) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (l < 2) throw Error(kInvalidArgument, "projection: sketch width l must be at least 2, got " + S(l));
+    if (l > n)
+      throw Error(kInvalidArgument, "projection: sketch width l = " + S(l) +
+                                        " exceeds data dimensionality n = " + S(n));
+    if (!(density > 0.0) || density > 1.0)
+      throw Error(kInvalidArgument, "projection: density must lie in (0, 1], got " + std::to_string(density));
+    lpca_config c{};
+    c.projection_kind = kind;
+    c.proj_n = n;
+    c.proj_l = l;
+    c.density = density;
+    c.seed = seed;
+    double* dst = out_location == LPCA_DEVICE ? static_cast<double*>(out) : ctx->get<double>("regen", n * l);
+    regenerate_dev(*ctx, c, dst);
+    if (out_location != LPCA_DEVICE)
+      LPCA_CUDA(cudaMemcpyAsync(out, dst, sizeof(double) * n * l, cudaMemcpyDeviceToHost, ctx->stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (scale) *scale = projection_scale(c);
+  });
+}
+
+lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_view* x,
+                     lpca_map** out_map, lpca_timings* timings) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!cfg || !out_map) throw Error(kInvalidArgument, "null argument");
+    *out_map = nullptr;
+    PhaseEvents ev(*ctx);
+    ev.mark(9);
+    double h2d = 0.0;
+    const DevX dx = stage_x(*ctx, x, "x", &h2d);
+    ev.mark(10);
+    *out_map = fit_dev(*ctx, *cfg, dx, timings);
+    if (timings) timings->h2d += ev.secs(9, 10);
+  });
+}
+
+lpca_status lpca_transform(lpca_ctx* ctx, const lpca_map* map, const lpca_matrix_view* x, void* y,
+                           int32_t y_dtype, int32_t y_layout, int32_t y_location, int64_t ldy,
+                           lpca_timings* timings) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!map) throw Error(kInvalidArgument, "null map");
+    if (!y && x && x->rows > 0 && map->k > 0) throw Error(kInvalidArgument, "null output");
+    PhaseEvents ev(*ctx);
+    ev.mark(9);
+    const DevX dx = stage_x(*ctx, x, "x", nullptr);
+    ev.mark(10);
+    transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
+    if (timings) timings->h2d += ev.secs(9, 10);
+  });
+}
+
+lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_view* x,
+                               lpca_map** out_map, void* y, int32_t y_dtype, int32_t y_layout,
+                               int32_t y_location, int64_t ldy, lpca_timings* timings) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!cfg || !out_map) throw Error(kInvalidArgument, "null argument");
+    *out_map = nullptr;
+    PhaseEvents ev(*ctx);
+    ev.mark(9);
+    const DevX dx = stage_x(*ctx, x, "x", nullptr);
+    ev.mark(10);
+    lpca_map* map = fit_dev(*ctx, *cfg, dx, timings);
+    try {
+      transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
+    } catch (...) {
+      delete map;
+      throw;
+    }
+    if (timings) timings->h2d += ev.secs(9, 10);
+    *out_map = map;
+  });
+}
+
+lpca_status lpca_map_info_get(const lpca_map* map, lpca_map_info* out) {
+  return guarded([&] {
+    if (!map || !out) throw Error(kInvalidArgument, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->method = map->method;
+    out->k = map->k;
+    out->l = map->l;
+    out->n = map->n;
+    out->seed = map->seed;
+    out->density = map->density;
+    out->scale = map->scale;
+    out->has_singular_values = map->sigma.empty() ? 0 : 1;
+  });
+}
+
+lpca_status lpca_map_copy_v(const lpca_map* map, double* v_out, int32_t out_location) {
+  return guarded([&] {
+    if (!map || !v_out) throw Error(kInvalidArgument, "null argument");
+    LPCA_CUDA(cudaSetDevice(map->device));
+    LPCA_CUDA(cudaMemcpy(v_out, map->v, sizeof(double) * map->n * map->k,
+                         out_location == LPCA_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  });
+}
+
+lpca_status lpca_map_copy_sigma(const lpca_map* map, double* sigma_out) {
+  return guarded([&] {
+    if (!map || !sigma_out) throw Error(kInvalidArgument, "null argument");
+    std::copy(map->sigma.begin(), map->sigma.end(), sigma_out);
+  });
+}
+
+lpca_status lpca_map_create(lpca_ctx* ctx, const lpca_map_info* info, const double* v_host,
+                            const double* sigma_host, lpca_map** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!info || !out || (!v_host && info->n * info->k > 0)) throw Error(kInvalidArgument, "null argument");
+    if (info->k < 0 || info->n < 0) throw Error(kInvalidArgument, "map: negative shape");
+    auto map = new lpca_map();
+    map->device = ctx->device;
+    map->method = info->method;
+    map->k = info->k;
+    map->l = info->l;
+    map->n = info->n;
+    map->seed = info->seed;
+    map->density = info->density;
+    map->scale = info->scale;
+    try {
+      LPCA_CUDA(cudaMalloc(&map->v, sizeof(double) * (info->n * info->k > 0 ? info->n * info->k : 1)));
+      if (info->n * info->k > 0)
+        LPCA_CUDA(cudaMemcpy(map->v, v_host, sizeof(double) * info->n * info->k, cudaMemcpyHostToDevice));
+      if (info->has_singular_values && sigma_host) map->sigma.assign(sigma_host, sigma_host + info->k);
+    } catch (...) {
+      delete map;
+      throw;
+    }
+    *out = map;
+  });
+}
+
+lpca_status lpca_map_destroy(lpca_map* map) {
+  return guarded([&] {
+    if (!map) return;
+    cudaSetDevice(map->device);
+    delete map;
+  });
+}
+
+// ---- kernel-level exports (fp64, reference summation order) -------------------
+namespace {
+
+// fp64 row-major device copy of a view (f32 data widened exactly).
+DevX stage_x_f64(lpca_ctx& ctx, const lpca_matrix_view* x) {
+  DevX d = stage_x(ctx, x, "kx", nullptr);
+  if (d.dtype == 8 || d.m * d.n == 0) {
+    d.dtype = 8;
+    return d;
+  }
+  double* wide = ctx.get<double>("kx.f64", d.m * d.n);
+  launch_widen_f32(ctx.stream, static_cast<const float*>(d.p), d.ld, d.m, d.n, wide);
+  LPCA_LAUNCHED(ctx);
+  return DevX{wide, 8, d.m, d.n, d.n};
+}
+
+const double* stage_f64(lpca_ctx& ctx, const double* p, index_t count, int location, const char* slot) {
+  if (location == LPCA_DEVICE) return p;
+  double* d = ctx.get<double>(slot, count > 0 ? count : 1);
+  if (count > 0) LPCA_CUDA(cudaMemcpyAsync(d, p, sizeof(double) * count, cudaMemcpyHostToDevice, ctx.stream));
+  return d;
+}
+
+void finish_out(lpca_ctx& ctx, double* out, const double* dev, index_t count, int location) {
+  if (location != LPCA_DEVICE && count > 0)
+    LPCA_CUDA(cudaMemcpyAsync(out, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+}  // namespace
+
+lpca_status lpca_spmm(lpca_ctx* ctx, const lpca_matrix_view* x, const double* w, int64_t w_cols,
+                      int32_t w_location, double* out, int32_t out_location) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const DevX d = stage_x_f64(*ctx, x);
+    const index_t m = d.m, n = d.n;
+    const double* wd = stage_f64(*ctx, w, n * w_cols, w_location, "k.w");
+    double* od = out_location == LPCA_DEVICE ? out : ctx->get<double>("k.out", m * w_cols);
+    if (m > 0 && w_cols > 0) {
+      launch_xw_simt<double, double>(ctx->stream, static_cast<const double*>(d.p), m, n, d.ld, wd,
+                                     w_cols, n, od, 1, m, true);
+      LPCA_LAUNCHED(*ctx);
+    }
+    finish_out(*ctx, out, od, m * w_cols, out_location);
+  });
+}
+
+lpca_status lpca_gemm_t(lpca_ctx* ctx, const double* u, int64_t m, int64_t l, int32_t u_location,
+                        const lpca_matrix_view* x, double* out, int32_t out_location) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const DevX d = stage_x_f64(*ctx, x);
+    if (d.m != m)
+      throw Error(kDimension, "gemm_t: inner dimensions differ (" + S(m) + " vs " + S(d.m) + ")");
+    const index_t n = d.n;
+    const double* ud = stage_f64(*ctx, u, m * l, u_location, "k.u");
+    double* urow = ctx->get<double>("k.urow", m * l);
+    if (m * l > 0) {
+      launch_transpose(ctx->stream, 8, ud, m, m, l, urow, l);
+      LPCA_LAUNCHED(*ctx);
+    }
+    double* od = out_location == LPCA_DEVICE ? out : ctx->get<double>("k.out", l * n);
+    if (l * n > 0) {
+      if (m > 0) {
+        launch_utx_simt<double>(ctx->stream, urow, l, static_cast<const double*>(d.p), d.ld, m, l, n,
+                                round_up(m, 16), od, true);
+        LPCA_LAUNCHED(*ctx);
+      } else {
+        launch_zero(ctx->stream, od, sizeof(double) * l * n);
+      }
+    }
+    finish_out(*ctx, out, od, l * n, out_location);
+  });
+}
+
+lpca_status lpca_dense_aat(lpca_ctx* ctx, const double* f, int64_t l, int64_t n, int32_t location,
+                           double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const double* fd = stage_f64(*ctx, f, l * n, location, "k.f");
+    double* od = location == LPCA_DEVICE ? out : ctx->get<double>("k.out", l * l);
+    if (l > 0) {
+      launch_gram(ctx->stream, fd, l, n, od);
+      LPCA_LAUNCHED(*ctx);
+    }
+    finish_out(*ctx, out, od, l * l, location);
+  });
+}
+
+lpca_status lpca_eigh(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                      double* evecs) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (l < 0) throw Error(kDimension, "eigh: negative size");
+    if (l == 0) return;
+    const double* ad = stage_f64(*ctx, a, l * l, location, "k.a");
+    double* acopy = ctx->get<double>("k.acopy", l * l);
+    LPCA_CUDA(cudaMemcpyAsync(acopy, ad, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, ctx->stream));
+    double* ev = ctx->get<double>("k.evals", l);
+    double* vec = location == LPCA_DEVICE ? evecs : ctx->get<double>("k.evecs", l * l);
+    double* work = ctx->get<double>("k.work", 2 * l * l);
+    int* st = ctx->get<int>("k.status", 2);
+    double* gap = ctx->get<double>("k.gap", 1);
+    launch_jacobi_eigh(ctx->stream, acopy, l, ev, vec, work, st, gap);
+    LPCA_LAUNCHED(*ctx);
+    int hst = 0;
+    double hgap = 0;
+    LPCA_CUDA(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LPCA_CUDA(cudaMemcpyAsync(&hgap, gap, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    LPCA_CUDA(cudaMemcpyAsync(evals, ev, sizeof(double) * l,
+                              location == LPCA_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    finish_out(*ctx, evecs, vec, l * l, location);
+    if (hst == 2)
+      throw Error(kInvalidArgument, "eigh: input is not symmetric (max |a_ij - a_ji| = " + std::to_string(hgap) + ")");
+    if (hst == 1)
+      throw Error(kConvergence, "eigh: Jacobi did not converge in 50 sweeps", -1, hgap);
+  });
+}
+
+lpca_status lpca_truncated_svd_via_gram(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
+                                        int64_t k, int32_t location, double* sigma, double* v,
+                                        double* u_tilde) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const double* fd = stage_f64(*ctx, f, l * n, location, "k.f");
+    double* vd = location == LPCA_DEVICE ? v : ctx->get<double>("k.v", n * (k > 0 ? k : 1));
+    double* ud = nullptr;
+    if (u_tilde) ud = location == LPCA_DEVICE ? u_tilde : ctx->get<double>("k.ut", l * (k > 0 ? k : 1));
+    std::vector<double> sg;
+    finish_spectral(*ctx, fd, l, n, k, vd, sg, ud);
+    std::copy(sg.begin(), sg.end(), sigma);
+    finish_out(*ctx, v, vd, n * k, location);
+    if (u_tilde) finish_out(*ctx, u_tilde, ud, l * k, location);
+  });
+}
+
+lpca_status lpca_synth_lowrank(lpca_ctx* ctx, int64_t row0, int64_t m, int64_t n, int64_t r,
+                               double rho, double noise, uint64_t seed, int32_t dtype, void* x_dev,
+                               int64_t ldx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (dtype != 4 && dtype != 8) throw Error(kInvalidArgument, "synth: dtype must be 4 or 8");
+    if (m < 0 || n < 1 || r < 1) throw Error(kInvalidArgument, "synth: bad shape");
+    if (ldx <= 0) ldx = n;
+    std::vector<double> sig(static_cast<std::size_t>(r));
+    double s = 1.0;
+    for (index_t t = 0; t < r; ++t) {  // sigma_t = rho^t, t = 0..r-1 (sigma_0 = 1)
+      sig[static_cast<std::size_t>(t)] = s;
+      s *= rho;
+    }
+    double* sd = ctx->get<double>("synth.sigma", r);
+    LPCA_CUDA(cudaMemcpyAsync(sd, sig.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+    const index_t batch = std::min<index_t>(m > 0 ? m : 1, 262144);
+    const index_t scratch = r * n + batch * r;
+    double* sc = ctx->get<double>("synth.scratch", scratch);
+    if (m > 0) {
+      launch_synth_lowrank(ctx->stream, row0, m, n, r, sd, noise, seed, dtype, x_dev, ldx, sc, scratch);
+      LPCA_LAUNCHED(*ctx);
+    }
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

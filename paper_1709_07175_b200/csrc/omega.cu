@@ -1,0 +1,284 @@
+// Projection generation, synthetic data and layout helpers.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "rng.cuh"
+
+namespace lpca {
+
+namespace {
+
+constexpr int kOmegaThreads = 256;
+constexpr int kOmegaChunk = 4096;  // raw draws staged per round (32 KB of smem)
+
+// One CTA per projection column (gen_gaussian runs one task per column,
+// projection.cpp:71-84). Lane 0 walks the column's xoshiro256** stream — the
+// only sequential part, integer ops only — staging raw 64-bit draws in shared
+// memory; then the whole CTA maps them through normal_icdf and writes the
+// column with coalesced stores.
+__global__ void __launch_bounds__(kOmegaThreads) omega_gaussian_kernel(index_t n, std::uint64_t seed,
+                                                                       double* out, index_t ld) {
+  __shared__ std::uint64_t raw[kOmegaChunk];
+  const index_t col = blockIdx.x;
+  Xoshiro rng = column_stream(seed, static_cast<std::uint64_t>(col));
+  double* dst = out + col * ld;
+  for (index_t base = 0; base < n; base += kOmegaChunk) {
+    const int cnt = static_cast<int>(n - base < kOmegaChunk ? n - base : kOmegaChunk);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < cnt; ++i) raw[i] = rng.next();
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += kOmegaThreads)
+      dst[base + i] = normal_icdf(u64_to_uniform(raw[i]));
+    __syncthreads();
+  }
+}
+
+// gen_very_sparse (projection.cpp:86-126): one uniform per cell, u < d/2 -> +1,
+// d/2 <= u < d -> -1, else 0. Dense {-1,0,+1} column, unscaled.
+__global__ void __launch_bounds__(kOmegaThreads) omega_sparse_kernel(index_t n, double density,
+                                                                     std::uint64_t seed, double* out,
+                                                                     index_t ld) {
+  __shared__ std::uint64_t raw[kOmegaChunk];
+  const index_t col = blockIdx.x;
+  Xoshiro rng = column_stream(seed, static_cast<std::uint64_t>(col));
+  double* dst = out + col * ld;
+  const double half = density / 2.0;
+  for (index_t base = 0; base < n; base += kOmegaChunk) {
+    const int cnt = static_cast<int>(n - base < kOmegaChunk ? n - base : kOmegaChunk);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < cnt; ++i) raw[i] = rng.next();
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += kOmegaThreads) {
+      const double u = u64_to_uniform(raw[i]);
+      dst[base + i] = u >= density ? 0.0 : (u < half ? 1.0 : -1.0);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- synthetic low-rank data --------------------------------------------------
+// G (rows x r, already scaled by sigma_t) and H (r x n) are materialised for one
+// row batch; X tiles are then a K = r DFMA product with t ascending, plus the
+// counter-based noise term, rounded once to the storage dtype.
+__global__ void synth_factor_kernel(index_t row0, index_t rows, index_t r, index_t n,
+                                    const double* sigma, std::uint64_t seed, double* gs, double* h,
+                                    bool make_h) {
+  const index_t tid = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  const index_t stride = static_cast<index_t>(gridDim.x) * blockDim.x;
+  const std::uint64_t seed_g = seed + 1001, seed_h = seed + 1002;
+  for (index_t e = tid; e < rows * r; e += stride) {
+    const index_t i = e / r, t = e % r;
+    gs[e] = counter_normal(seed_g, static_cast<std::uint64_t>((row0 + i) * r + t)) * sigma[t];
+  }
+  if (make_h)
+    for (index_t e = tid; e < r * n; e += stride)
+      h[e] = counter_normal(seed_h, static_cast<std::uint64_t>(e));
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(256) synth_gemm_kernel(index_t row0, index_t rows, index_t n,
+                                                         index_t r, const double* gs,
+                                                         const double* h, double noise,
+                                                         std::uint64_t seed, TO* x, index_t ldx,
+                                                         index_t x_row_off) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const index_t i0 = static_cast<index_t>(blockIdx.y) * BM, j0 = static_cast<index_t>(blockIdx.x) * BN;
+  double acc[4][4] = {};
+  for (index_t t0 = 0; t0 < r; t0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += 256) {
+      const int mi = e / BK, kk = e % BK;
+      const index_t gi = i0 + mi, gt = t0 + kk;
+      As[kk][mi] = (gi < rows && gt < r) ? gs[gi * r + gt] : 0.0;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += 256) {
+      const int kk = e / BN, nj = e % BN;
+      const index_t gt = t0 + kk, gj = j0 + nj;
+      Bs[kk][nj] = (gt < r && gj < n) ? h[gt * n + gj] : 0.0;
+    }
+    __syncthreads();
+    const int kmax = static_cast<int>(r - t0 < BK ? r - t0 : BK);
+    for (int kk = 0; kk < kmax; ++kk)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(As[kk][ty * 4 + a], Bs[kk][tx * 4 + b], acc[a][b]);
+    __syncthreads();
+  }
+  const std::uint64_t seed_e = seed + 1003;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const index_t gi = i0 + ty * 4 + a;
+    if (gi >= rows) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const index_t gj = j0 + tx * 4 + b;
+      if (gj >= n) continue;
+      const double e = counter_normal(seed_e, static_cast<std::uint64_t>((row0 + gi) * n + gj));
+      x[(x_row_off + gi) * ldx + gj] = static_cast<TO>(fma(noise, e, acc[a][b]));
+    }
+  }
+}
+
+__global__ void convert_kernel(const double* src, index_t lds, float* dst, index_t ldd,
+                               index_t rows, index_t cols, double scale) {
+  const index_t total = rows * cols;
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    const index_t c = e / rows, i = e % rows;
+    dst[c * ldd + i] = static_cast<float>(src[c * lds + i] * scale);
+  }
+}
+
+__global__ void scale_kernel(const double* src, double* dst, index_t count, double inv) {
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x)
+    dst[e] = src[e] * inv;
+}
+
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+__global__ void split_w_kernel(const double* w, index_t ldw, index_t n, index_t wc, index_t wpad,
+                               float* hi, float* lo, index_t ldd) {
+  const index_t total = wpad * ldd;
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    const index_t c = e / ldd, j = e % ldd;
+    float h = 0.f, lw = 0.f;
+    if (c < wc && j < n) {
+      const double v = w[c * ldw + j];
+      h = tf32_trunc(static_cast<float>(v));
+      lw = tf32_trunc(static_cast<float>(v - static_cast<double>(h)));
+    }
+    hi[e] = h;
+    lo[e] = lw;
+  }
+}
+
+template <typename TO>
+__global__ void csc_to_dense_kernel(index_t n, const std::int64_t* col_ptr,
+                                    const std::int64_t* row_idx, const double* vals, TO* x,
+                                    index_t ldx) {
+  for (index_t j = blockIdx.x; j < n; j += gridDim.x)
+    for (std::int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x)
+      x[row_idx[p] * ldx + j] = static_cast<TO>(vals[p]);
+}
+
+template <typename T>
+__global__ void transpose_kernel(const T* src, index_t lds, index_t rows, index_t cols, T* dst,
+                                 index_t ldd) {
+  __shared__ T tile[32][33];
+  const index_t r0 = static_cast<index_t>(blockIdx.x) * 32, c0 = static_cast<index_t>(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const index_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[c * lds + r];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const index_t r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) dst[r * ldd + c] = tile[threadIdx.x][k];
+  }
+}
+
+__global__ void widen_kernel(const float* src, index_t lds, index_t m, index_t n, double* dst) {
+  const index_t total = m * n;
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x)
+    dst[e] = static_cast<double>(src[(e / n) * lds + e % n]);
+}
+
+int grid_for(index_t work, int threads) {
+  index_t g = ceil_div(work, threads);
+  if (g > 148 * 16) g = 148 * 16;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+void launch_omega_gaussian(cudaStream_t s, index_t n, index_t l, std::uint64_t seed, double* out,
+                           index_t ld) {
+  if (l <= 0 || n <= 0) return;
+  omega_gaussian_kernel<<<static_cast<unsigned>(l), kOmegaThreads, 0, s>>>(n, seed, out, ld);
+}
+
+void launch_omega_very_sparse(cudaStream_t s, index_t n, index_t l, double density,
+                              std::uint64_t seed, double* out, index_t ld) {
+  if (l <= 0 || n <= 0) return;
+  omega_sparse_kernel<<<static_cast<unsigned>(l), kOmegaThreads, 0, s>>>(n, density, seed, out, ld);
+}
+
+void launch_synth_lowrank(cudaStream_t s, index_t row0, index_t m, index_t n, index_t r,
+                          const double* sigma_dev, double noise, std::uint64_t seed, int dtype,
+                          void* x, index_t ldx, double* scratch, index_t scratch_elems) {
+  double* h = scratch;
+  double* gs = scratch + r * n;
+  index_t batch = (scratch_elems - r * n) / r;
+  if (batch > m) batch = m;
+  if (batch < 64) throw Error(kInternal, "synth: scratch too small");
+  bool make_h = true;
+  for (index_t b0 = 0; b0 < m; b0 += batch) {
+    const index_t rows = m - b0 < batch ? m - b0 : batch;
+    synth_factor_kernel<<<grid_for(rows * r + (make_h ? r * n : 0), 256), 256, 0, s>>>(
+        row0 + b0, rows, r, n, sigma_dev, seed, gs, h, make_h);
+    make_h = false;
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 64)), static_cast<unsigned>(ceil_div(rows, 64)));
+    if (dtype == 4)
+      synth_gemm_kernel<float><<<grid, 256, 0, s>>>(row0 + b0, rows, n, r, gs, h, noise, seed,
+                                                    static_cast<float*>(x), ldx, b0);
+    else
+      synth_gemm_kernel<double><<<grid, 256, 0, s>>>(row0 + b0, rows, n, r, gs, h, noise, seed,
+                                                     static_cast<double*>(x), ldx, b0);
+  }
+}
+
+void launch_convert_f64_to_f32(cudaStream_t s, const double* src, index_t lds, float* dst,
+                               index_t ldd, index_t rows, index_t cols, double scale) {
+  convert_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, scale);
+}
+
+void launch_scale_f64(cudaStream_t s, const double* src, double* dst, index_t count, double inv) {
+  scale_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count, inv);
+}
+
+void launch_split_tf32_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc,
+                         index_t wpad, float* hi, float* lo, index_t ldd) {
+  split_w_kernel<<<grid_for(wpad * ldd, 256), 256, 0, s>>>(w, ldw, n, wc, wpad, hi, lo, ldd);
+}
+
+void launch_csc_to_dense(cudaStream_t s, index_t m, index_t n, const std::int64_t* col_ptr,
+                         const std::int64_t* row_idx, const double* vals, int dtype, void* x,
+                         index_t ldx) {
+  (void)m;
+  const unsigned g = static_cast<unsigned>(n < 148 * 8 ? n : 148 * 8);
+  if (n <= 0) return;
+  if (dtype == 4)
+    csc_to_dense_kernel<float><<<g, 128, 0, s>>>(n, col_ptr, row_idx, vals, static_cast<float*>(x), ldx);
+  else
+    csc_to_dense_kernel<double><<<g, 128, 0, s>>>(n, col_ptr, row_idx, vals, static_cast<double*>(x), ldx);
+}
+
+void launch_transpose(cudaStream_t s, int dtype, const void* src, index_t lds, index_t rows,
+                      index_t cols, void* dst, index_t ldd) {
+  dim3 grid(static_cast<unsigned>(ceil_div(rows, 32)), static_cast<unsigned>(ceil_div(cols, 32)));
+  dim3 block(32, 8);
+  if (dtype == 4)
+    transpose_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(src), lds, rows, cols,
+                                                   static_cast<float*>(dst), ldd);
+  else
+    transpose_kernel<double><<<grid, block, 0, s>>>(static_cast<const double*>(src), lds, rows,
+                                                    cols, static_cast<double*>(dst), ldd);
+}
+
+void launch_widen_f32(cudaStream_t s, const float* src, index_t lds, index_t m, index_t n, double* dst) {
+  widen_kernel<<<grid_for(m * n, 256), 256, 0, s>>>(src, lds, m, n, dst);
+}
+
+void launch_zero(cudaStream_t s, void* p, std::size_t bytes) {
+  LPCA_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+}
+
+}  // namespace lpca

@@ -1,0 +1,418 @@
+// The l x l step on the device, fp64 throughout:
+//   G = F F^T (dense_aat), symmetric eigendecomposition (parallel cyclic
+//   Jacobi in one CTA), V = F^T U~ diag(sigma)^-1 with canonical signs
+//   (truncated_svd_via_gram), and the Cholesky pieces of CholeskyQR2.
+// Reference: proj/core/src/kernels.cpp:148-172, proj/core/src/jacobi.cpp:18-135,
+// proj/core/src/truncated_svd.cpp:13-82, proj/core/src/lazy_projector.cpp:12-37.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace lpca {
+
+namespace {
+
+// dense_aat: G(r, c) = sum_j F(c, j) * F(r, j), j ascending, separate multiply
+// and add — the reference's exact rounding sequence, so G is bitwise equal to
+// the reference's for equal F and bitwise symmetric by construction.
+__global__ void gram_kernel(const double* __restrict__ f, index_t l, index_t n,
+                            double* __restrict__ g) {
+  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (e >= l * l) return;
+  const index_t c = e / l, r = e % l;
+  double acc = 0.0;
+  for (index_t j = 0; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(f[j * l + c], f[j * l + r]));
+  g[c * l + r] = acc;
+}
+
+constexpr int kJacobiThreads = 1024;
+constexpr int kMaxSweeps = 50;  // jacobi.cpp:64
+
+__device__ __forceinline__ void block_max_reduce(double& v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < static_cast<int>(blockDim.x / 32) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  v = red[0];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_sum_reduce(double& v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < static_cast<int>(blockDim.x / 32) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  v = red[0];
+  __syncthreads();
+}
+
+// Parallel cyclic Jacobi. Each round of the reference's round-robin schedule
+// (jacobi.cpp:18-33) is a set of l/2 disjoint pairs; rotations on disjoint
+// pairs commute and their angles depend only on their own 2x2 blocks, so the
+// whole round is applied at once as B <- J^T B J, one 2x2 block per task. The
+// rotation formulae, skip threshold (0.1 tol), stopping rule
+// (max |off-diagonal| <= 1e-14 ||A||_F) and sweep cap (50) are the reference's.
+// B (and V when it fits) live in shared memory; otherwise in the L2-resident
+// `work` buffer.
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(double* a, index_t l, double* evals,
+                                                                double* evecs, double* work,
+                                                                int b_in_smem, int v_in_smem,
+                                                                int* status, double* gap) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  const index_t npairs = (l + 1) / 2;
+  // per-round pair table
+  __shared__ int pp[512], qq[512];
+  __shared__ double cs[512], sn[512], tt[512];
+  __shared__ int act[512];
+  double* B = b_in_smem ? smem : work;
+  double* V = v_in_smem ? (b_in_smem ? smem + l * l : smem) : work + l * l;
+  const int tid = threadIdx.x;
+  const index_t ll = l * l;
+
+  // Copy in with exact symmetry (upper triangle mirrored, jacobi.cpp:54-56),
+  // checking the input symmetry like the reference (1e-10 ||A||_F).
+  double fro = 0.0, asym = 0.0;
+  for (index_t e = tid; e < ll; e += kJacobiThreads) {
+    const index_t j = e / l, i = e % l;
+    const double v = a[e];
+    fro += v * v;
+    asym = fmax(asym, fabs(v - a[i * l + j]));
+    B[e] = i <= j ? v : a[i * l + j];
+    V[e] = i == j ? 1.0 : 0.0;
+  }
+  block_sum_reduce(fro, red);
+  block_max_reduce(asym, red);
+  const double fnorm = sqrt(fro);
+  if (asym > 1e-10 * fnorm) {
+    if (tid == 0) {
+      status[0] = 2;
+      gap[0] = asym;
+    }
+    return;
+  }
+  const double tol = 1e-14 * fnorm;
+  const double skip_tol = 0.1 * tol;
+  const index_t players = l % 2 == 0 ? l : l + 1;
+
+  auto max_off = [&]() {
+    double w = 0.0;
+    for (index_t e = tid; e < ll; e += kJacobiThreads) {
+      const index_t j = e / l, i = e % l;
+      if (i < j) w = fmax(w, fabs(B[e]));
+    }
+    block_max_reduce(w, red);
+    return w;
+  };
+
+  double off = max_off();
+  int sweep = 0;
+  while (off > tol) {
+    if (sweep++ >= kMaxSweeps) {
+      if (tid == 0) {
+        status[0] = 1;
+        gap[0] = off;
+      }
+      return;
+    }
+    for (index_t round = 0; round < players - 1; ++round) {
+      // 1. rotation for each pair of this round
+      for (index_t k = tid; k < players / 2; k += kJacobiThreads) {
+        index_t x = k == 0 ? players - 1 : (round + k) % (players - 1);
+        index_t y = (round + players - 1 - k) % (players - 1);
+        if (x >= l || y >= l) {  // bye: a single index with identity rotation
+          pp[k] = static_cast<int>(x < l ? x : y);
+          qq[k] = -1;
+          act[k] = 0;
+          continue;
+        }
+        if (x > y) {
+          const index_t t = x;
+          x = y;
+          y = t;
+        }
+        pp[k] = static_cast<int>(x);
+        qq[k] = static_cast<int>(y);
+        const double apq = B[y * l + x];
+        if (fabs(apq) <= skip_tol) {
+          act[k] = 0;
+          continue;
+        }
+        const double app = B[x * l + x], aqq = B[y * l + y];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = theta >= 0.0 ? 1.0 / (theta + sqrt(theta * theta + 1.0))
+                                      : -1.0 / (-theta + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0);
+        act[k] = 1;
+        cs[k] = c;
+        sn[k] = t * c;
+        tt[k] = t;
+      }
+      __syncthreads();
+      // 2. B <- J^T B J over 2x2 blocks (P <= Q; the (Q, P) block is its transpose)
+      const index_t nblocks = npairs * (npairs + 1) / 2;
+      for (index_t e = tid; e < nblocks; e += kJacobiThreads) {
+        // unrank e -> (P, Q), P <= Q, row-major over the upper triangle
+        index_t P = static_cast<index_t>((2.0 * npairs + 1.0 -
+                                          sqrt((2.0 * npairs + 1.0) * (2.0 * npairs + 1.0) - 8.0 * e)) /
+                                         2.0);
+        if (P < 0) P = 0;
+        while (P > 0 && P * npairs - P * (P - 1) / 2 > e) --P;
+        while ((P + 1) * npairs - (P + 1) * P / 2 <= e) ++P;
+        const index_t Q = P + (e - (P * npairs - P * (P - 1) / 2));
+        const bool aP = act[P], aQ = act[Q];
+        if (!aP && !aQ) continue;
+        const int p1 = pp[P], q1 = qq[P], p2 = pp[Q], q2 = qq[Q];
+        if (P == Q) {  // diagonal block: the reference's closed form
+          const double apq = B[q1 * l + p1];
+          const double t = tt[P];
+          B[p1 * l + p1] = B[p1 * l + p1] - t * apq;
+          B[q1 * l + q1] = B[q1 * l + q1] + t * apq;
+          B[q1 * l + p1] = 0.0;
+          B[p1 * l + q1] = 0.0;
+          continue;
+        }
+        const double c1 = aP ? cs[P] : 1.0, s1 = aP ? sn[P] : 0.0;
+        const double c2 = aQ ? cs[Q] : 1.0, s2 = aQ ? sn[Q] : 0.0;
+        // rows {p1, q1} x cols {p2, q2}; q = -1 marks a bye (single index)
+        double b00 = B[p2 * l + p1];
+        double b01 = q2 >= 0 ? B[q2 * l + p1] : 0.0;
+        double b10 = q1 >= 0 ? B[p2 * l + q1] : 0.0;
+        double b11 = (q1 >= 0 && q2 >= 0) ? B[q2 * l + q1] : 0.0;
+        // columns (B J)
+        double n00 = c2 * b00 - s2 * b01, n01 = s2 * b00 + c2 * b01;
+        double n10 = c2 * b10 - s2 * b11, n11 = s2 * b10 + c2 * b11;
+        // rows (J^T B J)
+        b00 = c1 * n00 - s1 * n10;
+        b10 = s1 * n00 + c1 * n10;
+        b01 = c1 * n01 - s1 * n11;
+        b11 = s1 * n01 + c1 * n11;
+        B[p2 * l + p1] = b00;
+        B[p1 * l + p2] = b00;
+        if (q2 >= 0) {
+          B[q2 * l + p1] = b01;
+          B[p1 * l + q2] = b01;
+        }
+        if (q1 >= 0) {
+          B[p2 * l + q1] = b10;
+          B[q1 * l + p2] = b10;
+        }
+        if (q1 >= 0 && q2 >= 0) {
+          B[q2 * l + q1] = b11;
+          B[q1 * l + q2] = b11;
+        }
+      }
+      // 3. V <- V J (jacobi.cpp:107-114)
+      for (index_t e = tid; e < npairs * l; e += kJacobiThreads) {
+        const index_t P = e / l, i = e % l;
+        if (!act[P]) continue;
+        const int p = pp[P], q = qq[P];
+        const double c = cs[P], s = sn[P];
+        const double x = V[p * l + i], y = V[q * l + i];
+        V[p * l + i] = c * x - s * y;
+        V[q * l + i] = s * x + c * y;
+      }
+      __syncthreads();
+    }
+    off = max_off();
+  }
+  // Stable descending order of the diagonal (jacobi.cpp:119-133).
+  for (index_t i = tid; i < l; i += kJacobiThreads) {
+    const double di = B[i * l + i];
+    index_t rank = 0;
+    for (index_t j = 0; j < l; ++j) {
+      const double dj = B[j * l + j];
+      rank += (dj > di) || (dj == di && j < i);
+    }
+    evals[rank] = di;
+    for (index_t r = 0; r < l; ++r) evecs[rank * l + r] = V[i * l + r];
+  }
+  if (tid == 0) {
+    status[0] = 0;
+    gap[0] = off;
+  }
+}
+
+// V(j, r) = (sum_i F(i, j) U~(i, r)) / sigma_r, i ascending, separate mul/add
+// (truncated_svd.cpp:52-62); sigma_r = sqrt(lambda_r).
+__global__ void vform_kernel(const double* __restrict__ f, index_t l, index_t n,
+                             const double* __restrict__ ut, const double* __restrict__ evals,
+                             index_t k, double* __restrict__ sigma, double* __restrict__ v) {
+  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (e < k && sigma) sigma[e] = sqrt(evals[e]);
+  if (e >= n * k) return;
+  const index_t r = e / n, j = e % n;
+  double dot = 0.0;
+  for (index_t i = 0; i < l; ++i) dot = __dadd_rn(dot, __dmul_rn(f[j * l + i], ut[r * l + i]));
+  v[r * n + j] = dot / sqrt(evals[r]);
+}
+
+// Canonical signs (truncated_svd.cpp:64-80): in each V column the entry of
+// largest magnitude (first index on ties) is made non-negative; U~ follows.
+__global__ void sign_canon_kernel(double* v, index_t n, double* ut, index_t l) {
+  __shared__ double bm[32];
+  __shared__ index_t bi[32];
+  __shared__ int flip;
+  const index_t r = blockIdx.x;
+  double* col = v + r * n;
+  double best = -1.0;
+  index_t arg = 0;
+  for (index_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double mag = fabs(col[j]);
+    if (mag > best) {
+      best = mag;
+      arg = j;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const index_t oi = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oi < arg)) {
+      best = ob;
+      arg = oi;
+    }
+  }
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) {
+    bm[w] = best;
+    bi[w] = arg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < static_cast<int>(blockDim.x / 32); ++q)
+      if (bm[q] > best || (bm[q] == best && bi[q] < arg)) {
+        best = bm[q];
+        arg = bi[q];
+      }
+    flip = col[arg] < 0.0;
+  }
+  __syncthreads();
+  if (!flip) return;
+  for (index_t j = threadIdx.x; j < n; j += blockDim.x) col[j] = -col[j];
+  if (ut)
+    for (index_t i = threadIdx.x; i < l; i += blockDim.x) ut[r * l + i] = -ut[r * l + i];
+}
+
+// Cholesky (left-looking, lazy_projector.cpp:12-37) and the inverse of L,
+// written as w[c * l + j] = L^{-1}(c, j) — i.e. W = R^{-1} = L^{-T} as an
+// x-times-W operand of the sketch GEMM.
+__global__ void __launch_bounds__(1024) chol_inverse_kernel(const double* g, index_t l, double* w,
+                                                            double* lmat, int* status) {
+  __shared__ double red[32];
+  __shared__ int failed;
+  if (threadIdx.x == 0) failed = 0;
+  double maxd = 0.0;
+  for (index_t j = threadIdx.x; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
+  block_max_reduce(maxd, red);
+  const double pivot_tol = 1e-14 * maxd;
+  for (index_t e = threadIdx.x; e < l * l; e += blockDim.x) lmat[e] = 0.0;
+  __syncthreads();
+  for (index_t j = 0; j < l; ++j) {
+    // diagonal
+    if (threadIdx.x == 0) {
+      double d = g[j * l + j];
+      for (index_t r = 0; r < j; ++r) d -= lmat[r * l + j] * lmat[r * l + j];
+      if (d <= pivot_tol) {
+        failed = static_cast<int>(j) + 1;
+      } else {
+        lmat[j * l + j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (failed) break;
+    const double djj = lmat[j * l + j];
+    for (index_t i = j + 1 + threadIdx.x; i < l; i += blockDim.x) {
+      double v = g[j * l + i];
+      for (index_t r = 0; r < j; ++r) v -= lmat[r * l + i] * lmat[r * l + j];
+      lmat[j * l + i] = v / djj;
+    }
+    __syncthreads();
+  }
+  if (failed) {
+    if (threadIdx.x == 0) status[0] = failed;
+    return;
+  }
+  // L^{-1}: column c solves L x = e_c by forward substitution; x(j) = L^{-1}(j, c).
+  for (index_t c = threadIdx.x; c < l; c += blockDim.x) {
+    for (index_t j = 0; j < l; ++j) {
+      if (j < c) {
+        w[j * l + c] = 0.0;  // L^{-1}(j, c) = 0 above the diagonal -> w[j*l + c]
+        continue;
+      }
+      double v = j == c ? 1.0 : 0.0;
+      for (index_t r = c; r < j; ++r) v -= lmat[r * l + j] * w[r * l + c];
+      w[j * l + c] = v / lmat[j * l + j];
+    }
+  }
+  if (threadIdx.x == 0) status[0] = 0;
+}
+
+// tmp(r, j) = sum_{s <= r} L^{-1}(r, s) F(s, j); then F <- tmp.
+__global__ void apply_linv_kernel(const double* __restrict__ w, index_t l,
+                                  const double* __restrict__ f, index_t n, double* __restrict__ out) {
+  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (e >= l * n) return;
+  const index_t j = e / l, r = e % l;
+  double acc = 0.0;
+  for (index_t s = 0; s <= r; ++s) acc = fma(w[r * l + s], f[j * l + s], acc);
+  out[e] = acc;
+}
+
+}  // namespace
+
+void launch_gram(cudaStream_t s, const double* f, index_t l, index_t n, double* g) {
+  const index_t total = l * l;
+  gram_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(f, l, n, g);
+}
+
+void launch_jacobi_eigh(cudaStream_t s, double* a, index_t l, double* evals, double* evecs,
+                        double* work, int* status, double* gap) {
+  if (l > 1024) throw Error(kInvalidArgument, "eigh: l > 1024 is not supported on the device");
+  const std::size_t mat = static_cast<std::size_t>(l * l) * sizeof(double);
+  const std::size_t cap = 200 * 1024;
+  int b_smem = mat <= cap ? 1 : 0;
+  int v_smem = (b_smem && 2 * mat <= cap) ? 1 : 0;
+  const std::size_t smem = static_cast<std::size_t>(b_smem + v_smem) * mat;
+  LPCA_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem > 0 ? smem : 16)));
+  jacobi_kernel<<<1, kJacobiThreads, smem, s>>>(a, l, evals, evecs, work, b_smem, v_smem, status, gap);
+}
+
+void launch_vform(cudaStream_t s, const double* f, index_t l, index_t n, const double* ut,
+                  const double* evals, index_t k, double* sigma, double* v) {
+  const index_t total = n * k > k ? n * k : k;
+  vform_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(f, l, n, ut, evals, k, sigma, v);
+}
+
+void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* ut, index_t l) {
+  sign_canon_kernel<<<static_cast<unsigned>(k), 256, 0, s>>>(v, n, ut, l);
+}
+
+void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
+                         int* status) {
+  chol_inverse_kernel<<<1, 1024, 0, s>>>(g, l, rinv, work, status);
+}
+
+void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
+                         double* tmp) {
+  const index_t total = l * n;
+  apply_linv_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(rinv, l, f, n, tmp);
+  LPCA_CUDA(cudaMemcpyAsync(f, tmp, static_cast<std::size_t>(total) * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace lpca

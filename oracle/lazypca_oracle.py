@@ -96,8 +96,9 @@ _P_LOW = 0.02425
 _libm_log = np.frompyfunc(math.log, 1, 1)
 
 
-def normal_icdf(p: np.ndarray) -> np.ndarray:
-    """Acklam inverse normal CDF (rng.hpp:69-97), reference evaluation order."""
+def normal_icdf(p: np.ndarray, exact_log: bool = True) -> np.ndarray:
+    """Acklam inverse normal CDF (rng.hpp:69-97), reference evaluation order.
+    exact_log=False uses numpy's vectorised log (may differ by an ulp from libm)."""
     p = np.asarray(p, dtype=np.float64)
     out = np.empty_like(p)
     lo = p < _P_LOW
@@ -111,7 +112,7 @@ def normal_icdf(p: np.ndarray) -> np.ndarray:
     for mask, arg, sign in ((lo, p[lo], 1.0), (hi, 1.0 - p[hi], -1.0)):
         if not mask.any():
             continue
-        lg = _libm_log(arg).astype(np.float64)
+        lg = _libm_log(arg).astype(np.float64) if exact_log else np.log(arg)
         q = np.sqrt(-2.0 * lg)
         num = (((((_C[0] * q + _C[1]) * q + _C[2]) * q + _C[3]) * q + _C[4]) * q + _C[5])
         den = ((((_D[0] * q + _D[1]) * q + _D[2]) * q + _D[3]) * q + 1.0)
@@ -275,10 +276,14 @@ def chordal_distance(v1: np.ndarray, v2: np.ndarray) -> float:
 
 
 def principal_angles(v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+    """Principal angles between span(v1) and span(v2), ascending. Small angles
+    come from the sines (singular values of (I - Q1 Q1^T) Q2), which keep full
+    relative precision where arccos of the cosines bottoms out at sqrt(eps)."""
     q1, _ = np.linalg.qr(v1)
     q2, _ = np.linalg.qr(v2)
-    s = np.linalg.svd(q1.T @ q2, compute_uv=False)
-    return np.arccos(np.clip(s, -1.0, 1.0))
+    cos = np.sort(np.clip(np.linalg.svd(q1.T @ q2, compute_uv=False), -1.0, 1.0))[::-1]
+    sin = np.sort(np.clip(np.linalg.svd(q2 - q1 @ (q1.T @ q2), compute_uv=False), 0.0, 1.0))
+    return np.where(cos > np.sqrt(0.5), np.arcsin(sin[: cos.size]), np.arccos(cos))
 
 
 def pair_sample(m: int, max_pairs: int, seed: int):
@@ -295,13 +300,13 @@ def pair_sample(m: int, max_pairs: int, seed: int):
 
 
 # ---- BASELINE synthetic generator (not in the reference) ----------------------------
-def counter_normal(seed: int, idx: np.ndarray) -> np.ndarray:
+def counter_normal(seed: int, idx: np.ndarray, exact_log: bool = True) -> np.ndarray:
     with np.errstate(over="ignore"):
-        return normal_icdf(u64_to_uniform(mix64(_u(seed) ^ (_u(idx) * GOLDEN))))
+        return normal_icdf(u64_to_uniform(mix64(_u(seed) ^ (_u(idx) * GOLDEN))), exact_log)
 
 
 def synth_lowrank(row0: int, m: int, n: int, r: int, rho: float, noise: float, seed: int,
-                  dtype=np.float64) -> np.ndarray:
+                  dtype=np.float64, exact_log: bool = True) -> np.ndarray:
     """X = G diag(rho^t) H + noise E, t = 0..r-1, counter-based N(0,1) factors
     keyed exactly like the device generator (csrc/omega.cu). Summation order is
     numpy's, so the result agrees with the device to rounding, not bitwise."""
@@ -312,8 +317,11 @@ def synth_lowrank(row0: int, m: int, n: int, r: int, rho: float, noise: float, s
         s *= rho
     rows = np.arange(row0, row0 + m, dtype=np.uint64)
     gi = rows[:, None] * np.uint64(r) + np.arange(r, dtype=np.uint64)[None, :]
-    g = counter_normal(seed + 1001, gi) * sig[None, :]
-    h = counter_normal(seed + 1002, np.arange(r * n, dtype=np.uint64)).reshape(r, n)
-    ei = rows[:, None] * np.uint64(n) + np.arange(n, dtype=np.uint64)[None, :]
-    e = counter_normal(seed + 1003, ei)
-    return (g @ h + noise * e).astype(dtype)
+    g = counter_normal(seed + 1001, gi, exact_log) * sig[None, :]
+    h = counter_normal(seed + 1002, np.arange(r * n, dtype=np.uint64), exact_log).reshape(r, n)
+    out = np.empty((m, n), dtype=dtype)
+    for b0 in range(0, m, 4096):  # bounded temporaries
+        b1 = min(m, b0 + 4096)
+        ei = rows[b0:b1, None] * np.uint64(n) + np.arange(n, dtype=np.uint64)[None, :]
+        out[b0:b1] = g[b0:b1] @ h + noise * counter_normal(seed + 1003, ei, exact_log)
+    return out

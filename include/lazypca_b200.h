@@ -200,6 +200,15 @@ lpca_status lpca_truncated_svd_via_gram(lpca_ctx* ctx, const double* f, int64_t 
                                         int64_t k, int32_t location, double* sigma, double* v,
                                         double* u_tilde);
 
+/* fp32-data kernels of the fit, on the context's GEMM path (tcgen05 split-TF32
+ * or SIMT FFMA); all operands device-resident.
+ * sketch: out (m x w_cols, row-major fp32, ld ldo) = X W, W fp64 column-major n x w_cols.
+ * gemm_t: F (l x n column-major fp64) = U^T X, U row-major fp32 m x l (ld ldu). */
+lpca_status lpca_sketch_f32(lpca_ctx* ctx, const lpca_matrix_view* x, const double* w_dev,
+                            int64_t w_cols, float* out_dev, int64_t ldo);
+lpca_status lpca_gemm_t_f32(lpca_ctx* ctx, const float* u_dev, int64_t ldu, int64_t l,
+                            const lpca_matrix_view* x, double* f_dev);
+
 /* ---- synthetic data (BASELINE generator; not part of the reference) -------
  * X = G diag(rho^t) H + noise * E into device memory, row-major m x n, rows
  * [row0, row0 + m) of the global matrix (so any row shard can be produced on any

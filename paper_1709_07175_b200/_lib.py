@@ -88,6 +88,8 @@ SIGNATURES = {
     "lpca_eigh": (I32, [P, P, I64, I32, P, P]),
     "lpca_truncated_svd_via_gram": (I32, [P, P, I64, I64, I64, I32, P, P, P]),
     "lpca_synth_lowrank": (I32, [P, I64, I64, I64, I64, D, D, U64, I32, P, I64]),
+    "lpca_sketch_f32": (I32, [P, C.POINTER(MatrixView), P, I64, P, I64]),
+    "lpca_gemm_t_f32": (I32, [P, P, I64, I64, C.POINTER(MatrixView), P]),
 }
 
 _lib = None

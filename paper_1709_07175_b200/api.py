@@ -688,6 +688,34 @@ def truncated_svd_via_gram(f, k: int, ctx=None) -> TruncatedSVD:
     return TruncatedSVD(ut, sig[:kk], v)
 
 
+def sketch_f32(x_dev, w_dev, out_dev=None, ctx=None):
+    """OUT = X W for fp32 device X on the context's GEMM path (fp32-faithful).
+    w_dev: fp64 CUDA tensor n x w (any strides; made column-major). Returns fp32 m x w."""
+    import torch
+    ctx = ctx or default_context()
+    wc = w_dev.t().contiguous().t() if not w_dev.t().is_contiguous() else w_dev
+    wc = wc.to(torch.float64)
+    if out_dev is None:
+        out_dev = torch.empty((x_dev.shape[0], w_dev.shape[1]), dtype=torch.float32, device=x_dev.device)
+    vw = _View(x_dev)
+    _check(ctx.lib.lpca_sketch_f32(ctx.h, C.byref(vw.view), C.c_void_p(wc.data_ptr()), w_dev.shape[1],
+                                   C.c_void_p(out_dev.data_ptr()), out_dev.stride(0)))
+    return out_dev
+
+
+def gemm_t_f32(u_dev, x_dev, ctx=None):
+    """F = U^T X (l x n, fp64) for fp32 device U (m x l row-major) and X."""
+    import torch
+    ctx = ctx or default_context()
+    l = u_dev.shape[1]
+    ld = u_dev.stride(0)
+    f = torch.empty((x_dev.shape[1], l), dtype=torch.float64, device=x_dev.device)  # F^T row-major = F col-major
+    vw = _View(x_dev)
+    _check(ctx.lib.lpca_gemm_t_f32(ctx.h, C.c_void_p(u_dev.data_ptr()), ld, l, C.byref(vw.view),
+                                   C.c_void_p(f.data_ptr())))
+    return f.t()
+
+
 def synth_lowrank(x_dev, row0: int, r: int, rho: float, noise: float = 0.01, seed: int = 1000,
                   ctx=None) -> None:
     """Fills a row-major CUDA tensor with rows [row0, row0+m) of the BASELINE

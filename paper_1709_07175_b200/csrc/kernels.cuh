@@ -66,11 +66,29 @@ bool tc_xw_supported(index_t n, index_t wpad);
 void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
                   const float* w_hi, const float* w_lo, index_t wpad, index_t ldw, float* out,
                   index_t ldo, int num_sms);
-// part[c][j*l + r] for r < l: U^T X over row chunks with the same 3-term split.
+// Same, with any of: plain fp32 output (out, ldo, first wstore columns) and the
+// tf32 hi/lo planes of the output (out_hi/out_lo, ld ldh, all wpad columns).
+void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
+                         const float* w_hi, const float* w_lo, index_t wpad, index_t ldw, float* out,
+                         index_t ldo, index_t wstore, float* out_hi, float* out_lo, index_t ldh,
+                         int num_sms);
+// part[s][j*l + r] for r < l: U^T X with U given as tf32 hi/lo planes [m][ldu];
+// `splits` row splits (utx_tc_splits) summed afterwards in fixed order.
 bool tc_utx_supported(index_t l, index_t n);
+index_t utx_tc_splits(index_t m, index_t l, index_t n, int num_sms, index_t* rows_per_split);
+void launch_utx_tc_planes(cudaStream_t s, const float* u_hi, const float* u_lo, index_t ldu,
+                          const float* x, index_t ldx, index_t m, index_t l, index_t n, double* part,
+                          int num_sms);
 void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, index_t ldx,
                    index_t m, index_t l, index_t n, index_t chunk_rows, double* part,
                    int num_sms);
+// Split a row-major fp32 matrix (m x ld) into tf32 hi/lo planes of the same shape.
+void launch_split_tf32_rows(cudaStream_t s, const float* src, index_t m, index_t ld, float* hi,
+                            float* lo);
+// Transpose + split: src row-major m x cols (ld lds) -> hi/lo planes [cols][ldt]
+// (element (i, c) at c * ldt + i).
+void launch_split_tf32_transpose(cudaStream_t s, const float* src, index_t m, index_t cols, index_t lds,
+                                 float* hi, float* lo, index_t ldt);
 
 // ---- small fp64 kernels (the l x l step) ----------------------------------------
 // G = F F^T, F l x n column-major, bitwise symmetric (dense_aat, kernels.cpp:148-172).

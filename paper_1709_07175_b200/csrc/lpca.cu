@@ -309,20 +309,34 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
 
 // ---- GEMM dispatch ------------------------------------------------------------
 // Which engine runs an fp32 X-pass: tcgen05 split-TF32 when the path is
-// selected and the shape is supported, SIMT FFMA otherwise.
+// selected and the shape is supported, SIMT FFMA otherwise (fp64: DFMA).
 bool use_tc(const lpca_ctx& ctx, const DevX& x, index_t w) {
   return ctx.gemm_path == 0 && x.dtype == 4 && tc_xw_supported(x.n, round_up(w, 16)) &&
-         x.ld % 4 == 0;
+         x.ld % 4 == 0 && tc_utx_supported(w, x.n);
 }
 
-// out (T row-major [m][ldo]) = X W, W fp64 column-major (n x wc, ld ldw).
-// For fp32 X the operand is prepared once per call (rounded, or tf32 hi/lo).
-void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, void* out,
-             index_t ldo, bool exact) {
+// A sketch-shaped operand (m x l): the plain row-major matrix (dtype of X, ld
+// `ld`) and, on the tensor-core path, the tf32 hi/lo planes of its transpose
+// (round_up(l,16) rows of length m, ld `ldt`) — the K-major A operand of U^T X.
+struct Panel {
+  void* plain = nullptr;
+  float* hi = nullptr;
+  float* lo = nullptr;
+  index_t ld = 0;
+  index_t ldt = 0;
+};
+
+index_t planes_ld(index_t m) { return round_up(m > 0 ? m : 1, 4); }
+
+// out = X W, W fp64 column-major (n x wc, ld ldw). For fp32 X the operand is
+// prepared once per call (rounded to fp32, or split into tf32 hi/lo planes).
+void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, const Panel& out,
+             bool exact) {
   const index_t m = x.m, n = x.n;
+  if (m == 0) return;
   if (x.dtype == 8) {
     launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, w, wc,
-                                   ldw, static_cast<double*>(out), ldo, 1, exact);
+                                   ldw, static_cast<double*>(out.plain), out.ld, 1, exact);
     LPCA_LAUNCHED(ctx);
     return;
   }
@@ -332,8 +346,9 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
     float* lo = ctx.get<float>("w.lo", wpad * n);
     launch_split_tf32_w(ctx.stream, w, ldw, n, wc, wpad, hi, lo, n);
     LPCA_LAUNCHED(ctx);
-    launch_xw_tc(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, hi, lo, wpad, n,
-                 static_cast<float*>(out), ldo, ctx.num_sms);
+    launch_xw_tc_planes(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, hi, lo, wpad, n,
+                        static_cast<float*>(out.plain), out.ld, wc, out.hi, out.lo, out.ldt,
+                        ctx.num_sms);
     LPCA_LAUNCHED(ctx);
     return;
   }
@@ -341,7 +356,7 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
   launch_convert_f64_to_f32(ctx.stream, w, ldw, w32, n, n, wc, 1.0);
   LPCA_LAUNCHED(ctx);
   launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, w32, wc, n,
-                               static_cast<float*>(out), ldo, 1, false);
+                               static_cast<float*>(out.plain), out.ld, 1, false);
   LPCA_LAUNCHED(ctx);
 }
 
@@ -355,31 +370,33 @@ index_t pick_chunks(const lpca_ctx& ctx, index_t m, index_t tiles, bool exact) {
 }
 
 // F (l x n column-major fp64) = U^T X summed over this rank's rows, then
-// allreduced over ranks. U is T row-major [m][ldu].
-void utx_pass(lpca_ctx& ctx, const DevX& x, const void* u, index_t ldu, index_t l, double* f,
-              bool exact) {
+// allreduced over ranks.
+void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f, bool exact) {
   const index_t m = x.m, n = x.n;
   if (m == 0) {
     launch_zero(ctx.stream, f, sizeof(double) * l * n);
     ctx.allreduce(f, l * n);
     return;
   }
-  const bool tc = x.dtype == 4 && ctx.gemm_path == 0 && tc_utx_supported(l, n) && ldu % 4 == 0 &&
-                  x.ld % 4 == 0;
-  const index_t tiles = tc ? ceil_div(n, 256) : ceil_div(n, 64) * ceil_div(l, 64);
-  index_t chunks = pick_chunks(ctx, m, tiles, exact);
-  index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
-  chunks = ceil_div(m, chunk_rows);
-  double* part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
-  if (tc) {
-    launch_utx_tc(ctx.stream, static_cast<const float*>(u), ldu, static_cast<const float*>(x.p),
-                  x.ld, m, l, n, chunk_rows, part, ctx.num_sms);
-  } else if (x.dtype == 4) {
-    launch_utx_simt<float>(ctx.stream, static_cast<const float*>(u), ldu,
-                           static_cast<const float*>(x.p), x.ld, m, l, n, chunk_rows, part, false);
+  index_t chunks;
+  double* part;
+  if (u.hi && x.dtype == 4) {
+    index_t rps = 0;
+    chunks = utx_tc_splits(m, l, n, ctx.num_sms, &rps);
+    part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+    launch_utx_tc_planes(ctx.stream, u.hi, u.lo, u.ldt, static_cast<const float*>(x.p), x.ld, m, l, n, part,
+                         ctx.num_sms);
   } else {
-    launch_utx_simt<double>(ctx.stream, static_cast<const double*>(u), ldu,
-                            static_cast<const double*>(x.p), x.ld, m, l, n, chunk_rows, part, exact);
+    chunks = pick_chunks(ctx, m, ceil_div(n, 64) * ceil_div(l, 64), exact);
+    const index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
+    chunks = ceil_div(m, chunk_rows);
+    part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+    if (x.dtype == 4)
+      launch_utx_simt<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld,
+                             static_cast<const float*>(x.p), x.ld, m, l, n, chunk_rows, part, false);
+    else
+      launch_utx_simt<double>(ctx.stream, static_cast<const double*>(u.plain), u.ld,
+                              static_cast<const double*>(x.p), x.ld, m, l, n, chunk_rows, part, exact);
   }
   LPCA_LAUNCHED(ctx);
   if (chunks > 1) {
@@ -525,21 +542,31 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       return map;
     }
     const bool exact = ctx.exact != 0 && x.dtype == 8;
-    const index_t ldu = round_up(l, 16);
-    void* u = ctx.buf("u", dsize(x.dtype) * (m > 0 ? m : 1) * ldu);
+    const bool tc = use_tc(ctx, x, l);
+    const index_t mm = m > 0 ? m : 1;
+    // U (m x l, row-major, ld padded to 16): the plain matrix for the SIMT and
+    // SPCA paths, tf32 hi/lo planes for the tensor-core U^T X kernel.
+    Panel u;
+    u.ld = round_up(l, 16);
+    if (!tc || c.method == LPCA_SPCA) u.plain = ctx.buf("u", dsize(x.dtype) * mm * u.ld);
+    if (tc) {
+      u.ldt = planes_ld(m);
+      u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
+      u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
+    }
     // sketch U = X Omega (reducer.cpp:163-169)
-    if (m > 0) xw_pass(ctx, x, omega, l, n, u, ldu, exact);
+    xw_pass(ctx, x, omega, l, n, u, exact);
     ev.mark(1);
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
     double* f = ctx.get<double>("f", l * n);
     if (c.power_iters > 0) {
       double* z = ctx.get<double>("z.w", l * n);
       for (int it = 0; it < c.power_iters; ++it) {
-        utx_pass(ctx, x, u, ldu, l, f, exact);       // F = U^T X  (= Z^T)
-        orth_rows(ctx, f, l, n);                     // Z <- orth(Z)
+        utx_pass(ctx, x, u, l, f, exact);                    // F = U^T X  (= Z^T)
+        orth_rows(ctx, f, l, n);                             // Z <- orth(Z), CholeskyQR2
         launch_transpose(ctx.stream, 8, f, l, l, n, z, n);  // W = Z as n x l column-major
         LPCA_LAUNCHED(ctx);
-        if (m > 0) xw_pass(ctx, x, z, l, n, u, ldu, exact);  // U = X Z
+        xw_pass(ctx, x, z, l, n, u, exact);                  // U = X Z
       }
     }
     ev.mark(2);
@@ -558,9 +585,9 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
           chunks = ceil_div(m, chunk_rows);
           gpart = chunks == 1 ? gu : ctx.get<double>("spca.gpart", chunks * l * l);
           if (x.dtype == 4)
-            launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u), ldu, m, l, chunk_rows, gpart);
+            launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld, m, l, chunk_rows, gpart);
           else
-            launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u), ldu, m, l, chunk_rows, gpart);
+            launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u.plain), u.ld, m, l, chunk_rows, gpart);
           LPCA_LAUNCHED(ctx);
           if (chunks > 1) {
             launch_reduce_partials(ctx.stream, gpart, chunks, l * l, gu);
@@ -580,26 +607,30 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
                                            " is numerically dependent on earlier columns", h - 1);
         if (m > 0) {
           // Q = U R^{-1}: the sketch GEMM with X := U (m x l) and W := R^{-1}
-          DevX ux{u, x.dtype, m, l, ldu};
-          void* q = ctx.buf("q", dsize(x.dtype) * m * ldu);
+          void* q = ctx.buf("q", dsize(x.dtype) * m * u.ld);
           if (x.dtype == 8) {
-            launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(u), m, l, ldu, w,
-                                           l, l, static_cast<double*>(q), ldu, 1, exact);
+            launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(u.plain), m, l, u.ld, w,
+                                           l, l, static_cast<double*>(q), u.ld, 1, exact);
           } else {
             float* w32 = ctx.get<float>("spca.w32", l * l);
             launch_convert_f64_to_f32(ctx.stream, w, l, w32, l, l, l, 1.0);
             LPCA_LAUNCHED(ctx);
-            launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(u), m, l, ldu, w32,
-                                         l, l, static_cast<float*>(q), ldu, 1, false);
+            launch_zero(ctx.stream, q, sizeof(float) * m * u.ld);
+            launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(u.plain), m, l, u.ld, w32,
+                                         l, l, static_cast<float*>(q), u.ld, 1, false);
           }
           LPCA_LAUNCHED(ctx);
-          (void)ux;
-          LPCA_CUDA(cudaMemcpyAsync(u, q, dsize(x.dtype) * m * ldu, cudaMemcpyDeviceToDevice, ctx.stream));
+          LPCA_CUDA(cudaMemcpyAsync(u.plain, q, dsize(x.dtype) * m * u.ld, cudaMemcpyDeviceToDevice, ctx.stream));
         }
+      }
+      if (u.hi && m > 0) {  // Q's tf32 planes for the tensor-core F = Q^T X
+        launch_split_tf32_transpose(ctx.stream, static_cast<const float*>(u.plain), m, l, u.ld, u.hi, u.lo,
+                                    u.ldt);
+        LPCA_LAUNCHED(ctx);
       }
     }
     ev.mark(3);
-    utx_pass(ctx, x, u, ldu, l, f, exact);  // F = U^T X (or Q^T X)
+    utx_pass(ctx, x, u, l, f, exact);  // F = U^T X (or Q^T X)
     ev.mark(4);
     finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
     ev.mark(5);
@@ -644,8 +675,11 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
         launch_xw_simt<double, float>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
                                       map.v, k, map.n, static_cast<float*>(ydev), ors, ocs, ctx.exact != 0);
       LPCA_LAUNCHED(ctx);
-    } else if (row && y_dtype == 4 && use_tc(ctx, x, k)) {
-      xw_pass(ctx, x, map.v, k, map.n, ydev, ldy, false);
+    } else if (row && y_dtype == 4 && use_tc(ctx, x, k) && ldy % 4 == 0) {
+      Panel yo;
+      yo.plain = ydev;
+      yo.ld = ldy;
+      xw_pass(ctx, x, map.v, k, map.n, yo, false);
     } else {
       float* w32 = ctx.get<float>("v.f32", k * x.n);
       launch_convert_f64_to_f32(ctx.stream, map.v, map.n, w32, x.n, x.n, k, 1.0);
@@ -1093,6 +1127,70 @@ lpca_status lpca_truncated_svd_via_gram(lpca_ctx* ctx, const double* f, int64_t 
     std::copy(sg.begin(), sg.end(), sigma);
     finish_out(*ctx, v, vd, n * k, location);
     if (u_tilde) finish_out(*ctx, u_tilde, ud, l * k, location);
+  });
+}
+
+lpca_status lpca_sketch_f32(lpca_ctx* ctx, const lpca_matrix_view* x, const double* w_dev,
+                            int64_t w_cols, float* out_dev, int64_t ldo) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const DevX d = stage_x(*ctx, x, "kx", nullptr);
+    if (d.dtype != 4) throw Error(kInvalidArgument, "sketch_f32: X must be fp32");
+    if (ldo < w_cols) throw Error(kInvalidArgument, "sketch_f32: ldo < w_cols");
+    Panel out;
+    out.plain = out_dev;
+    out.ld = ldo;
+    if (use_tc(*ctx, d, w_cols) && ldo % 4 == 0) {
+      // the fit's layout: hi/lo planes at ld round_up(w, 16) plus the plain output
+      const index_t ld = round_up(w_cols, 16);
+      const index_t wpad = ld;
+      float* hi = ctx->get<float>("w.hi", wpad * d.n);
+      float* lo = ctx->get<float>("w.lo", wpad * d.n);
+      launch_split_tf32_w(ctx->stream, w_dev, d.n, d.n, w_cols, wpad, hi, lo, d.n);
+      LPCA_LAUNCHED(*ctx);
+      const index_t ldt = planes_ld(d.m);
+      float* uh = ctx->get<float>("k.uh", ld * ldt);
+      float* ul = ctx->get<float>("k.ul", ld * ldt);
+      launch_xw_tc_planes(ctx->stream, static_cast<const float*>(d.p), d.m, d.n, d.ld, hi, lo, wpad, d.n,
+                          out_dev, ldo, w_cols, uh, ul, ldt, ctx->num_sms);
+      LPCA_LAUNCHED(*ctx);
+    } else {
+      xw_pass(*ctx, d, w_dev, w_cols, d.n, out, false);
+    }
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lpca_status lpca_gemm_t_f32(lpca_ctx* ctx, const float* u_dev, int64_t ldu, int64_t l,
+                            const lpca_matrix_view* x, double* f_dev) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const DevX d = stage_x(*ctx, x, "kx", nullptr);
+    if (d.dtype != 4) throw Error(kInvalidArgument, "gemm_t_f32: X must be fp32");
+    Panel u;
+    u.plain = const_cast<float*>(u_dev);
+    u.ld = ldu;
+    if (ctx->gemm_path == 0 && tc_utx_supported(l, d.n) && ldu % 4 == 0 && d.ld % 4 == 0) {
+      u.ldt = planes_ld(d.m);
+      u.hi = ctx->get<float>("k.uh", round_up(l, 16) * u.ldt);
+      u.lo = ctx->get<float>("k.ul", round_up(l, 16) * u.ldt);
+      launch_zero(ctx->stream, u.hi, sizeof(float) * round_up(l, 16) * u.ldt);
+      launch_zero(ctx->stream, u.lo, sizeof(float) * round_up(l, 16) * u.ldt);
+      if (d.m > 0) {
+        launch_split_tf32_transpose(ctx->stream, u_dev, d.m, l, ldu, u.hi, u.lo, u.ldt);
+        LPCA_LAUNCHED(*ctx);
+      }
+    }
+    const int world = ctx->world;
+    ctx->world = 1;  // kernel-level: this rank's rows only
+    try {
+      utx_pass(*ctx, d, u, l, f_dev, false);
+    } catch (...) {
+      ctx->world = world;
+      throw;
+    }
+    ctx->world = world;
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

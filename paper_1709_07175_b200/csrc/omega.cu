@@ -159,6 +159,38 @@ __global__ void split_w_kernel(const double* w, index_t ldw, index_t n, index_t 
   }
 }
 
+__global__ void split_rows_kernel(const float* src, index_t count, float* hi, float* lo) {
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    const float v = src[e];
+    const float h = tf32_trunc(v);
+    hi[e] = h;
+    lo[e] = tf32_trunc(v - h);
+  }
+}
+
+// 32 x 32 tiles through shared memory: coalesced reads of src rows, coalesced
+// writes of the transposed planes.
+__global__ void split_transpose_kernel(const float* src, index_t m, index_t cols, index_t lds, float* hi,
+                                       float* lo, index_t ldt) {
+  __shared__ float tile[32][33];
+  const index_t r0 = static_cast<index_t>(blockIdx.x) * 32, c0 = static_cast<index_t>(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const index_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < m && c < cols) ? src[r * lds + c] : 0.f;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const index_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < m) {
+      const float v = tile[threadIdx.x][k];
+      const float h = tf32_trunc(v);
+      hi[c * ldt + r] = h;
+      lo[c * ldt + r] = tf32_trunc(v - h);
+    }
+  }
+}
+
 template <typename TO>
 __global__ void csc_to_dense_kernel(index_t n, const std::int64_t* col_ptr,
                                     const std::int64_t* row_idx, const double* vals, TO* x,
@@ -247,6 +279,18 @@ void launch_scale_f64(cudaStream_t s, const double* src, double* dst, index_t co
 void launch_split_tf32_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc,
                          index_t wpad, float* hi, float* lo, index_t ldd) {
   split_w_kernel<<<grid_for(wpad * ldd, 256), 256, 0, s>>>(w, ldw, n, wc, wpad, hi, lo, ldd);
+}
+
+void launch_split_tf32_rows(cudaStream_t s, const float* src, index_t m, index_t ld, float* hi,
+                            float* lo) {
+  split_rows_kernel<<<grid_for(m * ld, 256), 256, 0, s>>>(src, m * ld, hi, lo);
+}
+
+void launch_split_tf32_transpose(cudaStream_t s, const float* src, index_t m, index_t cols, index_t lds,
+                                 float* hi, float* lo, index_t ldt) {
+  if (m <= 0 || cols <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(cols, 32)));
+  split_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, m, cols, lds, hi, lo, ldt);
 }
 
 void launch_csc_to_dense(cudaStream_t s, index_t m, index_t n, const std::int64_t* col_ptr,

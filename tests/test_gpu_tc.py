@@ -1,0 +1,77 @@
+"""GPU: the tcgen05 split-TF32 kernels (fp32 data) against the SIMT FFMA path and
+the reference, over the shapes that exercise tails and both tile layouts:
+m not a multiple of 128, n not a multiple of 32 or 256, odd l, l > 128."""
+import numpy as np
+import pytest
+
+import paper_1709_07175_b200 as lp
+from oracle import lazypca_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _x(m, n, r, rho, seed=1000):
+    import torch
+    x = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(x, 0, r, rho, 0.01, seed)
+    return x
+
+
+def _fit(ctx, x, k, l, path, q=0, method=lp.ReducerMethod.lazy_spca, seed=7):
+    ctx.set_gemm_path(path)
+    try:
+        cfg = lp.ReducerConfig(method=method, k=k, l=l, projection=lp.ProjectionSpec(seed=seed),
+                               power_iters=q)
+        return lp.reduce(x, cfg, ctx=ctx)
+    finally:
+        ctx.set_gemm_path("tcgen05")
+
+
+@pytest.mark.parametrize("m,n,r,k,l", [
+    (1000, 256, 30, 8, 16),      # single partial tile
+    (5003, 1000, 60, 20, 37),    # odd m, n % 32 != 0, odd l
+    (20000, 4096, 200, 100, 110),  # c2 shape
+    (9000, 2048, 300, 200, 220),   # l > 128: two M halves in U^T X (configs[2] rho)
+    (4000, 300, 40, 16, 256),     # l = 256 boundary
+])
+def test_tc_matches_reference(ctx, ref, m, n, r, k, l):
+    x = _x(m, n, r, 0.98 if l > 128 else 0.97)
+    xh = x.cpu().numpy()
+    got = _fit(ctx, x, k, l, "tcgen05")
+    rv, rs, _, _ = ref.reduce(2, xh, k, l, 7)
+    rel = np.abs(got.singular_values - rs) / rs
+    print(f"m={m} n={n} l={l}: sigma rel max {rel.max():.3e}")
+    assert rel.max() < 1e-4
+    kk = max(1, k // 2)
+    assert np.max(O.principal_angles(got.v[:, :kk], rv[:, :kk])) < 1e-3
+
+
+def test_tc_and_simt_paths_agree(ctx):
+    x = _x(30000, 1024, 80, 0.96)
+    a = _fit(ctx, x, 32, 48, "tcgen05")
+    b = _fit(ctx, x, 32, 48, "simt")
+    rel = np.abs(a.singular_values - b.singular_values) / b.singular_values
+    assert rel.max() < 2e-5, rel.max()
+    assert O.chordal_distance(a.v[:, :16], b.v[:, :16]) < 1e-3
+
+
+def test_tc_transform_matches_fp64(ctx):
+    import torch
+    x = _x(7777, 512, 50, 0.95)
+    m = _fit(ctx, x, 40, 48, "tcgen05")
+    y = torch.empty((7777, 40), dtype=torch.float32, device="cuda")
+    lp.apply_map(m, x, out=y, ctx=ctx)
+    yr = x.double().cpu().numpy() @ m.v
+    err = np.abs(y.cpu().numpy() - yr).max() / np.abs(yr).max()
+    assert err < 1e-5, err  # fp32 output; split-TF32 bias ~1.3e-6 (see gemm_tc.cu)
+
+
+def test_tc_power_and_spca(ctx, ref):
+    x = _x(6000, 1024, 120, 0.97)
+    xh = x.cpu().numpy().astype(np.float64)
+    p = _fit(ctx, x, 40, 60, "tcgen05", q=1)
+    v, s, _ = O.reduce_lazy_spca(xh, 40, 60, 7, power_iters=1)
+    assert np.max(np.abs(p.singular_values - s) / s) < 1e-4
+    sp = _fit(ctx, x, 40, 60, "tcgen05", method=lp.ReducerMethod.spca)
+    rv, rs, _, _ = ref.reduce(1, x.cpu().numpy(), 40, 60, 7)
+    assert np.max(np.abs(sp.singular_values - rs) / rs) < 1e-4

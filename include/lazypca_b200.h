@@ -191,10 +191,17 @@ lpca_status lpca_gemm_t(lpca_ctx* ctx, const double* u, int64_t m, int64_t l, in
 /* dense_aat(F): F l x n, out l x l, bitwise symmetric. */
 lpca_status lpca_dense_aat(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
                            int32_t location, double* out);
-/* Symmetric eigendecomposition (replaces tridiag_eigh / jacobi_eigh): eigenvalues
- * descending, eigenvectors column-major. Parallel cyclic Jacobi on the device. */
+/* Symmetric eigendecomposition, eigenvalues descending, eigenvectors column-major.
+ * lpca_eigh replaces tridiag_eigh (tridiag_eigh.hpp:8): Householder tridiagonalisation,
+ * multisection eigenvalues, inverse-iteration eigenvectors, back-transformation.
+ * lpca_eigh_jacobi replaces the cross-check jacobi_eigh (jacobi.hpp:14): parallel
+ * cyclic Jacobi with the reference's schedule and stopping rule. */
 lpca_status lpca_eigh(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
                       double* evecs);
+lpca_status lpca_eigh_jacobi(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                             double* evecs);
+/* Eigensolver used by the fit's l x l step: 0 = tridiagonal route (default), 1 = Jacobi. */
+lpca_status lpca_ctx_set_eigensolver(lpca_ctx* ctx, int32_t method);
 /* truncated_svd_via_gram(F, k): sigma (k), v (n x k), u_tilde (l x k, may be NULL). */
 lpca_status lpca_truncated_svd_via_gram(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
                                         int64_t k, int32_t location, double* sigma, double* v,

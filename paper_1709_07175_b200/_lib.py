@@ -86,6 +86,8 @@ SIGNATURES = {
     "lpca_gemm_t": (I32, [P, P, I64, I64, I32, C.POINTER(MatrixView), P, I32]),
     "lpca_dense_aat": (I32, [P, P, I64, I64, I32, P]),
     "lpca_eigh": (I32, [P, P, I64, I32, P, P]),
+    "lpca_eigh_jacobi": (I32, [P, P, I64, I32, P, P]),
+    "lpca_ctx_set_eigensolver": (I32, [P, I32]),
     "lpca_truncated_svd_via_gram": (I32, [P, P, I64, I64, I64, I32, P, P, P]),
     "lpca_synth_lowrank": (I32, [P, I64, I64, I64, I64, D, D, U64, I32, P, I64]),
     "lpca_sketch_f32": (I32, [P, C.POINTER(MatrixView), P, I64, P, I64]),

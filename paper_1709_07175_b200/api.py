@@ -387,6 +387,9 @@ class Context:
     def set_gemm_path(self, path: str) -> None:
         _check(self.lib.lpca_ctx_set_gemm_path(self.h, {"tcgen05": 0, "simt": 1}[path]))
 
+    def set_eigensolver(self, method: str) -> None:
+        _check(self.lib.lpca_ctx_set_eigensolver(self.h, {"tridiag": 0, "jacobi": 1}[method]))
+
     def set_exact_order(self, on: bool) -> None:
         _check(self.lib.lpca_ctx_set_exact_order(self.h, int(bool(on))))
 
@@ -648,8 +651,8 @@ class EigenDecomposition:
     eigenvectors: np.ndarray
 
 
-def eigh(a, ctx=None) -> EigenDecomposition:
-    """Replaces tridiag_eigh / jacobi_eigh: eigenvalues descending."""
+def eigh(a, ctx=None, method: str = "tridiag") -> EigenDecomposition:
+    """tridiag_eigh (default) or jacobi_eigh on the device: eigenvalues descending."""
     ctx = ctx or default_context()
     a = np.asfortranarray(np.asarray(a, dtype=np.float64))
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
@@ -657,13 +660,18 @@ def eigh(a, ctx=None) -> EigenDecomposition:
     lsz = a.shape[0]
     ev = np.zeros(lsz)
     vec = np.zeros((lsz, lsz), order="F")
-    _check(ctx.lib.lpca_eigh(ctx.h, a.ctypes.data if a.size else None, lsz, L.LPCA_HOST,
-                             ev.ctypes.data if lsz else None, vec.ctypes.data if lsz else None))
+    fn = ctx.lib.lpca_eigh if method == "tridiag" else ctx.lib.lpca_eigh_jacobi
+    _check(fn(ctx.h, a.ctypes.data if a.size else None, lsz, L.LPCA_HOST,
+              ev.ctypes.data if lsz else None, vec.ctypes.data if lsz else None))
     return EigenDecomposition(ev, vec)
 
 
-tridiag_eigh = eigh
-jacobi_eigh = eigh
+def tridiag_eigh(a, ctx=None) -> EigenDecomposition:
+    return eigh(a, ctx, "tridiag")
+
+
+def jacobi_eigh(a, ctx=None) -> EigenDecomposition:
+    return eigh(a, ctx, "jacobi")
 
 
 @dataclass

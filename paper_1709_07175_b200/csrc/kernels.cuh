@@ -102,6 +102,12 @@ void launch_syrk_partials(cudaStream_t s, const T* u, index_t ldu, index_t m, in
 // status[0] = 0 ok / 1 no convergence; gap[0] = last max off-diagonal.
 void launch_jacobi_eigh(cudaStream_t s, double* a, index_t l, double* evals, double* evecs,
                         double* work, int* status, double* gap);
+// Tridiagonal route (eigh.cu): a (l x l column-major, read only) -> evals
+// descending, evecs column-major. `work` holds eigh_tridiag_workspace(l) bytes.
+// status[0] = 0 ok / 2 asymmetric input (gap[0] = max asymmetry).
+std::size_t eigh_tridiag_workspace(index_t l);
+void launch_eigh_tridiag(cudaStream_t s, const double* a, index_t l, double* evals, double* evecs, void* work,
+                         int* status, double* gap);
 // V(j,r) = (sum_i F(i,j) Ut(i,r)) / sigma_r  (truncated_svd.cpp:52-62), then the
 // canonical sign flip (truncated_svd.cpp:64-80) applied to V and Ut.
 void launch_vform(cudaStream_t s, const double* f, index_t l, index_t n, const double* ut,

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -99,6 +100,8 @@ struct lpca_ctx {
   int gemm_path = 0;  // 0 = tcgen05 split-TF32 for fp32 data, 1 = SIMT
   int exact = 0;      // fp64 reference summation order (tests)
   std::int64_t launches = 0;
+  int last_sweeps = 0;
+  int eigensolver = 0;  // 0: tridiagonal route (tridiag_eigh), 1: parallel Jacobi (jacobi_eigh)
   std::unordered_map<std::string, std::pair<void*, std::size_t>> ws;
   cudaEvent_t ev[12] = {};
 
@@ -136,8 +139,16 @@ struct lpca_map {
   double density = 1.0, scale = 1.0;
   double* v = nullptr;  // device, n x k column-major fp64
   std::vector<double> sigma;
+  // V comes from the stream-ordered allocator on the creating context's stream:
+  // no device-wide synchronisation per fit (cudaMalloc/cudaFree would stall the
+  // pipeline). A map must be destroyed before its context.
+  cudaStream_t stream = nullptr;
+  void alloc_v(cudaStream_t s, std::size_t bytes) {
+    stream = s;
+    LPCA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&v), bytes, s));
+  }
   ~lpca_map() {
-    if (v) cudaFree(v);
+    if (v) cudaFreeAsync(v, stream);
   }
 };
 
@@ -452,6 +463,23 @@ void regenerate_dev(lpca_ctx& ctx, const lpca_config& c, double* omega) {
   LPCA_LAUNCHED(ctx);
 }
 
+// Symmetric eigensolve of a device l x l matrix (overwritten for Jacobi).
+// method 0: tridiagonal route (Householder + multisection + inverse iteration),
+// method 1: parallel cyclic Jacobi (the cross-check solver).
+void eigh_dev(lpca_ctx& ctx, double* a, index_t l, double* evals, double* evecs, int* st, double* gap,
+              int method) {
+  if (method == 1) {
+    double* work = ctx.get<double>("eig.jwork", 2 * l * l);
+    launch_jacobi_eigh(ctx.stream, a, l, evals, evecs, work, st, gap);
+    LPCA_LAUNCHED(ctx);
+    return;
+  }
+  void* work = ctx.buf("eig.twork", eigh_tridiag_workspace(l));
+  launch_eigh_tridiag(ctx.stream, a, l, evals, evecs, work, st, gap);
+  ctx.note_launch(10);
+  LPCA_CUDA(cudaGetLastError());
+}
+
 // truncated_svd_via_gram on a device F (l x n). Fills v (n x k), sigma (host),
 // and optionally u~ (device, l x k). Throws the reference's errors.
 void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index_t k, double* v,
@@ -463,13 +491,11 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
   double* g = ctx.get<double>("svd.g", l * l);
   double* evals = ctx.get<double>("svd.evals", l);
   double* evecs = ctx.get<double>("svd.evecs", l * l);
-  double* work = ctx.get<double>("svd.work", 2 * l * l);
   int* st = ctx.get<int>("svd.status", 2);
   double* gap = ctx.get<double>("svd.gap", 1);
   launch_gram(ctx.stream, f, l, n, g);
   LPCA_LAUNCHED(ctx);
-  launch_jacobi_eigh(ctx.stream, g, l, evals, evecs, work, st, gap);
-  LPCA_LAUNCHED(ctx);
+  eigh_dev(ctx, g, l, evals, evecs, st, gap, ctx.eigensolver);
   launch_vform(ctx.stream, f, l, n, evecs, evals, k, nullptr, v);
   LPCA_LAUNCHED(ctx);
   launch_sign_canon(ctx.stream, v, n, k, evecs, l);
@@ -478,12 +504,15 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
     LPCA_CUDA(cudaMemcpyAsync(ut_out, evecs, sizeof(double) * l * k, cudaMemcpyDeviceToDevice, ctx.stream));
   }
   std::vector<double> lam(static_cast<std::size_t>(l));
-  int hst = 0;
+  int hst = 0, hsw[2] = {0, 0};
   double hgap = 0.0;
   LPCA_CUDA(cudaMemcpyAsync(lam.data(), evals, sizeof(double) * l, cudaMemcpyDeviceToHost, ctx.stream));
-  LPCA_CUDA(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaMemcpyAsync(hsw, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   LPCA_CUDA(cudaMemcpyAsync(&hgap, gap, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
   LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  hst = hsw[0];
+  ctx.last_sweeps = hsw[1];
+  if (std::getenv("LPCA_VERBOSE")) std::fprintf(stderr, "lazypca_b200: eigh l=%lld sweeps=%d\n", (long long)l, hsw[1]);
   if (hst == 2)
     throw Error(kInvalidArgument, "eigh: input is not symmetric (max |a_ij - a_ji| = " +
                                       std::to_string(hgap) + ")");
@@ -527,7 +556,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
   map->density = c.density;
   map->scale = projection_scale(c);
   try {
-    LPCA_CUDA(cudaMalloc(&map->v, sizeof(double) * (n * k > 0 ? n * k : 1)));
+    map->alloc_v(ctx.stream, sizeof(double) * (n * k > 0 ? n * k : 1));
     double* omega = ctx.get<double>("omega", n * l);
     regenerate_dev(ctx, c, omega);
     if (c.method == LPCA_RP) {
@@ -944,8 +973,10 @@ lpca_status lpca_map_copy_v(const lpca_map* map, double* v_out, int32_t out_loca
   return guarded([&] {
     if (!map || !v_out) throw Error(kInvalidArgument, "null argument");
     LPCA_CUDA(cudaSetDevice(map->device));
-    LPCA_CUDA(cudaMemcpy(v_out, map->v, sizeof(double) * map->n * map->k,
-                         out_location == LPCA_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    LPCA_CUDA(cudaMemcpyAsync(v_out, map->v, sizeof(double) * map->n * map->k,
+                              out_location == LPCA_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              map->stream));
+    LPCA_CUDA(cudaStreamSynchronize(map->stream));
   });
 }
 
@@ -972,9 +1003,10 @@ lpca_status lpca_map_create(lpca_ctx* ctx, const lpca_map_info* info, const doub
     map->density = info->density;
     map->scale = info->scale;
     try {
-      LPCA_CUDA(cudaMalloc(&map->v, sizeof(double) * (info->n * info->k > 0 ? info->n * info->k : 1)));
+      map->alloc_v(ctx->stream, sizeof(double) * (info->n * info->k > 0 ? info->n * info->k : 1));
       if (info->n * info->k > 0)
-        LPCA_CUDA(cudaMemcpy(map->v, v_host, sizeof(double) * info->n * info->k, cudaMemcpyHostToDevice));
+        LPCA_CUDA(cudaMemcpyAsync(map->v, v_host, sizeof(double) * info->n * info->k, cudaMemcpyHostToDevice, ctx->stream));
+      LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
       if (info->has_singular_values && sigma_host) map->sigma.assign(sigma_host, sigma_host + info->k);
     } catch (...) {
       delete map;
@@ -1082,8 +1114,29 @@ lpca_status lpca_dense_aat(lpca_ctx* ctx, const double* f, int64_t l, int64_t n,
   });
 }
 
+static lpca_status eigh_impl(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                             double* evecs, int method);
+
 lpca_status lpca_eigh(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
                       double* evecs) {
+  return eigh_impl(ctx, a, l, location, evals, evecs, 0);
+}
+
+lpca_status lpca_eigh_jacobi(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                             double* evecs) {
+  return eigh_impl(ctx, a, l, location, evals, evecs, 1);
+}
+
+lpca_status lpca_ctx_set_eigensolver(lpca_ctx* ctx, int32_t method) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (method != 0 && method != 1) throw Error(kInvalidArgument, "eigensolver must be 0 (tridiagonal) or 1 (jacobi)");
+    ctx->eigensolver = method;
+  });
+}
+
+static lpca_status eigh_impl(lpca_ctx* ctx, const double* a, int64_t l, int32_t location, double* evals,
+                             double* evecs, int method) {
   return guarded([&] {
     check_ctx(ctx);
     if (l < 0) throw Error(kDimension, "eigh: negative size");
@@ -1093,11 +1146,9 @@ lpca_status lpca_eigh(lpca_ctx* ctx, const double* a, int64_t l, int32_t locatio
     LPCA_CUDA(cudaMemcpyAsync(acopy, ad, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, ctx->stream));
     double* ev = ctx->get<double>("k.evals", l);
     double* vec = location == LPCA_DEVICE ? evecs : ctx->get<double>("k.evecs", l * l);
-    double* work = ctx->get<double>("k.work", 2 * l * l);
     int* st = ctx->get<int>("k.status", 2);
     double* gap = ctx->get<double>("k.gap", 1);
-    launch_jacobi_eigh(ctx->stream, acopy, l, ev, vec, work, st, gap);
-    LPCA_LAUNCHED(*ctx);
+    eigh_dev(*ctx, acopy, l, ev, vec, st, gap, method);
     int hst = 0;
     double hgap = 0;
     LPCA_CUDA(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -243,9 +243,11 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(double* a, index
   }
   if (tid == 0) {
     status[0] = 0;
+    status[1] = sweep;
     gap[0] = off;
   }
 }
+
 
 // V(j, r) = (sum_i F(i, j) U~(i, r)) / sigma_r, i ascending, separate mul/add
 // (truncated_svd.cpp:52-62); sigma_r = sqrt(lambda_r).

@@ -2,33 +2,40 @@
 //
 // Both X-passes of Lazy SPCA are tall-skinny products that stream X (m x n,
 // fp32, row-major) once from HBM:
-//   xw  : OUT = X W      (sketch U = X Omega, power U = X Z, transform Y = X V)
-//   utx : F_part = U^T X (F formation and the power step's Z^T = U^T X)
+//   XW  : OUT = X W        (sketch U = X Omega, power U = X Z, transform Y = X V)
+//   XTU : F^T = X^T U      (F formation and the power step's Z = X^T U)
 // fp32-faithful results need more than one TF32 product (1xTF32
 // misses the 1e-4 singular-value target), so every product is the 3-term split
-//   a*b ~= a_hi*b_hi + a_lo*b_hi + a_hi*b_lo,  a_hi = tf32(a), a_lo = tf32(a - a_hi)
-// accumulated in fp32 in TMEM. The small operand (W, or U^T) arrives pre-split
-// as hi/lo planes; X is split in shared memory by four converter warps after
-// TMA lands each stage, so X is read from HBM exactly once per pass.
+//   a*b ~= a_hi*b_hi + a_lo*b_hi + a_hi*b_lo,  a_hi = tf32(a), a_lo = tf32(a - a_hi).
 //
-// All UMMA operands are K-major with the 128 B swizzle (kind::tf32 with an
-// MN-major operand produced no result on this part in our probes). For utx the
-// reduction runs over X's rows, so the converter warps transpose each raw X
-// tile into the K-major layout while splitting it; the swizzle makes those
-// transposing stores bank-conflict free.
+// Operand placement (one kernel template for both passes):
+//   A = the X tile, M = 128 (XW: 128 rows of X; XTU: 128 columns of X), read
+//       once from HBM by TMA, split into tf32 hi/lo by four converter warps and
+//       written straight into a TMEM ring with tcgen05.st (the MMA reads A from
+//       TMEM, the "TS" form) — XTU's converters transpose while they split.
+//   B = the small operand's pre-split hi/lo planes, K-major [N][K] in shared
+//       memory (XW: W^T planes; XTU: U^T planes), N = round_up(w, 16).
+// With A in TMEM the tensor core reads only B from shared memory (42 KB per
+// 32-deep stage at N = 112, plus the converters' 16 KB), under the MMA time of
+// the stage; with A in shared memory as well it was smem-bandwidth bound
+// (90 KB of operand reads per stage; ncu: tensor pipe 51% active).
 //
-// Warp roles (one CTA per SM):
+// Accumulation: the tensor core's fp32 accumulation rounds toward zero
+// (measured bias ~ -5e-8 of the running sum per K=8 step, -2.6e-5 at K=4096).
+// MMAs accumulate runs of kRunStages stages (K = 128) into a TMEM run buffer;
+// epilogue warps fold each run into a TMEM-resident long accumulator with
+// round-to-nearest fp32 adds, so the bias stays ~1e-6 for any K.
+//
+// Warp roles (one CTA per SM, persistent over work items):
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      MMA issuer (one lane) + TMEM allocator
-//   warps 2-5   split converters (128 threads)
-//   warps 6-9   epilogue (TMEM -> registers -> global), one TMEM lane quarter each
-// Pipelines: smem full/conv/empty ring (TMA -> convert -> MMA), and a
-// double-buffered TMEM accumulator (MMA -> epilogue) so one tile's epilogue
-// overlaps the next tile's MMAs.
+//   warps 2-5   split converters: smem X tile -> TMEM A hi/lo (one lane quarter each)
+//   warps 6-9   epilogue: TMEM -> registers -> global (one lane quarter each)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "kernels.cuh"
@@ -41,28 +48,34 @@ namespace {
 using namespace tc;
 
 constexpr int kThreads = 320;
-constexpr int kBM = 128;         // UMMA M
-constexpr int kBK = 32;          // K per stage: 32 fp32 = one 128 B swizzle row
-constexpr uint32_t kSmemBudget = 200 * 1024;
-// The tensor core's fp32 accumulation rounds toward zero: measured bias about
-// -5e-8 of the running sum per K=8 step (-2.6e-5 at K = 4096). MMAs therefore
-// accumulate runs of at most kRunStages stages (K = 128, 16 steps) into a TMEM
-// run buffer; epilogue warps fold runs into a TMEM-resident long accumulator
-// with round-to-nearest fp32 adds, so the bias stays ~1e-6 for any K.
+constexpr int kBM = 128;  // UMMA M (A rows = TMEM lanes)
+constexpr int kBK = 32;   // K per stage
 constexpr int kRunStages = 4;
+constexpr uint32_t kSmemBudget = 200 * 1024;
 
-__device__ __forceinline__ void split4(float4& v, float4& lo) {
-  float4 h;
-  h.x = tf32_trunc(v.x);
-  h.y = tf32_trunc(v.y);
-  h.z = tf32_trunc(v.z);
-  h.w = tf32_trunc(v.w);
-  lo.x = tf32_trunc(v.x - h.x);
-  lo.y = tf32_trunc(v.y - h.y);
-  lo.z = tf32_trunc(v.z - h.z);
-  lo.w = tf32_trunc(v.w - h.w);
-  v = h;
-}
+enum Mode : int { kXW = 0, kXTU = 1 };
+
+struct TcArgs {
+  int m, n;          // X is m x n
+  int npad;          // UMMA N
+  int stages;        // smem ring depth
+  int aslots;        // TMEM A ring depth (each slot: 64 columns, hi + lo)
+  int nrb;           // TMEM run buffers
+  uint32_t tmem_cols;
+  int items;         // work items (XW: row tiles; XTU: n tiles x row chunks)
+  int chunks;        // XTU: row chunks per n tile
+  int chunk_rows;    // XTU: rows per chunk (multiple of kBK)
+  // XW outputs
+  int wstore;        // columns of `out` stored
+  float* out;        // plain fp32 row-major, ld ldo (nullable)
+  int ldo;
+  float* out_hi;     // tf32 planes of OUT^T: [npad][ldh] (nullable)
+  float* out_lo;
+  int ldh;
+  // XTU output: part[chunk][j * l + r] (fp64), r < l
+  double* part;
+  int l;
+};
 
 __device__ __forceinline__ void ring_advance(int& stage, uint32_t& phase, int S) {
   if (++stage == S) {
@@ -71,47 +84,51 @@ __device__ __forceinline__ void ring_advance(int& stage, uint32_t& phase, int S)
   }
 }
 
-// ------------------------------------------------------------------------------------
-// xw: OUT[m x npad] = X[m x K] * W, W given as K-major hi/lo planes [npad][K].
-// Persistent over 128-row tiles of X.
-struct XwArgs {
-  int m, kdim, npad, stages;
-  int nrb;         // TMEM run buffers (2 when 3 * npad columns fit, else 1)
-  uint32_t tmem_cols;
-  int wstore;      // columns of `out` stored (<= npad)
-  float* out;      // plain fp32, row-major, ld ldo (nullable)
-  int ldo;
-  float* out_hi;   // tf32 planes of OUT^T: [npad][ldh] (nullable)
-  float* out_lo;
-  int ldh;
-};
+// Work item -> (X tile origin along M, K range).
+template <int kMode>
+__device__ __forceinline__ void item_coords(const TcArgs& a, int item, int& t0, int& k0, int& k1) {
+  if (kMode == kXW) {
+    t0 = item * kBM;  // first row
+    k0 = 0;
+    k1 = a.n;
+  } else {
+    const int nt = item / a.chunks, ch = item % a.chunks;
+    t0 = nt * kBM;  // first column
+    k0 = ch * a.chunk_rows;
+    k1 = min(a.m, k0 + a.chunk_rows);
+  }
+}
 
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
-    xw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmwh,
-                 const __grid_constant__ CUtensorMap tmwl, XwArgs a) {
+    tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
+              const __grid_constant__ CUtensorMap tmbl, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = a.stages;
-  constexpr uint32_t a_bytes = kBM * kBK * 4;  // 16 KB
+  const int S = a.stages, AS = a.aslots;
+  constexpr uint32_t x_bytes = kBM * kBK * 4;  // 16 KB X tile
   const uint32_t b_bytes = static_cast<uint32_t>(a.npad) * kBK * 4;
-  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  const uint32_t stage_bytes = x_bytes + 2 * b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + S;
-  uint64_t* empty = bars + 2 * S;
-  uint64_t* tfull = bars + 3 * S;
-  uint64_t* tempty = tfull + 2;
+  uint64_t* full = bars;            // S: TMA landed (X + B planes)
+  uint64_t* empty = full + S;       // S: MMAs done with the smem stage
+  uint64_t* conv = empty + S;       // AS: A slot written to TMEM
+  uint64_t* aempty = conv + AS;     // AS: MMAs done with the A slot
+  uint64_t* tfull = aempty + AS;    // 2: run accumulated
+  uint64_t* tempty = tfull + 2;     // 2: run buffer drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int num_tiles = (a.m + kBM - 1) / kBM;
-  const int kiters = (a.kdim + kBK - 1) / kBK;
+  const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);  // A ring after the accumulators
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&conv[s], 4);
+      mbar_init(&aempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -119,8 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
     tma_prefetch(&tmx);
-    tma_prefetch(&tmwh);
-    tma_prefetch(&tmwl);
+    tma_prefetch(&tmbh);
+    tma_prefetch(&tmbl);
   }
   if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
   tc_fence_before();
@@ -129,85 +146,125 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        for (int kb = 0; kb < kiters; ++kb) {
+      for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+        int t0, k0, k1;
+        item_coords<kMode>(a, item, t0, k0, k1);
+        for (int k = k0; k < k1; k += kBK) {
           mbar_wait(&empty[stage], phase ^ 1, 1);
           uint8_t* st = smem + stage * stage_bytes;
-          mbar_expect_tx(&full[stage], a_bytes + 2 * b_bytes);
-          tma_load_2d(st, &tmx, &full[stage], kb * kBK, tile * kBM);
-          tma_load_2d(st + 2 * a_bytes, &tmwh, &full[stage], kb * kBK, 0);
-          tma_load_2d(st + 2 * a_bytes + b_bytes, &tmwl, &full[stage], kb * kBK, 0);
+          mbar_expect_tx(&full[stage], x_bytes + 2 * b_bytes);
+          if (kMode == kXW)
+            tma_load_2d(st, &tmx, &full[stage], k, t0);  // rows t0.., cols k..
+          else
+            tma_load_2d(st, &tmx, &full[stage], t0, k);  // cols t0.., rows k..
+          tma_load_2d(st + x_bytes, &tmbh, &full[stage], k, 0);
+          tma_load_2d(st + x_bytes + b_bytes, &tmbl, &full[stage], k, 0);
           ring_advance(stage, phase, S);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(kBM, a.npad, 0, 0);
-      int stage = 0, rc = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        for (int kb0 = 0; kb0 < kiters; kb0 += kRunStages, ++rc) {
-          const int b = rc % a.nrb;
-          mbar_wait(&tempty[b], ((rc / a.nrb) & 1) ^ 1, 2);
+    // ---------------- MMA issuer ----------------
+    // The whole warp walks the schedule (so every value below is warp-uniform)
+    // and one elected lane issues each stage's 12 MMAs + commits in one go.
+    const uint32_t idesc = idesc_tf32(kBM, a.npad, 0, 0);
+    const uint64_t desc0 = sw128_desc(smem_u32(smem) + x_bytes, 16, 1024);
+    int stage = 0, aslot = 0, rc = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+      int t0, k0, k1;
+      item_coords<kMode>(a, item, t0, k0, k1);
+      for (int q0 = k0; q0 < k1; q0 += kRunStages * kBK, ++rc) {
+        const int b = rc % a.nrb;
+        mbar_wait(&tempty[b], ((rc / a.nrb) & 1) ^ 1, 2);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(b * a.npad);
+        const int q1 = min(k1, q0 + kRunStages * kBK);
+        for (int k = q0; k < q1; k += kBK) {
+          mbar_wait(&conv[aslot], aphase, 3);
+          mbar_wait(&full[stage], phase, 3);
           tc_fence_after();
-          const uint32_t d = tmem_base + static_cast<uint32_t>(b * a.npad);
-          const int kb1 = min(kiters, kb0 + kRunStages);
-          for (int kb = kb0; kb < kb1; ++kb) {
-            mbar_wait(&conv[stage], phase, 3);
-            tc_fence_after();
-            const uint32_t ah = smem_u32(smem + stage * stage_bytes);
-            const uint32_t al = ah + a_bytes, bh = ah + 2 * a_bytes, bl = bh + b_bytes;
-#pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
-              const uint32_t off = kk * 32;  // 8 tf32 of K inside the 128 B swizzled row
-              const uint64_t dah = sw128_desc(ah + off, 16, 1024), dal = sw128_desc(al + off, 16, 1024);
-              const uint64_t dbh = sw128_desc(bh + off, 16, 1024), dbl = sw128_desc(bl + off, 16, 1024);
-              mma_tf32(d, dah, dbh, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
-              mma_tf32(d, dal, dbh, idesc, 1u);
-              mma_tf32(d, dah, dbl, idesc, 1u);
-            }
+          // descriptor start address advances in 16 B units
+          const uint64_t bh = desc0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
+          const uint64_t bl = bh + static_cast<uint64_t>(b_bytes >> 4);
+          const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+          if (elect_one()) {
+            mma_stage_ts(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u);
             mma_commit(&empty[stage]);
-            ring_advance(stage, phase, S);
+            mma_commit(&aempty[aslot]);
           }
-          mma_commit(&tfull[b]);
+          __syncwarp();
+          ring_advance(stage, phase, S);
+          ring_advance(aslot, aphase, AS);
         }
+        if (elect_one()) mma_commit(&tfull[b]);
+        __syncwarp();
       }
     }
   } else if (warp < 6) {
-    const int t = threadIdx.x - 64;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < kiters; ++kb) {
+    // ---------------- converters: smem X -> TMEM A (hi, lo) ----------------
+    const int q = warp & 3;
+    const int i = q * 32 + lane;  // A row = TMEM lane
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    int stage = 0, aslot = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+      int t0, k0, k1;
+      item_coords<kMode>(a, item, t0, k0, k1);
+      for (int k = k0; k < k1; k += kBK) {
         mbar_wait(&full[stage], phase, 4);
-        float4* hi = reinterpret_cast<float4*>(smem + stage * stage_bytes);
-        float4* lo = reinterpret_cast<float4*>(smem + stage * stage_bytes + a_bytes);
+        mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+        tc_fence_after();
+        const uint8_t* xt = smem + stage * stage_bytes;
+        float v[32];
+        if (kMode == kXW) {
+          // row i of a 128 B-swizzled [128][32] tile: 16 B chunk c at (c ^ (i & 7))
 #pragma unroll
-        for (int i = 0; i < static_cast<int>(a_bytes / 16 / 128); ++i) {
-          const int idx = t + 128 * i;
-          float4 v = hi[idx], l4;
-          split4(v, l4);
-          hi[idx] = v;
-          lo[idx] = l4;
+          for (int c = 0; c < 8; ++c) {
+            const float4 f = *reinterpret_cast<const float4*>(xt + i * 128 + ((c ^ (i & 7)) << 4));
+            v[4 * c] = f.x;
+            v[4 * c + 1] = f.y;
+            v[4 * c + 2] = f.z;
+            v[4 * c + 3] = f.w;
+          }
+        } else {
+          // column i of a plain [32][128] tile
+          const float* raw = reinterpret_cast<const float*>(xt);
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
         }
-        fence_proxy_async_smem();
+        float hi[32], lo[32];
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) {
+          hi[kk] = tf32_trunc(v[kk]);
+          lo[kk] = tf32_trunc(v[kk] - hi[kk]);
+        }
+        const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+        tmem_st32(at, hi);
+        tmem_st32(at + 32, lo);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (lane == 0) mbar_arrive(&conv[aslot]);
         ring_advance(stage, phase, S);
+        ring_advance(aslot, aphase, AS);
       }
     }
   } else {
+    // ---------------- epilogue ----------------
     const int q = warp & 3;
-    const int runs = (kiters + kRunStages - 1) / kRunStages;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t lacc = lane_base + static_cast<uint32_t>(a.nrb * a.npad);  // long accumulator
+    const uint32_t lacc = lane_base + static_cast<uint32_t>(a.nrb * a.npad);
     int rc = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int row = tile * kBM + q * 32 + lane;
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+      int t0, k0, k1;
+      item_coords<kMode>(a, item, t0, k0, k1);
+      const int runs = (k1 - k0 + kRunStages * kBK - 1) / (kRunStages * kBK);
+      const int row = t0 + q * 32 + lane;  // XW: X row; XTU: X column j
       for (int r = 0; r < runs; ++r, ++rc) {
         const int b = rc % a.nrb;
         mbar_wait(&tfull[b], (rc / a.nrb) & 1, 5);
@@ -217,249 +274,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < a.npad; c0 += 16) {
           float v[16];
           tmem_ld16(racc + c0, v);
-          if (!first) {  // fold the run into the long accumulator, round-to-nearest
+          if (!first) {
             float s[16];
             tmem_ld16(lacc + c0, s);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], s[i]);
+            for (int e = 0; e < 16; ++e) v[e] = __fadd_rn(v[e], s[e]);
           }
           if (!last) {
             tmem_st16(lacc + c0, v);
             continue;
           }
-          if (row < a.m) {
-            if (a.out_hi) {
-              // transposed tf32 planes (OUT^T, [npad][ldh]): one row per lane, so
-              // each column store of the warp is 32 consecutive floats (coalesced)
+          if (kMode == kXW) {
+            if (row < a.m) {
+              if (a.out_hi) {
+                // transposed planes [npad][ldh]: one row per lane -> coalesced columns
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float h = tf32_trunc(v[i]);
-                a.out_hi[static_cast<size_t>(c0 + i) * a.ldh + row] = h;
-                a.out_lo[static_cast<size_t>(c0 + i) * a.ldh + row] = tf32_trunc(v[i] - h);
-              }
-            }
-            if (a.out) {
-              float* po = a.out + static_cast<size_t>(row) * a.ldo;
-#pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (c0 + i < a.wstore) po[c0 + i] = v[i];
-            }
-          }
-        }
-        if (!last) tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[b]);
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, a.tmem_cols);
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// utx: part[s][j*l + r] = sum over the rows of split s of U[i, r] X[i, j].
-// A = U^T from K-major tf32 planes [lpad][ldt] (as the sketch epilogue writes
-// them), B = X^T tiles made K-major by the converters, K = rows of X. A CTA
-// owns (n tile, row split); it accumulates `flush_rows` rows at a time in fp32
-// in TMEM and folds each segment into its own fp64 slot of `part` (the first
-// segment stores), so fp32 run lengths stay bounded and every cross-segment and
-// cross-split sum is fp64 in a fixed order.
-struct UtxArgs {
-  int m, l, n;
-  int mhalves;  // 1: l <= 128; 2: l <= 256 (two M = 128 halves sharing B)
-  int bn;       // UMMA N = n tile (128 or 64)
-  int rows_per_split, flush_rows, stages;
-  uint32_t tmem_cols;
-  double* part;
-};
-
-__global__ void __launch_bounds__(kThreads, 1)
-    utx_tc_kernel(const __grid_constant__ CUtensorMap tmuh, const __grid_constant__ CUtensorMap tmul,
-                  const __grid_constant__ CUtensorMap tmx, UtxArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = a.stages;
-  const uint32_t a_half = kBM * kBK * 4;                      // 16 KB per M half
-  const uint32_t a_bytes = a.mhalves * a_half;                // per plane
-  const uint32_t b_bytes = static_cast<uint32_t>(a.bn) * kBK * 4;  // per plane, K-major
-  const uint32_t raw_bytes = b_bytes;                         // raw X tile [32][bn]
-  const uint32_t stage_bytes = 2 * a_bytes + 3 * b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + S;
-  uint64_t* empty = bars + 2 * S;
-  uint64_t* tfull = bars + 3 * S;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n0 = blockIdx.x * a.bn;
-  const int split = blockIdx.y;
-  const int r_begin = split * a.rows_per_split;
-  const int r_end = min(a.m, r_begin + a.rows_per_split);
-  const int nseg = r_end > r_begin ? (r_end - r_begin + a.flush_rows - 1) / a.flush_rows : 0;
-  const uint32_t buf_cols = static_cast<uint32_t>(a.mhalves * a.bn);
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
-    }
-    fence_barrier_init();
-    tma_prefetch(&tmuh);
-    tma_prefetch(&tmul);
-    tma_prefetch(&tmx);
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int sg = 0; sg < nseg; ++sg) {
-        const int s0 = r_begin + sg * a.flush_rows;
-        const int s1 = min(r_end, s0 + a.flush_rows);
-        for (int row = s0; row < s1; row += kBK) {
-          mbar_wait(&empty[stage], phase ^ 1, 11);
-          uint8_t* st = smem + stage * stage_bytes;
-          mbar_expect_tx(&full[stage], 2 * a_bytes + raw_bytes);
-          for (int h = 0; h < a.mhalves; ++h) {
-            tma_load_2d(st + h * a_half, &tmuh, &full[stage], row, h * kBM);
-            tma_load_2d(st + a_bytes + h * a_half, &tmul, &full[stage], row, h * kBM);
-          }
-          tma_load_2d(st + 2 * a_bytes + 2 * b_bytes, &tmx, &full[stage], n0, row);
-          ring_advance(stage, phase, S);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(kBM, a.bn, 0, 0);
-      int stage = 0, rc = 0;
-      uint32_t phase = 0;
-      for (int sg = 0; sg < nseg; ++sg) {
-        const int s0 = r_begin + sg * a.flush_rows;
-        const int s1 = min(r_end, s0 + a.flush_rows);
-        for (int q0 = s0; q0 < s1; q0 += kRunStages * kBK, ++rc) {
-          const int b = rc & 1;
-          mbar_wait(&tempty[b], ((rc >> 1) & 1) ^ 1, 12);
-          tc_fence_after();
-          const int q1 = min(s1, q0 + kRunStages * kBK);
-          for (int row = q0; row < q1; row += kBK) {
-            mbar_wait(&conv[stage], phase, 13);
-            tc_fence_after();
-            const uint32_t ah = smem_u32(smem + stage * stage_bytes);
-            const uint32_t al = ah + a_bytes, bh = ah + 2 * a_bytes, bl = bh + b_bytes;
-#pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
-              const uint32_t off = kk * 32;
-              const uint64_t dbh = sw128_desc(bh + off, 16, 1024), dbl = sw128_desc(bl + off, 16, 1024);
-              for (int h = 0; h < a.mhalves; ++h) {
-                const uint64_t dah = sw128_desc(ah + h * a_half + off, 16, 1024);
-                const uint64_t dal = sw128_desc(al + h * a_half + off, 16, 1024);
-                const uint32_t d = tmem_base + b * buf_cols + h * a.bn;
-                mma_tf32(d, dah, dbh, idesc, (row != q0 || kk != 0) ? 1u : 0u);
-                mma_tf32(d, dal, dbh, idesc, 1u);
-                mma_tf32(d, dah, dbl, idesc, 1u);
-              }
-            }
-            mma_commit(&empty[stage]);
-            ring_advance(stage, phase, S);
-          }
-          mma_commit(&tfull[b]);
-        }
-      }
-    }
-  } else if (warp < 6) {
-    // transpose + split: raw[k][j] (k = row in the stage, j = column of the n
-    // tile) -> K-major SW128 planes, row j holding its 32 k values in 128 B with
-    // 16 B chunk c stored at chunk (c ^ (j & 7)).
-    const int t = threadIdx.x - 64;
-    const int groups = 128 / a.bn;  // threads per n column (1 or 2)
-    const int j = t % a.bn, g = t / a.bn;
-    const int kper = kBK / groups;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const int s0 = r_begin + sg * a.flush_rows;
-      const int s1 = min(r_end, s0 + a.flush_rows);
-      for (int row = s0; row < s1; row += kBK) {
-        mbar_wait(&full[stage], phase, 14);
-        uint8_t* st = smem + stage * stage_bytes;
-        const float* raw = reinterpret_cast<const float*>(st + 2 * a_bytes + 2 * b_bytes);
-        uint8_t* bh = st + 2 * a_bytes;
-        uint8_t* bl = bh + b_bytes;
-        for (int c4 = 0; c4 < kper / 4; ++c4) {
-          const int k0 = g * kper + c4 * 4;
-          float4 v = make_float4(raw[(k0 + 0) * a.bn + j], raw[(k0 + 1) * a.bn + j],
-                                 raw[(k0 + 2) * a.bn + j], raw[(k0 + 3) * a.bn + j]);
-          float4 l4;
-          split4(v, l4);
-          const uint32_t off = static_cast<uint32_t>(j) * 128 + ((((k0 >> 2) ^ (j & 7))) << 4);
-          *reinterpret_cast<float4*>(bh + off) = v;
-          *reinterpret_cast<float4*>(bl + off) = l4;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
-        ring_advance(stage, phase, S);
-      }
-    }
-  } else {
-    const int q = warp & 3;
-    double* dst = a.part + static_cast<size_t>(split) * a.l * a.n;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t lacc = lane_base + 2 * buf_cols;  // long accumulator
-    int rc = 0;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const int s0 = r_begin + sg * a.flush_rows;
-      const int s1 = min(r_end, s0 + a.flush_rows);
-      const int runs = (s1 - s0 + kRunStages * kBK - 1) / (kRunStages * kBK);
-      for (int rr = 0; rr < runs; ++rr, ++rc) {
-        const int b = rc & 1;
-        mbar_wait(&tfull[b], (rc >> 1) & 1, 15);
-        tc_fence_after();
-        const bool first = rr == 0, last = rr == runs - 1;
-        for (int h = 0; h < a.mhalves; ++h) {
-          const int r = h * kBM + q * 32 + lane;
-          const uint32_t racc = lane_base + b * buf_cols + h * a.bn;
-          const uint32_t lh = lacc + h * a.bn;
-          for (int c0 = 0; c0 < a.bn; c0 += 16) {
-            float v[16];
-            tmem_ld16(racc + c0, v);
-            if (!first) {
-              float s[16];
-              tmem_ld16(lh + c0, s);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], s[i]);
-            }
-            if (!last) {
-              tmem_st16(lh + c0, v);
-              continue;
-            }
-            if (r < a.l) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const int jj = n0 + c0 + i;
-                if (jj < a.n) {
-                  double* p = dst + static_cast<size_t>(jj) * a.l + r;
-                  *p = sg == 0 ? static_cast<double>(v[i]) : *p + static_cast<double>(v[i]);
+                for (int e = 0; e < 16; ++e) {
+                  const float h = tf32_trunc(v[e]);
+                  a.out_hi[static_cast<size_t>(c0 + e) * a.ldh + row] = h;
+                  a.out_lo[static_cast<size_t>(c0 + e) * a.ldh + row] = tf32_trunc(v[e] - h);
                 }
               }
+              if (a.out) {
+                float* po = a.out + static_cast<size_t>(row) * a.ldo;
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  if (c0 + e < a.wstore) po[c0 + e] = v[e];
+              }
             }
+          } else if (row < a.n) {
+            // F^T row j = F column j: part[chunk][j * l + r]
+            double* p = a.part + static_cast<size_t>(item % a.chunks) * a.l * a.n + static_cast<size_t>(row) * a.l;
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (c0 + e < a.l) p[c0 + e] = static_cast<double>(v[e]);
           }
         }
         if (!last) tmem_st_wait();
@@ -512,45 +360,70 @@ uint32_t tmem_cols_for(uint32_t need) {
   return c;
 }
 
-int utx_bn(index_t l) { return l <= 128 ? 128 : 64; }
+// TMEM plan: run buffers + long accumulator + A ring (64 columns per slot).
+bool plan_tmem(int npad, TcArgs& a) {
+  const char* env_nrb = getenv("LPCA_TC_NRB");
+  const char* env_as = getenv("LPCA_TC_ASLOTS");
+  const int max_nrb = env_nrb ? atoi(env_nrb) : 2;
+  const int max_as = env_as ? atoi(env_as) : 2;
+  for (int nrb = max_nrb; nrb >= 1; --nrb) {
+    const int acc = (nrb + 1) * npad;
+    const int slots = (512 - acc) / 64;
+    if (slots >= 1) {
+      a.nrb = nrb;
+      a.aslots = slots > max_as ? max_as : slots;
+      a.tmem_cols = tmem_cols_for(static_cast<uint32_t>(acc + 64 * a.aslots));
+      return true;
+    }
+  }
+  return false;
+}
+
+template <int kMode>
+void launch(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, TcArgs& a,
+            int grid) {
+  const uint32_t stage_bytes = kBM * kBK * 4 + 2 * static_cast<uint32_t>(a.npad) * kBK * 4;
+  a.stages = static_cast<int>(kSmemBudget / stage_bytes);
+  if (a.stages > 6) a.stages = 6;
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 256;
+  LPCA_CUDA(cudaFuncSetAttribute(tc_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  tc_kernel<kMode><<<grid, kThreads, smem, s>>>(tx, th, tl, a);
+}
 
 }  // namespace
 
-bool tc_xw_supported(index_t n, index_t wpad) { return wpad >= 16 && wpad <= 256 && wpad % 16 == 0 && n >= 1; }
+bool tc_xw_supported(index_t n, index_t wpad) {
+  TcArgs a{};
+  return wpad >= 16 && wpad <= 256 && wpad % 16 == 0 && n >= 1 && plan_tmem(static_cast<int>(wpad), a);
+}
 
-bool tc_utx_supported(index_t l, index_t n) { return l >= 1 && l <= 256 && n >= 1; }
+bool tc_utx_supported(index_t l, index_t n) { return l >= 1 && n >= 1 && tc_xw_supported(1, round_up(l, 16)); }
 
 void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
                          const float* w_hi, const float* w_lo, index_t wpad, index_t ldw, float* out,
                          index_t ldo, index_t wstore, float* out_hi, float* out_lo, index_t ldh,
                          int num_sms) {
   if (m <= 0) return;
-  if (!tc_xw_supported(n, wpad)) throw Error(kInternal, "xw_tc: unsupported shape");
+  TcArgs a{};
+  if (!tc_xw_supported(n, wpad) || !plan_tmem(static_cast<int>(wpad), a))
+    throw Error(kInternal, "xw_tc: unsupported shape");
   if (ldx % 4 || ldw % 4 || (out_hi && ldh % 4))
     throw Error(kInternal, "xw_tc: leading dimensions must be multiples of 4 floats");
   const CUtensorMap tx = map_2d(x, n, m, ldx, 32, kBM, true);
   const CUtensorMap th = map_2d(w_hi, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
   const CUtensorMap tl = map_2d(w_lo, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
-  XwArgs a{};
   a.m = static_cast<int>(m);
-  a.kdim = static_cast<int>(n);
+  a.n = static_cast<int>(n);
   a.npad = static_cast<int>(wpad);
-  const uint32_t stage_bytes = 2 * kBM * kBK * 4 + 2 * static_cast<uint32_t>(wpad) * kBK * 4;
-  a.stages = static_cast<int>(kSmemBudget / stage_bytes);
-  if (a.stages > 6) a.stages = 6;
-  a.nrb = 3 * wpad <= 512 ? 2 : 1;
-  a.tmem_cols = tmem_cols_for(static_cast<uint32_t>((a.nrb + 1) * wpad));
+  a.items = static_cast<int>(ceil_div(m, kBM));
+  a.chunks = 1;
   a.wstore = static_cast<int>(wstore);
   a.out = out;
   a.ldo = static_cast<int>(ldo);
   a.out_hi = out_hi;
   a.out_lo = out_lo;
   a.ldh = static_cast<int>(ldh);
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 256;
-  LPCA_CUDA(cudaFuncSetAttribute(xw_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const index_t tiles = ceil_div(m, kBM);
-  const int grid = static_cast<int>(tiles < num_sms ? tiles : num_sms);
-  xw_tc_kernel<<<grid, kThreads, smem, s>>>(tx, th, tl, a);
+  launch<kXW>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 
 void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx, const float* w_hi,
@@ -558,46 +431,41 @@ void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t 
   launch_xw_tc_planes(s, x, m, n, ldx, w_hi, w_lo, wpad, ldw, out, ldo, wpad, nullptr, nullptr, 0, num_sms);
 }
 
+// Row chunks per n tile so that tiles x chunks spreads evenly over the CTAs.
 index_t utx_tc_splits(index_t m, index_t l, index_t n, int num_sms, index_t* rows_per_split) {
-  const index_t ntiles = ceil_div(n, utx_bn(l));
-  index_t splits = num_sms / ntiles;
-  if (splits < 1) splits = 1;
-  const index_t max_splits = ceil_div(m, kBK);
-  if (splits > max_splits) splits = max_splits;
-  index_t rps = round_up(ceil_div(m, splits), kBK);
-  splits = ceil_div(m, rps);
-  *rows_per_split = rps;
-  return splits;
+  (void)l;
+  const index_t ntiles = ceil_div(n, kBM);
+  index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms), ntiles);  // ~8 items per CTA
+  const index_t max_chunks = ceil_div(m, 4 * kRunStages * kBK);          // >= 4 runs per item
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  const index_t rows = round_up(ceil_div(m, chunks), kBK);
+  chunks = ceil_div(m, rows);
+  *rows_per_split = rows;
+  return chunks;
 }
 
 void launch_utx_tc_planes(cudaStream_t s, const float* ut_hi, const float* ut_lo, index_t ldt, const float* x,
                           index_t ldx, index_t m, index_t l, index_t n, double* part, int num_sms) {
-  if (!tc_utx_supported(l, n)) throw Error(kInternal, "utx_tc: unsupported shape");
+  TcArgs a{};
+  const index_t npad = round_up(l, 16);
+  if (!tc_utx_supported(l, n) || !plan_tmem(static_cast<int>(npad), a))
+    throw Error(kInternal, "utx_tc: unsupported shape");
   if (ldt % 4 || ldx % 4) throw Error(kInternal, "utx_tc: leading dimensions must be multiples of 4 floats");
-  UtxArgs a{};
+  index_t rows = 0;
+  const index_t chunks = utx_tc_splits(m, l, n, num_sms, &rows);
   a.m = static_cast<int>(m);
-  a.l = static_cast<int>(l);
   a.n = static_cast<int>(n);
-  a.mhalves = l <= 128 ? 1 : 2;
-  a.bn = utx_bn(l);
-  index_t rps = 0;
-  const index_t splits = utx_tc_splits(m, l, n, num_sms, &rps);
-  a.rows_per_split = static_cast<int>(rps);
-  a.flush_rows = 8192;
-  const uint32_t stage_bytes = 2 * static_cast<uint32_t>(a.mhalves) * kBM * kBK * 4 +
-                               3 * static_cast<uint32_t>(a.bn) * kBK * 4;
-  a.stages = static_cast<int>(kSmemBudget / stage_bytes);
-  if (a.stages > 6) a.stages = 6;
-  a.tmem_cols = tmem_cols_for(3 * static_cast<uint32_t>(a.mhalves * a.bn));
+  a.npad = static_cast<int>(npad);
+  a.chunks = static_cast<int>(chunks);
+  a.chunk_rows = static_cast<int>(rows);
+  a.items = static_cast<int>(ceil_div(n, kBM) * chunks);
   a.part = part;
-  const index_t lrows = round_up(l, 16);  // rows of the U^T planes
-  const CUtensorMap th = map_2d(ut_hi, m, lrows, ldt, 32, kBM, true);
-  const CUtensorMap tl = map_2d(ut_lo, m, lrows, ldt, 32, kBM, true);
-  const CUtensorMap tx = map_2d(x, n, m, ldx, static_cast<uint32_t>(a.bn), kBK, false);
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 256;
-  LPCA_CUDA(cudaFuncSetAttribute(utx_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  dim3 grid(static_cast<unsigned>(ceil_div(n, a.bn)), static_cast<unsigned>(splits));
-  utx_tc_kernel<<<grid, kThreads, smem, s>>>(th, tl, tx, a);
+  a.l = static_cast<int>(l);
+  const CUtensorMap tx = map_2d(x, n, m, ldx, kBM, kBK, false);
+  const CUtensorMap th = map_2d(ut_hi, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
+  const CUtensorMap tl = map_2d(ut_lo, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
+  launch<kXTU>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 
 void launch_utx_tc(cudaStream_t, const float*, index_t, const float*, index_t, index_t, index_t, index_t,

@@ -98,6 +98,51 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem], kind::tf32 ("TS" form: A is 128 lanes x K
+// columns of TMEM starting at a_tmem), issued by one thread.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+// One K=32 stage of the 3-term split in a single asm block (12 MMAs): for kk in
+// 0..3, A columns at a_hi + 8kk / a_lo + 8kk, B descriptors advanced by 32 B
+// (2 in the descriptor's 16 B units). Issued by the calling (elected) thread;
+// one block keeps ptxas from re-electing and re-broadcasting per instruction.
+__device__ __forceinline__ void mma_stage_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                             uint32_t idesc, uint32_t acc_first) {
+  asm volatile(
+      "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, {%7, %7, %7, %7}, p;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, {%7, %7, %7, %7}, t;\n"
+      " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"
+      " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %5, {%7, %7, %7, %7}, t;\n"
+      " add.u32 ah, %1, 16;\n add.u32 al, %2, 16;\n add.u64 dh, %3, 4;\n add.u64 dl, %4, 4;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %5, {%7, %7, %7, %7}, t;\n"
+      " add.u32 ah, %1, 24;\n add.u32 al, %2, 24;\n add.u64 dh, %3, 6;\n add.u64 dl, %4, 6;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %5, {%7, %7, %7, %7}, t;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %5, {%7, %7, %7, %7}, t;\n"
+      "}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // Arrives on `bar` once all previously issued MMAs of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -130,6 +175,19 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 32 lanes x 32 consecutive 32-bit columns.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+#define LPCA_U(i) "r"(__float_as_uint(v[i]))
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      LPCA_U(0), LPCA_U(1), LPCA_U(2), LPCA_U(3), LPCA_U(4), LPCA_U(5), LPCA_U(6), LPCA_U(7), LPCA_U(8),
+      LPCA_U(9), LPCA_U(10), LPCA_U(11), LPCA_U(12), LPCA_U(13), LPCA_U(14), LPCA_U(15), LPCA_U(16),
+      LPCA_U(17), LPCA_U(18), LPCA_U(19), LPCA_U(20), LPCA_U(21), LPCA_U(22), LPCA_U(23), LPCA_U(24),
+      LPCA_U(25), LPCA_U(26), LPCA_U(27), LPCA_U(28), LPCA_U(29), LPCA_U(30), LPCA_U(31)
+      : "memory");
+#undef LPCA_U
+}
 
 // ---- descriptors ------------------------------------------------------------------------
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits (46..47 = 1).

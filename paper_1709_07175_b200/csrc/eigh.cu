@@ -257,8 +257,8 @@ __device__ __forceinline__ double hash_uniform(unsigned j, unsigned i) {
 // field f, row i -> scratch[(f * l + i) * l + j]; fields DL, D, DU, DU2, b.
 struct Scr {
   double* base;
-  int l, j;
-  __device__ double& at(int f, int i) const { return base[(static_cast<size_t>(f) * l + i) * l + j]; }
+  int l, j, stride;  // element (f, i) of thread j at base[(f * l + i) * stride + j]
+  __device__ double& at(int f, int i) const { return base[(static_cast<size_t>(f) * l + i) * stride + j]; }
 };
 
 // (T - lam I) x = b by pivoted LU (the dgttrf/dgttrs recurrences), b overwritten.
@@ -323,7 +323,10 @@ __device__ __forceinline__ bool same_cluster(double a, double b, double tn) {
 __global__ void invit_kernel(const double* __restrict__ d, const double* __restrict__ e, int l,
                              const double* __restrict__ evals, const double* __restrict__ tnorm,
                              double* __restrict__ scratch, unsigned char* __restrict__ pivs,
-                             double* __restrict__ y) {
+                             double* __restrict__ y, int smem_threads) {
+  // LU scratch: in shared memory (5 l doubles + l pivots per thread) when the
+  // block fits, else the interleaved global buffer.
+  extern __shared__ double sh_scr[];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= l) return;
   const double tn = tnorm[0] > 0.0 ? tnorm[0] : 1.0;  // zero matrix: any orthonormal basis
@@ -331,8 +334,11 @@ __global__ void invit_kernel(const double* __restrict__ d, const double* __restr
   if (j > 0 && same_cluster(evals[j - 1], evals[j], tn)) return;
   int end = j + 1;
   while (end < l && same_cluster(evals[end - 1], evals[end], tn)) ++end;
-  const Scr s{scratch, l, j};
-  unsigned char* piv = pivs + static_cast<size_t>(j) * l;
+  const Scr s = smem_threads ? Scr{sh_scr, l, static_cast<int>(threadIdx.x), smem_threads} : Scr{scratch, l, j, l};
+  unsigned char* piv = smem_threads
+                           ? reinterpret_cast<unsigned char*>(sh_scr + static_cast<size_t>(5) * l * smem_threads) +
+                                 static_cast<size_t>(threadIdx.x) * l
+                           : pivs + static_cast<size_t>(j) * l;
   const double tiny = DBL_EPSILON * tn;
   double prev_shift = 0.0;
   for (int jj = j; jj < end; ++jj) {
@@ -504,8 +510,14 @@ void launch_eigh_tridiag(cudaStream_t s, const double* a, index_t l, double* eva
   const int warps_per_block = 4;
   const unsigned gblocks = static_cast<unsigned>(ceil_div(l, warps_per_block));
   bisect_kernel<<<gblocks, 32 * warps_per_block, 0, s>>>(d, e, static_cast<int>(l), tn, evals);
-  invit_kernel<<<static_cast<unsigned>(ceil_div(l, 64)), 64, 0, s>>>(d, e, static_cast<int>(l), evals, tn, scratch,
-                                                                    piv, y);
+  int it = 32;
+  while (it > 1 && static_cast<std::size_t>(it) * (40 * l + l) > 200 * 1024) it >>= 1;
+  const bool smem_ok = static_cast<std::size_t>(it) * (40 * l + l) <= 200 * 1024;
+  const int ithreads = smem_ok ? it : 64;
+  const std::size_t ismem = smem_ok ? static_cast<std::size_t>(it) * (40 * l + l) + 16 : 0;
+  LPCA_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ismem)));
+  invit_kernel<<<static_cast<unsigned>(ceil_div(l, ithreads)), ithreads, ismem, s>>>(
+      d, e, static_cast<int>(l), evals, tn, scratch, piv, y, smem_ok ? ithreads : 0);
   backxform_kernel<<<gblocks, 32 * warps_per_block, 0, s>>>(refl, h, static_cast<int>(l), y, evecs);
   // refinement: scratch holds AZ, S, R, E; y receives Z E
   double* az = scratch;

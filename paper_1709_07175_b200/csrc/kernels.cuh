@@ -93,6 +93,11 @@ void launch_split_tf32_transpose(cudaStream_t s, const float* src, index_t m, in
 // ---- small fp64 kernels (the l x l step) ----------------------------------------
 // G = F F^T, F l x n column-major, bitwise symmetric (dense_aat, kernels.cpp:148-172).
 void launch_gram(cudaStream_t s, const double* f, index_t l, index_t n, double* g);
+// Same product for the fit path: split-K DFMA tiles, chunk partials summed in a
+// fixed order (deterministic, not the reference's rounding sequence).
+// `part` holds gram_fast_chunks(l, n) * l * l doubles.
+index_t gram_fast_chunks(index_t l, index_t n);
+void launch_gram_fast(cudaStream_t s, const double* f, index_t l, index_t n, double* g, double* part);
 // U^T U for tall U (m x l row-major) into chunk partials part[c][a + b*l] (full square).
 template <typename T>
 void launch_syrk_partials(cudaStream_t s, const T* u, index_t ldu, index_t m, index_t l,

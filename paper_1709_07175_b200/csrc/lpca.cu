@@ -425,8 +425,9 @@ void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
   double* lm = ctx.get<double>("orth.l", l * l);
   double* tmp = ctx.get<double>("orth.tmp", l * n);
   int* st = ctx.get<int>("orth.status", 1);
+  double* gpart = ctx.get<double>("gram.part", gram_fast_chunks(l, n) * l * l);
   for (int pass = 0; pass < 2; ++pass) {
-    launch_gram(ctx.stream, f, l, n, g);
+    launch_gram_fast(ctx.stream, f, l, n, g, gpart);
     LPCA_LAUNCHED(ctx);
     launch_chol_inverse(ctx.stream, g, l, w, lm, st);
     LPCA_LAUNCHED(ctx);
@@ -493,7 +494,11 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
   double* evecs = ctx.get<double>("svd.evecs", l * l);
   int* st = ctx.get<int>("svd.status", 2);
   double* gap = ctx.get<double>("svd.gap", 1);
-  launch_gram(ctx.stream, f, l, n, g);
+  if (ctx.exact) {
+    launch_gram(ctx.stream, f, l, n, g);  // the reference's rounding sequence
+  } else {
+    launch_gram_fast(ctx.stream, f, l, n, g, ctx.get<double>("gram.part", gram_fast_chunks(l, n) * l * l));
+  }
   LPCA_LAUNCHED(ctx);
   eigh_dev(ctx, g, l, evals, evecs, st, gap, ctx.eigensolver);
   launch_vform(ctx.stream, f, l, n, evecs, evals, k, nullptr, v);

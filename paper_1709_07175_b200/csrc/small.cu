@@ -381,6 +381,70 @@ void launch_gram(cudaStream_t s, const double* f, index_t l, index_t n, double* 
   gram_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(f, l, n, g);
 }
 
+namespace {
+// G partial for one n-chunk: 64 x 64 output tile, DFMA, 4 x 4 per thread.
+__global__ void __launch_bounds__(256) gram_split_kernel(const double* __restrict__ f, int l, int n, int chunk,
+                                                         double* __restrict__ part) {
+  constexpr int T = 64, BK = 16;
+  __shared__ double As[BK][T + 1];
+  __shared__ double Bs[BK][T + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int i0 = blockIdx.x * T, j0 = blockIdx.y * T;
+  const int c = blockIdx.z;
+  const int k_begin = c * chunk, k_end = min(n, k_begin + chunk);
+  double acc[4][4] = {};
+  for (int k0 = k_begin; k0 < k_end; k0 += BK) {
+    for (int idx = threadIdx.x; idx < T * BK; idx += 256) {
+      const int ii = idx % T, kk = idx / T;  // consecutive threads -> consecutive rows of F
+      const int gk = k0 + kk;
+      As[kk][ii] = (i0 + ii < l && gk < k_end) ? f[static_cast<size_t>(gk) * l + i0 + ii] : 0.0;
+      Bs[kk][ii] = (j0 + ii < l && gk < k_end) ? f[static_cast<size_t>(gk) * l + j0 + ii] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        av[q] = As[kk][ty + 16 * q];
+        bv[q] = Bs[kk][tx + 16 * q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(av[p], bv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+  double* dst = part + static_cast<size_t>(c) * l * l;
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gi = i0 + ty + 16 * p, gj = j0 + tx + 16 * q;
+      if (gi < l && gj < l) dst[static_cast<size_t>(gj) * l + gi] = acc[p][q];
+    }
+}
+}  // namespace
+
+index_t gram_fast_chunks(index_t l, index_t n) {
+  const index_t tiles = ceil_div(l, 64) * ceil_div(l, 64);
+  index_t chunks = ceil_div(2 * 148, tiles);
+  const index_t max_chunks = ceil_div(n, 64);
+  return chunks < max_chunks ? (chunks < 1 ? 1 : chunks) : max_chunks;
+}
+
+void launch_gram_fast(cudaStream_t s, const double* f, index_t l, index_t n, double* g, double* part) {
+  const index_t chunks = gram_fast_chunks(l, n);
+  const index_t chunk = round_up(ceil_div(n, chunks), 16);
+  const index_t nch = ceil_div(n, chunk);
+  dim3 grid(static_cast<unsigned>(ceil_div(l, 64)), static_cast<unsigned>(ceil_div(l, 64)),
+            static_cast<unsigned>(nch));
+  gram_split_kernel<<<grid, 256, 0, s>>>(f, static_cast<int>(l), static_cast<int>(n), static_cast<int>(chunk),
+                                         nch == 1 ? g : part);
+  if (nch > 1) launch_reduce_partials(s, part, nch, l * l, g);
+}
+
 void launch_jacobi_eigh(cudaStream_t s, double* a, index_t l, double* evals, double* evecs,
                         double* work, int* status, double* gap) {
   if (l > 1024) throw Error(kInvalidArgument, "eigh: l > 1024 is not supported on the device");

@@ -92,7 +92,10 @@ __device__ __forceinline__ void item_coords(const TcArgs& a, int item, int& t0, 
     k0 = 0;
     k1 = a.n;
   } else {
-    const int nt = item / a.chunks, ch = item % a.chunks;
+    // chunk-major: the CTAs running together share row chunks, so the U^T
+    // planes of those rows are re-read from L2 by every n tile, not from HBM
+    const int ntiles = (a.n + kBM - 1) / kBM;
+    const int nt = item % ntiles, ch = item / ntiles;
     t0 = nt * kBM;  // first column
     k0 = ch * a.chunk_rows;
     k1 = min(a.m, k0 + a.chunk_rows);
@@ -304,7 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else if (row < a.n) {
             // F^T row j = F column j: part[chunk][j * l + r]
-            double* p = a.part + static_cast<size_t>(item % a.chunks) * a.l * a.n + static_cast<size_t>(row) * a.l;
+            double* p = a.part + static_cast<size_t>(item / ((a.n + kBM - 1) / kBM)) * a.l * a.n +
+                        static_cast<size_t>(row) * a.l;
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               if (c0 + e < a.l) p[c0 + e] = static_cast<double>(v[e]);
@@ -324,7 +328,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+#include "tc_pair.cuh"
+
 // ---- host side ----------------------------------------------------------------------
+// 2-SM pair kernels (tc_pair.cuh) unless LPCA_TC_PAIR=0.
+bool pair_mode() {
+  static const bool on = [] {
+    const char* e = getenv("LPCA_TC_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -380,6 +395,19 @@ bool plan_tmem(int npad, TcArgs& a) {
 }
 
 template <int kMode>
+void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, TcArgs& a,
+                 int num_sms) {
+  const uint32_t stage_bytes = kBM * kBK * 4 + static_cast<uint32_t>(a.npad) * kBK * 4;  // X + half B (hi, lo)
+  a.stages = static_cast<int>(kSmemBudget / stage_bytes);
+  if (a.stages > 8) a.stages = 8;
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512;
+  LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
+  tc2_kernel<kMode><<<2 * pairs, kThreads, smem, s>>>(tx, th, tl, a);
+}
+
+template <int kMode>
 void launch(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, TcArgs& a,
             int grid) {
   const uint32_t stage_bytes = kBM * kBK * 4 + 2 * static_cast<uint32_t>(a.npad) * kBK * 4;
@@ -409,9 +437,11 @@ void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, i
     throw Error(kInternal, "xw_tc: unsupported shape");
   if (ldx % 4 || ldw % 4 || (out_hi && ldh % 4))
     throw Error(kInternal, "xw_tc: leading dimensions must be multiples of 4 floats");
+  const bool pair = pair_mode();
+  const uint32_t brows = static_cast<uint32_t>(pair ? wpad / 2 : wpad);
   const CUtensorMap tx = map_2d(x, n, m, ldx, 32, kBM, true);
-  const CUtensorMap th = map_2d(w_hi, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
-  const CUtensorMap tl = map_2d(w_lo, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
+  const CUtensorMap th = map_2d(w_hi, n, wpad, ldw, 32, brows, true);
+  const CUtensorMap tl = map_2d(w_lo, n, wpad, ldw, 32, brows, true);
   a.m = static_cast<int>(m);
   a.n = static_cast<int>(n);
   a.npad = static_cast<int>(wpad);
@@ -423,6 +453,11 @@ void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, i
   a.out_hi = out_hi;
   a.out_lo = out_lo;
   a.ldh = static_cast<int>(ldh);
+  if (pair) {
+    a.items = static_cast<int>(ceil_div(m, 2 * kBM));
+    launch_pair<kXW>(s, tx, th, tl, a, num_sms);
+    return;
+  }
   launch<kXW>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 
@@ -434,8 +469,10 @@ void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t 
 // Row chunks per n tile so that tiles x chunks spreads evenly over the CTAs.
 index_t utx_tc_splits(index_t m, index_t l, index_t n, int num_sms, index_t* rows_per_split) {
   (void)l;
-  const index_t ntiles = ceil_div(n, kBM);
-  index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms), ntiles);  // ~8 items per CTA
+  const bool pair = pair_mode();
+  const index_t ntiles = ceil_div(n, pair ? 2 * kBM : kBM);
+  const index_t workers = pair ? num_sms / 2 : num_sms;
+  index_t chunks = ceil_div(8 * workers, ntiles);  // ~8 items per CTA (pair)
   const index_t max_chunks = ceil_div(m, 4 * kRunStages * kBK);          // >= 4 runs per item
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
@@ -459,12 +496,19 @@ void launch_utx_tc_planes(cudaStream_t s, const float* ut_hi, const float* ut_lo
   a.npad = static_cast<int>(npad);
   a.chunks = static_cast<int>(chunks);
   a.chunk_rows = static_cast<int>(rows);
-  a.items = static_cast<int>(ceil_div(n, kBM) * chunks);
   a.part = part;
   a.l = static_cast<int>(l);
+  const bool pair = pair_mode();
+  const uint32_t brows = static_cast<uint32_t>(pair ? npad / 2 : npad);
   const CUtensorMap tx = map_2d(x, n, m, ldx, kBM, kBK, false);
-  const CUtensorMap th = map_2d(ut_hi, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
-  const CUtensorMap tl = map_2d(ut_lo, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
+  const CUtensorMap th = map_2d(ut_hi, m, npad, ldt, 32, brows, true);
+  const CUtensorMap tl = map_2d(ut_lo, m, npad, ldt, 32, brows, true);
+  if (pair) {
+    a.items = static_cast<int>(ceil_div(n, 2 * kBM) * chunks);
+    launch_pair<kXTU>(s, tx, th, tl, a, num_sms);
+    return;
+  }
+  a.items = static_cast<int>(ceil_div(n, kBM) * chunks);
   launch<kXTU>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 

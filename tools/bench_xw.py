@@ -11,7 +11,7 @@ ctx = lp.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 m, n = 1_000_000, 4096
 x = torch.randn(m, n, device="cuda")
-for w in [16, 32, 48, 64, 112, 128, 224]:
+for w in [int(a) for a in sys.argv[1:]] or [16, 32, 48, 64, 112, 128, 224]:
     W = torch.randn(n, w, device="cuda", dtype=torch.float64)
     out = torch.empty((m, w), device="cuda")
     for _ in range(2):

@@ -340,6 +340,11 @@ bool pair_mode() {
   return on;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -352,19 +357,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor map: `inner` contiguous elements per row, `outer` rows, row
-// pitch `ld` elements, box {box_inner, box_outer}.
-CUtensorMap map_2d(const float* base, index_t inner, index_t outer, index_t ld, uint32_t box_inner,
-                   uint32_t box_outer, bool swizzle128) {
+// 2-D tensor map of fp32 (esize 4) or fp16 (esize 2) elements: `inner`
+// contiguous elements per row, `outer` rows, row pitch `ld` elements, box
+// {box_inner, box_outer}.
+CUtensorMap map_2d(const void* base, index_t inner, index_t outer, index_t ld, uint32_t box_inner,
+                   uint32_t box_outer, bool swizzle128, int esize = 4) {
   CUtensorMap m;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = encode_fn()(
+      &m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+      dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
 }
@@ -375,36 +382,39 @@ uint32_t tmem_cols_for(uint32_t need) {
   return c;
 }
 
-// TMEM plan: run buffers + long accumulator + A ring (64 columns per slot).
-bool plan_tmem(int npad, TcArgs& a) {
-  const char* env_nrb = getenv("LPCA_TC_NRB");
-  const char* env_as = getenv("LPCA_TC_ASLOTS");
-  const int max_nrb = env_nrb ? atoi(env_nrb) : 2;
-  const int max_as = env_as ? atoi(env_as) : 2;
-  for (int nrb = max_nrb; nrb >= 1; --nrb) {
-    const int acc = (nrb + 1) * npad;
+// TMEM plan: nrb run buffers + long accumulator + A ring (64 columns per slot).
+bool plan_tmem(int npad, int& nrb, int& aslots, uint32_t& cols) {
+  const int max_nrb = env_int("LPCA_TC_NRB", 2);
+  const int max_as = env_int("LPCA_TC_ASLOTS", 2);
+  for (int r = max_nrb; r >= 1; --r) {
+    const int acc = (r + 1) * npad;
     const int slots = (512 - acc) / 64;
     if (slots >= 1) {
-      a.nrb = nrb;
-      a.aslots = slots > max_as ? max_as : slots;
-      a.tmem_cols = tmem_cols_for(static_cast<uint32_t>(acc + 64 * a.aslots));
+      nrb = r;
+      aslots = slots > max_as ? max_as : slots;
+      cols = tmem_cols_for(static_cast<uint32_t>(acc + 64 * aslots));
       return true;
     }
   }
   return false;
 }
+bool plan_tmem(int npad, TcArgs& a) { return plan_tmem(npad, a.nrb, a.aslots, a.tmem_cols); }
 
-template <int kMode>
-void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, TcArgs& a,
+constexpr uint32_t kPairSmemBudget = 208 * 1024;
+
+template <int kMode, bool kHalf>
+void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, PairArgs& a,
                  int num_sms) {
-  const uint32_t stage_bytes = kBM * kBK * 4 + static_cast<uint32_t>(a.npad) * kBK * 4;  // X + half B (hi, lo)
-  a.stages = static_cast<int>(kSmemBudget / stage_bytes);
+  if (!plan_tmem(a.npad, a.nrb, a.aslots, a.tmem_cols)) throw Error(kInternal, "tc pair: TMEM plan failed");
+  const uint32_t bk = kHalf ? 64 : 32;
+  const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
+  a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512;
-  LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad;
+  LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
-  tc2_kernel<kMode><<<2 * pairs, kThreads, smem, s>>>(tx, th, tl, a);
+  tc2_kernel<kMode, kHalf><<<2 * pairs, kThreads, smem, s>>>(tx, th, tl, a);
 }
 
 template <int kMode>
@@ -421,27 +431,132 @@ void launch(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const 
 }  // namespace
 
 bool tc_xw_supported(index_t n, index_t wpad) {
-  TcArgs a{};
-  return wpad >= 16 && wpad <= 256 && wpad % 16 == 0 && n >= 1 && plan_tmem(static_cast<int>(wpad), a);
+  int nrb, as;
+  uint32_t cols;
+  return wpad >= 16 && wpad <= 256 && wpad % 16 == 0 && n >= 1 && plan_tmem(static_cast<int>(wpad), nrb, as, cols);
 }
 
 bool tc_utx_supported(index_t l, index_t n) { return l >= 1 && n >= 1 && tc_xw_supported(1, round_up(l, 16)); }
+
+bool tc_pair_mode() { return pair_mode(); }
+
+void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
+  if (p.m <= 0) return;
+  if (!tc_xw_supported(p.n, p.wpad)) throw Error(kInternal, "xw_pair: unsupported shape");
+  if (p.ldx % 4 || (p.half ? p.ldw % 8 : p.ldw % 4) || (p.out_hi && p.ldh % 4) || (p.uh && p.ldh % 8))
+    throw Error(kInternal, "xw_pair: leading dimensions must be 16-byte multiples");
+  if (p.half && ((!p.xmax_in && !(p.xmax_val > 0.0f)) || !p.winv)) throw Error(kInternal, "xw_pair: fp16 encoding needs its scales");
+  PairArgs a{};
+  a.m = static_cast<int>(p.m);
+  a.n = static_cast<int>(p.n);
+  a.npad = static_cast<int>(p.wpad);
+  a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
+  a.run_stages = env_int("LPCA_TC_RUN", p.half ? 2 : 4);
+  a.xmax_in = p.xmax_in;
+  a.xmax_val = p.xmax_val;
+  a.xmax_out = p.xmax_out;
+  a.winv = p.winv;
+  a.wstore = static_cast<int>(p.wstore);
+  a.out = p.out;
+  a.ldo = static_cast<int>(p.ldo);
+  a.out_hi = p.out_hi;
+  a.out_lo = p.out_lo;
+  a.uh = p.uh;
+  a.ul = p.ul;
+  a.uinv = p.uinv;
+  a.ldh = static_cast<int>(p.ldh);
+  const uint32_t brows = static_cast<uint32_t>(p.wpad / 2);
+  const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, 32, kBM, true);
+  if (p.half) {
+    const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 64, brows, true, 2);
+    const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 64, brows, true, 2);
+    launch_pair<kXW, true>(s, tx, th, tl, a, num_sms);
+  } else {
+    const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 32, brows, true);
+    const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 32, brows, true);
+    launch_pair<kXW, false>(s, tx, th, tl, a, num_sms);
+  }
+}
+
+// Row chunks per 256-column tile so that tiles x chunks spreads evenly over the
+// pairs; chunks are whole 128-row blocks (the fp16 U^T scale granularity).
+index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_split) {
+  const index_t ntiles = ceil_div(n, 2 * kBM);
+  index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms / 2), ntiles);  // ~8 items per pair
+  const index_t max_chunks = ceil_div(m, 4 * 128);                           // >= 4 runs per item
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  const index_t rows = round_up(ceil_div(m, chunks), 128);
+  chunks = ceil_div(m, rows);
+  *rows_per_split = rows;
+  return chunks;
+}
+
+void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
+  const index_t npad = round_up(p.l, 16);
+  if (!tc_utx_supported(p.l, p.n)) throw Error(kInternal, "utx_pair: unsupported shape");
+  if (p.ldx % 4 || (p.half ? p.ldt % 8 : p.ldt % 4))
+    throw Error(kInternal, "utx_pair: leading dimensions must be 16-byte multiples");
+  if (p.half && (!p.xmax_in || !p.uinv)) throw Error(kInternal, "utx_pair: fp16 encoding needs its scales");
+  index_t rows = 0;
+  const index_t chunks = utx_pair_splits(p.m, p.n, num_sms, &rows);
+  PairArgs a{};
+  a.m = static_cast<int>(p.m);
+  a.n = static_cast<int>(p.n);
+  a.npad = static_cast<int>(npad);
+  a.chunk_rows = static_cast<int>(rows);
+  a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
+  a.run_stages = p.half ? 2 : 4;  // fp16: one run per 128-row block of U^T scales
+  a.xmax_in = p.xmax_in;
+  a.uinv_in = p.uinv;
+  a.part = p.part;
+  a.l = static_cast<int>(p.l);
+  const uint32_t brows = static_cast<uint32_t>(npad / 2);
+  if (p.half) {
+    const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 64, false);
+    const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 64, brows, true, 2);
+    const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 64, brows, true, 2);
+    launch_pair<kXTU, true>(s, tx, th, tl, a, num_sms);
+  } else {
+    const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 32, false);
+    const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 32, brows, true);
+    const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 32, brows, true);
+    launch_pair<kXTU, false>(s, tx, th, tl, a, num_sms);
+  }
+}
 
 void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
                          const float* w_hi, const float* w_lo, index_t wpad, index_t ldw, float* out,
                          index_t ldo, index_t wstore, float* out_hi, float* out_lo, index_t ldh,
                          int num_sms) {
   if (m <= 0) return;
+  if (pair_mode()) {
+    XwPairArgs p{};
+    p.x = x;
+    p.m = m;
+    p.n = n;
+    p.ldx = ldx;
+    p.w_hi = w_hi;
+    p.w_lo = w_lo;
+    p.wpad = wpad;
+    p.ldw = ldw;
+    p.out = out;
+    p.ldo = ldo;
+    p.wstore = wstore;
+    p.out_hi = out_hi;
+    p.out_lo = out_lo;
+    p.ldh = ldh;
+    launch_xw_pair(s, p, num_sms);
+    return;
+  }
   TcArgs a{};
   if (!tc_xw_supported(n, wpad) || !plan_tmem(static_cast<int>(wpad), a))
     throw Error(kInternal, "xw_tc: unsupported shape");
   if (ldx % 4 || ldw % 4 || (out_hi && ldh % 4))
     throw Error(kInternal, "xw_tc: leading dimensions must be multiples of 4 floats");
-  const bool pair = pair_mode();
-  const uint32_t brows = static_cast<uint32_t>(pair ? wpad / 2 : wpad);
   const CUtensorMap tx = map_2d(x, n, m, ldx, 32, kBM, true);
-  const CUtensorMap th = map_2d(w_hi, n, wpad, ldw, 32, brows, true);
-  const CUtensorMap tl = map_2d(w_lo, n, wpad, ldw, 32, brows, true);
+  const CUtensorMap th = map_2d(w_hi, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
+  const CUtensorMap tl = map_2d(w_lo, n, wpad, ldw, 32, static_cast<uint32_t>(wpad), true);
   a.m = static_cast<int>(m);
   a.n = static_cast<int>(n);
   a.npad = static_cast<int>(wpad);
@@ -453,11 +568,6 @@ void launch_xw_tc_planes(cudaStream_t s, const float* x, index_t m, index_t n, i
   a.out_hi = out_hi;
   a.out_lo = out_lo;
   a.ldh = static_cast<int>(ldh);
-  if (pair) {
-    a.items = static_cast<int>(ceil_div(m, 2 * kBM));
-    launch_pair<kXW>(s, tx, th, tl, a, num_sms);
-    return;
-  }
   launch<kXW>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 
@@ -469,10 +579,9 @@ void launch_xw_tc(cudaStream_t s, const float* x, index_t m, index_t n, index_t 
 // Row chunks per n tile so that tiles x chunks spreads evenly over the CTAs.
 index_t utx_tc_splits(index_t m, index_t l, index_t n, int num_sms, index_t* rows_per_split) {
   (void)l;
-  const bool pair = pair_mode();
-  const index_t ntiles = ceil_div(n, pair ? 2 * kBM : kBM);
-  const index_t workers = pair ? num_sms / 2 : num_sms;
-  index_t chunks = ceil_div(8 * workers, ntiles);  // ~8 items per CTA (pair)
+  if (pair_mode()) return utx_pair_splits(m, n, num_sms, rows_per_split);
+  const index_t ntiles = ceil_div(n, kBM);
+  index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms), ntiles);  // ~8 items per CTA
   const index_t max_chunks = ceil_div(m, 4 * kRunStages * kBK);          // >= 4 runs per item
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
@@ -484,6 +593,20 @@ index_t utx_tc_splits(index_t m, index_t l, index_t n, int num_sms, index_t* row
 
 void launch_utx_tc_planes(cudaStream_t s, const float* ut_hi, const float* ut_lo, index_t ldt, const float* x,
                           index_t ldx, index_t m, index_t l, index_t n, double* part, int num_sms) {
+  if (pair_mode()) {
+    UtxPairArgs p{};
+    p.u_hi = ut_hi;
+    p.u_lo = ut_lo;
+    p.ldt = ldt;
+    p.x = x;
+    p.ldx = ldx;
+    p.m = m;
+    p.l = l;
+    p.n = n;
+    p.part = part;
+    launch_utx_pair(s, p, num_sms);
+    return;
+  }
   TcArgs a{};
   const index_t npad = round_up(l, 16);
   if (!tc_utx_supported(l, n) || !plan_tmem(static_cast<int>(npad), a))
@@ -496,19 +619,12 @@ void launch_utx_tc_planes(cudaStream_t s, const float* ut_hi, const float* ut_lo
   a.npad = static_cast<int>(npad);
   a.chunks = static_cast<int>(chunks);
   a.chunk_rows = static_cast<int>(rows);
+  a.items = static_cast<int>(ceil_div(n, kBM) * chunks);
   a.part = part;
   a.l = static_cast<int>(l);
-  const bool pair = pair_mode();
-  const uint32_t brows = static_cast<uint32_t>(pair ? npad / 2 : npad);
   const CUtensorMap tx = map_2d(x, n, m, ldx, kBM, kBK, false);
-  const CUtensorMap th = map_2d(ut_hi, m, npad, ldt, 32, brows, true);
-  const CUtensorMap tl = map_2d(ut_lo, m, npad, ldt, 32, brows, true);
-  if (pair) {
-    a.items = static_cast<int>(ceil_div(n, 2 * kBM) * chunks);
-    launch_pair<kXTU>(s, tx, th, tl, a, num_sms);
-    return;
-  }
-  a.items = static_cast<int>(ceil_div(n, kBM) * chunks);
+  const CUtensorMap th = map_2d(ut_hi, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
+  const CUtensorMap tl = map_2d(ut_lo, m, npad, ldt, 32, static_cast<uint32_t>(npad), true);
   launch<kXTU>(s, tx, th, tl, a, a.items < num_sms ? a.items : num_sms);
 }
 

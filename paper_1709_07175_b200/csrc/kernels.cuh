@@ -2,6 +2,7 @@
 // routine whose semantics it implements.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 
 #include "common.cuh"
@@ -82,6 +83,51 @@ void launch_utx_tc_planes(cudaStream_t s, const float* u_hi, const float* u_lo, 
 void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, index_t ldx,
                    index_t m, index_t l, index_t n, index_t chunk_rows, double* part,
                    int num_sms);
+// ---- 2-SM pair passes (tc_pair.cuh) -------------------------------------------
+// Both encodings of the 3-term split: tf32 hi/lo (half = false) or fp16 hi/lo of
+// power-of-two scaled operands (half = true: X scaled from max|X| = *xmax_in,
+// W planes per column (winv = inverse scales), U^T planes per column and 128-row
+// block (uinv[block][c])). Planes are K-major: [wpad or round_up(l,16)][ld].
+struct XwPairArgs {
+  const float* x = nullptr;
+  index_t m = 0, n = 0, ldx = 0;
+  bool half = false;
+  const void* w_hi = nullptr;
+  const void* w_lo = nullptr;
+  index_t wpad = 0, ldw = 0;
+  const float* winv = nullptr;
+  const uint32_t* xmax_in = nullptr;  // max|X| bits on the device, or
+  float xmax_val = 0.0f;              // max|X| by value (xmax_in null)
+  uint32_t* xmax_out = nullptr;       // atomicMax of the |X| bits actually read
+  float* out = nullptr;          // plain fp32 row-major (first wstore columns)
+  index_t ldo = 0, wstore = 0;
+  float* out_hi = nullptr;       // tf32 planes of OUT^T [wpad][ldh]
+  float* out_lo = nullptr;
+  __half* uh = nullptr;          // fp16 planes of OUT^T [wpad][ldh] ...
+  __half* ul = nullptr;
+  float* uinv = nullptr;         // ... with inverse scales [ceil(m/128)][wpad]
+  index_t ldh = 0;
+};
+struct UtxPairArgs {
+  bool half = false;
+  const void* u_hi = nullptr;
+  const void* u_lo = nullptr;
+  index_t ldt = 0;
+  const float* uinv = nullptr;
+  const uint32_t* xmax_in = nullptr;
+  const float* x = nullptr;
+  index_t ldx = 0, m = 0, l = 0, n = 0;
+  double* part = nullptr;  // [chunks][n][l] (utx_pair_splits)
+};
+bool tc_pair_mode();
+void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms);
+index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_split);
+void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms);
+// W (fp64 n x wc, column-major ld ldw) -> fp16 hi/lo planes [wpad][ldd] scaled per
+// column by 2^(14 - floor(log2 max|W[:,c]|)); winv[c] = inverse scale (1 for padding).
+void launch_split_f16_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc, index_t wpad,
+                        __half* hi, __half* lo, index_t ldd, float* winv);
+
 // Split a row-major fp32 matrix (m x ld) into tf32 hi/lo planes of the same shape.
 void launch_split_tf32_rows(cudaStream_t s, const float* src, index_t m, index_t ld, float* hi,
                             float* lo);

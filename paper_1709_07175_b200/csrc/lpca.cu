@@ -139,6 +139,7 @@ struct lpca_map {
   double density = 1.0, scale = 1.0;
   double* v = nullptr;  // device, n x k column-major fp64
   std::vector<double> sigma;
+  float xmax = 0.0f;    // max|X| of the fitted rows (scale of the fp16 transform; 0 = unknown)
   // V comes from the stream-ordered allocator on the creating context's stream:
   // no device-wide synchronisation per fit (cudaMalloc/cudaFree would stall the
   // pipeline). A map must be destroyed before its context.
@@ -335,19 +336,92 @@ struct Panel {
   float* lo = nullptr;
   index_t ld = 0;
   index_t ldt = 0;
+  // pair fp16 path: U^T as fp16 hi/lo planes [ld][ldt16] scaled per (column,
+  // 128-row block), inverse scales uinv[block][ld] (tc_pair.cuh)
+  __half* h16hi = nullptr;
+  __half* h16lo = nullptr;
+  float* uinv = nullptr;
+  index_t ldt16 = 0;
 };
+
+// fp16 operand encoding of the X passes (tc_pair.cuh): the first pass over X
+// (tf32) records max|X| on the device; later passes scale X by it. A transform
+// gets the fitted data's max by value and re-checks the data it actually reads.
+struct XScale {
+  uint32_t* dev = nullptr;    // max|X| bits on the device
+  float host = 0.0f;          // or by value (dev null)
+  bool record = false;        // tf32 pass that records max|X| into dev
+  bool use = false;           // fp16 pass
+  uint32_t* check = nullptr;  // fp16 X W: max|X| of the rows read
+};
+
+bool f16_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LPCA_TC_F16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 index_t planes_ld(index_t m) { return round_up(m > 0 ? m : 1, 4); }
 
 // out = X W, W fp64 column-major (n x wc, ld ldw). For fp32 X the operand is
 // prepared once per call (rounded to fp32, or split into tf32 hi/lo planes).
 void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, const Panel& out,
-             bool exact) {
+             bool exact, const XScale* xs = nullptr) {
   const index_t m = x.m, n = x.n;
   if (m == 0) return;
   if (x.dtype == 8) {
     launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, w, wc,
                                    ldw, static_cast<double*>(out.plain), out.ld, 1, exact);
+    LPCA_LAUNCHED(ctx);
+    return;
+  }
+  if (use_tc(ctx, x, wc) && tc_pair_mode()) {
+    XwPairArgs p;
+    p.x = static_cast<const float*>(x.p);
+    p.m = m;
+    p.n = n;
+    p.ldx = x.ld;
+    p.wpad = round_up(wc, 16);
+    if (xs && xs->use) {
+      p.ldw = round_up(n, 8);
+      __half* hi = ctx.get<__half>("w.h16hi", p.wpad * p.ldw);
+      __half* lo = ctx.get<__half>("w.h16lo", p.wpad * p.ldw);
+      float* winv = ctx.get<float>("w.inv", p.wpad);
+      launch_split_f16_w(ctx.stream, w, ldw, n, wc, p.wpad, hi, lo, p.ldw, winv);
+      LPCA_LAUNCHED(ctx);
+      p.half = true;
+      p.w_hi = hi;
+      p.w_lo = lo;
+      p.winv = winv;
+      p.xmax_in = xs->dev;
+      p.xmax_val = xs->host;
+      p.xmax_out = xs->check;
+    } else {
+      p.ldw = round_up(n, 4);
+      float* hi = ctx.get<float>("w.hi", p.wpad * p.ldw);
+      float* lo = ctx.get<float>("w.lo", p.wpad * p.ldw);
+      launch_split_tf32_w(ctx.stream, w, ldw, n, wc, p.wpad, hi, lo, p.ldw);
+      LPCA_LAUNCHED(ctx);
+      p.w_hi = hi;
+      p.w_lo = lo;
+      p.xmax_out = xs && xs->record ? xs->dev : nullptr;
+    }
+    p.out = static_cast<float*>(out.plain);
+    p.ldo = out.ld;
+    p.wstore = wc;
+    if (out.h16hi) {
+      p.uh = out.h16hi;
+      p.ul = out.h16lo;
+      p.uinv = out.uinv;
+      p.ldh = out.ldt16;
+    } else {
+      p.out_hi = out.hi;
+      p.out_lo = out.lo;
+      p.ldh = out.ldt;
+    }
+    launch_xw_pair(ctx.stream, p, ctx.num_sms);
     LPCA_LAUNCHED(ctx);
     return;
   }
@@ -382,7 +456,8 @@ index_t pick_chunks(const lpca_ctx& ctx, index_t m, index_t tiles, bool exact) {
 
 // F (l x n column-major fp64) = U^T X summed over this rank's rows, then
 // allreduced over ranks.
-void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f, bool exact) {
+void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f, bool exact,
+              const XScale* xs = nullptr) {
   const index_t m = x.m, n = x.n;
   if (m == 0) {
     launch_zero(ctx.stream, f, sizeof(double) * l * n);
@@ -391,7 +466,25 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
   }
   index_t chunks;
   double* part;
-  if (u.hi && x.dtype == 4) {
+  if (u.h16hi && x.dtype == 4) {
+    index_t rps = 0;
+    chunks = utx_pair_splits(m, n, ctx.num_sms, &rps);
+    part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+    UtxPairArgs p;
+    p.half = true;
+    p.u_hi = u.h16hi;
+    p.u_lo = u.h16lo;
+    p.ldt = u.ldt16;
+    p.uinv = u.uinv;
+    p.xmax_in = xs ? xs->dev : nullptr;
+    p.x = static_cast<const float*>(x.p);
+    p.ldx = x.ld;
+    p.m = m;
+    p.l = l;
+    p.n = n;
+    p.part = part;
+    launch_utx_pair(ctx.stream, p, ctx.num_sms);
+  } else if (u.hi && x.dtype == 4) {
     index_t rps = 0;
     chunks = utx_tc_splits(m, l, n, ctx.num_sms, &rps);
     part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
@@ -578,29 +671,44 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     const bool exact = ctx.exact != 0 && x.dtype == 8;
     const bool tc = use_tc(ctx, x, l);
     const index_t mm = m > 0 ? m : 1;
+    // fp16 encoding for every pass after the sketch (pair kernels, Lazy SPCA)
+    const bool f16 = tc && tc_pair_mode() && f16_enabled() && c.method == LPCA_LAZY_SPCA;
+    XScale xs;
+    if (f16) {
+      xs.dev = ctx.get<uint32_t>("xmax", 1);
+      launch_zero(ctx.stream, xs.dev, sizeof(uint32_t));
+    }
     // U (m x l, row-major, ld padded to 16): the plain matrix for the SIMT and
     // SPCA paths, tf32 hi/lo planes for the tensor-core U^T X kernel.
     Panel u;
     u.ld = round_up(l, 16);
     if (!tc || c.method == LPCA_SPCA) u.plain = ctx.buf("u", dsize(x.dtype) * mm * u.ld);
-    if (tc) {
+    if (f16) {
+      u.ldt16 = round_up(mm, 8);
+      u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
+      u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
+      u.uinv = ctx.get<float>("u.inv", ceil_div(mm, 128) * u.ld);
+    } else if (tc) {
       u.ldt = planes_ld(m);
       u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
       u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
     }
-    // sketch U = X Omega (reducer.cpp:163-169)
-    xw_pass(ctx, x, omega, l, n, u, exact);
+    // sketch U = X Omega (reducer.cpp:163-169); tf32, records max|X|
+    xs.record = true;
+    xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &xs : nullptr);
+    xs.record = false;
+    xs.use = f16;
     ev.mark(1);
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
     double* f = ctx.get<double>("f", l * n);
     if (c.power_iters > 0) {
       double* z = ctx.get<double>("z.w", l * n);
       for (int it = 0; it < c.power_iters; ++it) {
-        utx_pass(ctx, x, u, l, f, exact);                    // F = U^T X  (= Z^T)
+        utx_pass(ctx, x, u, l, f, exact, &xs);               // F = U^T X  (= Z^T)
         orth_rows(ctx, f, l, n);                             // Z <- orth(Z), CholeskyQR2
         launch_transpose(ctx.stream, 8, f, l, l, n, z, n);  // W = Z as n x l column-major
         LPCA_LAUNCHED(ctx);
-        xw_pass(ctx, x, z, l, n, u, exact);                  // U = X Z
+        xw_pass(ctx, x, z, l, n, u, exact, f16 ? &xs : nullptr);  // U = X Z
       }
     }
     ev.mark(2);
@@ -664,9 +772,10 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       }
     }
     ev.mark(3);
-    utx_pass(ctx, x, u, l, f, exact);  // F = U^T X (or Q^T X)
+    utx_pass(ctx, x, u, l, f, exact, &xs);  // F = U^T X (or Q^T X)
     ev.mark(4);
     finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
+    if (f16) LPCA_CUDA(cudaMemcpyAsync(&map->xmax, xs.dev, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
     ev.mark(5);
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
     if (t) {
@@ -713,7 +822,23 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       Panel yo;
       yo.plain = ydev;
       yo.ld = ldy;
-      xw_pass(ctx, x, map.v, k, map.n, yo, false);
+      if (map.xmax > 0.0f && tc_pair_mode() && f16_enabled()) {
+        // fp16 encoding scaled by the fitted data's max|X|; if the rows read
+        // here exceed it (fp16 overflow) or sit far below it (lost bits), the
+        // pass is redone in tf32
+        XScale xs;
+        xs.use = true;
+        xs.host = map.xmax;
+        xs.check = ctx.get<uint32_t>("xmax.chk", 1);
+        launch_zero(ctx.stream, xs.check, sizeof(uint32_t));
+        xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
+        float seen = 0.0f;
+        LPCA_CUDA(cudaMemcpyAsync(&seen, xs.check, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
+        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (!(seen <= map.xmax && seen >= map.xmax * 0x1p-8f)) xw_pass(ctx, x, map.v, k, map.n, yo, false);
+      } else {
+        xw_pass(ctx, x, map.v, k, map.n, yo, false);
+      }
     } else {
       float* w32 = ctx.get<float>("v.f32", k * x.n);
       launch_convert_f64_to_f32(ctx.stream, map.v, map.n, w32, x.n, x.n, k, 1.0);

@@ -276,6 +276,48 @@ void launch_scale_f64(cudaStream_t s, const double* src, double* dst, index_t co
   scale_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count, inv);
 }
 
+// One CTA per W column: the column's max |w| sets a power-of-two scale
+// 2^(14 - floor(log2 max)) (as tc_pair.cuh's pow2_scale_for), then
+// hi = fp16_rn(w s), lo = fp16_rn(w s - hi).
+__global__ void split_f16_w_kernel(const double* __restrict__ w, index_t ldw, index_t n, index_t wc,
+                                   __half* __restrict__ hi, __half* __restrict__ lo, index_t ldd,
+                                   float* __restrict__ winv) {
+  const index_t c = blockIdx.x;
+  __shared__ float red[32];
+  float mx = 0.0f;
+  if (c < wc)
+    for (index_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmaxf(mx, fabsf(static_cast<float>(w[c * ldw + j])));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  float sc = 1.0f;
+  if (mx > 0.0f && !isinf(mx)) {
+    int e = 14 - ilogbf(mx);
+    e = e > 126 ? 126 : (e < -126 ? -126 : e);
+    sc = ldexpf(1.0f, e);
+  }
+  if (threadIdx.x == 0) winv[c] = 1.0f / sc;
+  for (index_t j = threadIdx.x; j < ldd; j += blockDim.x) {
+    const float y = (c < wc && j < n) ? static_cast<float>(w[c * ldw + j] * static_cast<double>(sc)) : 0.0f;
+    const __half h = __float2half_rn(y);
+    hi[c * ldd + j] = h;
+    lo[c * ldd + j] = __float2half_rn(y - __half2float(h));
+  }
+}
+
+void launch_split_f16_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc, index_t wpad,
+                        __half* hi, __half* lo, index_t ldd, float* winv) {
+  if (wpad <= 0) return;
+  split_f16_w_kernel<<<static_cast<unsigned>(wpad), 256, 0, s>>>(w, ldw, n, wc, hi, lo, ldd, winv);
+}
+
 void launch_split_tf32_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc,
                          index_t wpad, float* hi, float* lo, index_t ldd) {
   split_w_kernel<<<grid_for(wpad * ldd, 256), 256, 0, s>>>(w, ldw, n, wc, wpad, hi, lo, ldd);

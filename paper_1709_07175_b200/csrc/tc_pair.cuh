@@ -1,13 +1,25 @@
-// 2-SM (cta_group::2) variant of the split-TF32 pass kernels in gemm_tc.cu.
+// 2-SM (cta_group::2) pass kernels: X W and X^T U with the 3-term split
+//   a*b ~= a_hi*b_hi + a_lo*b_hi + a_hi*b_lo
+// in one of two operand encodings:
+//   kHalf = false : tf32 hi/lo (kind::tf32, K = 32 per stage). Needs no scale;
+//                   the first pass over X (the sketch) runs this way.
+//   kHalf = true  : fp16 hi/lo of power-of-two scaled operands (kind::f16,
+//                   K = 64 per stage, twice the tf32 MMA rate, half the TMEM
+//                   A traffic per K). X is scaled by s_x = 2^(14 - floor(log2
+//                   max|X|)) (max|X| recorded by the sketch's converters), the
+//                   small operand per column (W planes) or per column and
+//                   128-row block (U^T planes, written by the sketch epilogue).
+//                   hi = fp16_rn(a s), lo = fp16_rn(a s - hi): with every
+//                   scaled value in [2^-14, 2^15] the split keeps 22 bits
+//                   (tf32 hi/lo keeps 20); values more than 2^18 below their
+//                   scale's maximum lose relative precision gradually.
+// Scales are exact powers of two; results are unscaled per run (X^T U) or at
+// the final store (X W) before they leave the kernel.
 //
-// Why: at the fit's widths (N = 112..224) every 32-deep stage of the 1-SM
-// kernel moves the B hi/lo planes (2 * N * 128 B) through L2, TMA and shared
-// memory for only 12 MMAs; with M = 128 rows per CTA the B re-reads are
-// 1.75x the X bytes and the L2 -> SM traffic saturates (~8 TB/s measured,
-// tools/bench_xw.py) well before the MMA floor or HBM. A CTA pair issues
-// M = 256 MMAs: each CTA keeps its own 128 rows of A in its TMEM and loads only
-// its half of B (N/2 rows); the tensor core reads B from both CTAs' shared
-// memory. Per SM, B traffic halves.
+// Why pairs: at the fit's widths (N = 112..224) every stage of the 1-SM kernel
+// moves the B planes through L2, TMA and shared memory for 12 MMAs; a CTA pair
+// issues M = 256 MMAs with each CTA holding its own 128 rows of A (in TMEM) and
+// half of B (N/2 rows) — per SM, B traffic halves.
 //
 // Protocol (leader = cluster rank 0 issues every MMA):
 //   full_x[s]   local   : TMA of this CTA's X tile landed (converter waits)
@@ -19,10 +31,42 @@
 //   tempty[b]   leader  : 8 epilogue warps drained run buffer b
 // Remote arrivals use mapa + mbarrier.arrive on the shared::cluster address;
 // waits are the usual cta-scoped try_wait loops (as CUTLASS's cluster barriers).
-// Included by gemm_tc.cu inside its anonymous namespace (shares kBM, kBK,
-// kRunStages, TcArgs and the tc:: helpers). Pair work items: XW 256-row tiles;
-// XTU 256-column tiles x row chunks. Each CTA holds npad / 2 rows of B.
+//
+// Included by gemm_tc.cu inside its anonymous namespace (shares kBM, kThreads,
+// kXW/kXTU and the tc:: helpers). Work items: XW 256-row tiles (128 per CTA);
+// XTU 256-column tiles x row chunks.
 #pragma once
+#include <cuda_fp16.h>
+
+struct PairArgs {
+  int m, n;          // X is m x n
+  int npad;          // UMMA N (multiple of 16); each CTA holds npad / 2 rows of B
+  int stages, aslots, nrb, run_stages;
+  uint32_t tmem_cols;
+  int items;
+  int chunk_rows;    // XTU: rows per chunk (multiple of 128)
+  // fp16 encoding: max|X| (s_x derived in-kernel) from *xmax_in (bits) or xmax_val
+  const uint32_t* xmax_in;
+  float xmax_val;
+  // X W: accumulate max|X| bits of the data actually read here (nullable)
+  uint32_t* xmax_out;
+  // X W, fp16: inverse column scales of the W planes (npad)
+  const float* winv;
+  // X W outputs
+  int wstore;
+  float* out;        // plain fp32 row-major (nullable)
+  int ldo;
+  float* out_hi;     // tf32 planes of OUT^T [npad][ldh] (nullable)
+  float* out_lo;
+  __half* uh;        // fp16 planes of OUT^T [npad][ldh] with block scales (nullable)
+  __half* ul;
+  float* uinv;       // [ceil(m/128)][npad] inverse block scales of uh/ul
+  int ldh;
+  // X^T U: U^T block inverse scales (fp16), partial output part[chunk][j * l + r]
+  const float* uinv_in;
+  double* part;
+  int l;
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -69,41 +113,105 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
-// One K=32 stage of the 3-term split as M = 256 pair MMAs (A from TMEM of both CTAs).
-__device__ __forceinline__ void mma_stage_ts_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
-                                                  uint32_t idesc, uint32_t acc_first) {
-#define LPCA_M2 "{%7, %7, %7, %7, %7, %7, %7, %7}"
-  asm volatile(
-      "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"
-      " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %3, %5, " LPCA_M2 ", p;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %4, %5, " LPCA_M2 ", t;\n"
-      " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dl, %5, " LPCA_M2 ", t;\n"
-      " add.u32 ah, %1, 16;\n add.u32 al, %2, 16;\n add.u64 dh, %3, 4;\n add.u64 dl, %4, 4;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dl, %5, " LPCA_M2 ", t;\n"
-      " add.u32 ah, %1, 24;\n add.u32 al, %2, 24;\n add.u64 dh, %3, 6;\n add.u64 dl, %4, 6;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], dh, %5, " LPCA_M2 ", t;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], dl, %5, " LPCA_M2 ", t;\n"
-      "}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first), "r"(0u)
-      : "memory");
-#undef LPCA_M2
+// One stage of the 3-term split as 12 M = 256 pair MMAs, A from TMEM of both
+// CTAs: four K-steps (tf32: K = 8, fp16: K = 16), each 8 TMEM columns of A and
+// 32 B of the B rows (descriptor +2).
+#define LPCA_PAIR_STAGE(KIND)                                                                              \
+  "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"                                \
+  " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"                                                              \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %3, %5, p;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%2], %3, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
+  " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"                   \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " add.u32 ah, %1, 16;\n add.u32 al, %2, 16;\n add.u64 dh, %3, 4;\n add.u64 dl, %4, 4;\n"                 \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " add.u32 ah, %1, 24;\n add.u32 al, %2, 24;\n add.u64 dh, %3, 6;\n add.u64 dl, %4, 6;\n"                 \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  "}"
+
+template <bool kHalf>
+__device__ __forceinline__ void mma_stage_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                               uint32_t idesc, uint32_t acc_first) {
+  if constexpr (kHalf)
+    asm volatile(LPCA_PAIR_STAGE("f16")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc),
+                 "r"(acc_first), "r"(0u)
+                 : "memory");
+  else
+    asm volatile(LPCA_PAIR_STAGE("tf32")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc),
+                 "r"(acc_first), "r"(0u)
+                 : "memory");
+}
+#undef LPCA_PAIR_STAGE
+
+// Instruction descriptor, kind::f16 with fp16 A/B and fp32 accumulation.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// s = 2^(14 - floor(log2 mx)) so that |a| s < 2^15 for |a| <= mx (1 for mx = 0,
+// inf or NaN), built from the exponent bits (subnormal mx counts as 2^-126).
+__device__ __forceinline__ float pow2_scale_for(float mx) {
+  if (!(mx > 0.0f) || isinf(mx)) return 1.0f;
+  int e = static_cast<int>((__float_as_uint(mx) >> 23) & 0xffu) - 127;
+  e = e < -126 ? -126 : e;
+  int t = 14 - e;
+  t = t > 126 ? 126 : (t < -126 ? -126 : t);
+  return __uint_as_float(static_cast<uint32_t>(t + 127) << 23);
+}
+
+// Max over the warp's 32 lanes of each of x[0..15] in 16 shuffles (halving
+// butterfly). Lane L ends with the max of column
+//   ((L >> 4) & 1) * 8 + ((L >> 3) & 1) * 4 + ((L >> 2) & 1) * 2 + ((L >> 1) & 1).
+__device__ __forceinline__ float warp_max16(const float (&x)[16], int lane) {
+  const bool u4 = lane & 16, u3 = lane & 8, u2 = lane & 4, u1 = lane & 2;
+  float y8[8], y4[4], y2[2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    y8[j] = fmaxf(u4 ? x[8 + j] : x[j], __shfl_xor_sync(0xffffffffu, u4 ? x[j] : x[8 + j], 16));
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    y4[j] = fmaxf(u3 ? y8[4 + j] : y8[j], __shfl_xor_sync(0xffffffffu, u3 ? y8[j] : y8[4 + j], 8));
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    y2[j] = fmaxf(u2 ? y4[2 + j] : y4[j], __shfl_xor_sync(0xffffffffu, u2 ? y4[j] : y4[2 + j], 4));
+  float y = fmaxf(u1 ? y2[1] : y2[0], __shfl_xor_sync(0xffffffffu, u1 ? y2[0] : y2[1], 2));
+  return fmaxf(y, __shfl_xor_sync(0xffffffffu, y, 1));
+}
+__device__ __forceinline__ int warp_max16_col(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Splits 32 consecutive-K values (already scaled) into 16 packed hi and 16 packed lo columns.
+__device__ __forceinline__ void split_f16_32(const float (&v)[32], float (&hi)[16], float (&lo)[16]) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const __half2 h = __floats2half2_rn(v[2 * c], v[2 * c + 1]);
+    const float2 hf = __half22float2(h);
+    hi[c] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h));
+    lo[c] = __uint_as_float(pack_h2(v[2 * c] - hf.x, v[2 * c + 1] - hf.y));
+  }
 }
 
 template <int kMode>
-__device__ __forceinline__ void pair_item_coords(const TcArgs& a, int item, int& t0, int& k0, int& k1) {
+__device__ __forceinline__ void pair_item_coords(const PairArgs& a, int item, int& t0, int& k0, int& k1) {
   if (kMode == kXW) {
     t0 = item * 2 * kBM;
     k0 = 0;
     k1 = a.n;
   } else {
+    // chunk-major: pairs running together share row chunks (U^T planes stay in L2)
     const int ntiles = (a.n + 2 * kBM - 1) / (2 * kBM);
     const int nt = item % ntiles, ch = item / ntiles;
     t0 = nt * 2 * kBM;
@@ -112,17 +220,20 @@ __device__ __forceinline__ void pair_item_coords(const TcArgs& a, int item, int&
   }
 }
 
-template <int kMode>
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <int kMode, bool kHalf>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
-               const __grid_constant__ CUtensorMap tmbl, TcArgs a) {
+               const __grid_constant__ CUtensorMap tmbl, PairArgs a) {
+  constexpr int BK = kHalf ? 64 : 32;  // K per stage (one 128 B swizzle row of B)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = a.stages, AS = a.aslots;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  constexpr uint32_t x_bytes = kBM * kBK * 4;                          // this CTA's 128 A rows
-  const uint32_t bh_bytes = static_cast<uint32_t>(a.npad / 2) * kBK * 4;  // this CTA's half of B
+  constexpr uint32_t x_bytes = kBM * BK * 4;                              // this CTA's 128 A rows (fp32)
+  const uint32_t bh_bytes = static_cast<uint32_t>(a.npad / 2) * 128;     // this CTA's half of one B plane
   const uint32_t stage_bytes = x_bytes + 2 * bh_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* full_x = bars;
@@ -133,10 +244,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = aempty + AS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int run_k = a.run_stages * BK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -163,6 +276,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();  // peer barriers initialised before any remote arrival
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  float xs = 1.0f;  // s_x (fp16 encoding)
+  if (kHalf) xs = pow2_scale_for(a.xmax_in ? __uint_as_float(*a.xmax_in) : a.xmax_val);
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -174,14 +289,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int t0, k0, k1;
         pair_item_coords<kMode>(a, item, t0, k0, k1);
         const int mine = t0 + static_cast<int>(rank) * kBM;
-        for (int k = k0; k < k1; k += kBK) {
+        for (int k = k0; k < k1; k += BK) {
           mbar_wait(&empty[stage], phase ^ 1, 1);
           uint8_t* st = smem + stage * stage_bytes;
           mbar_expect_tx(&full_x[stage], x_bytes);
-          if (kMode == kXW)
-            tma_load_2d(st, &tmx, &full_x[stage], k, mine);
-          else
-            tma_load_2d(st, &tmx, &full_x[stage], mine, k);
+          if (kMode == kXW) {
+            tma_load_2d(st, &tmx, &full_x[stage], k, mine);  // [128 rows][32 fp32] SW128 sub-tiles
+            if (kHalf) tma_load_2d(st + 16384, &tmx, &full_x[stage], k + 32, mine);
+          } else {
+            tma_load_2d(st, &tmx, &full_x[stage], mine, k);  // [BK rows][128 cols]
+          }
           if (leader) mbar_expect_tx(&full_b[stage], 4 * bh_bytes);  // both halves, both planes
           tma_load_2d_pair(st + x_bytes, &tmbh, &full_b[stage], k, brow);
           tma_load_2d_pair(st + x_bytes + bh_bytes, &tmbl, &full_b[stage], k, brow);
@@ -192,20 +309,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only, whole warp) ----------------
     if (leader) {
-      const uint32_t idesc = idesc_tf32(2 * kBM, a.npad, 0, 0);
+      const uint32_t idesc = kHalf ? idesc_f16(2 * kBM, a.npad) : idesc_tf32(2 * kBM, a.npad, 0, 0);
       const uint64_t desc0 = sw128_desc(smem_u32(smem) + x_bytes, 16, 1024);
       int stage = 0, aslot = 0, rc = 0;
       uint32_t phase = 0, aphase = 0;
       for (int item = pair; item < a.items; item += npairs) {
         int t0, k0, k1;
         pair_item_coords<kMode>(a, item, t0, k0, k1);
-        for (int q0 = k0; q0 < k1; q0 += kRunStages * kBK, ++rc) {
+        for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
           const int b = rc % a.nrb;
           mbar_wait(&tempty[b], ((rc / a.nrb) & 1) ^ 1, 2);
           tc_fence_after();
           const uint32_t d = tmem_base + static_cast<uint32_t>(b * a.npad);
-          const int q1 = min(k1, q0 + kRunStages * kBK);
-          for (int k = q0; k < q1; k += kBK) {
+          const int q1 = min(k1, q0 + run_k);
+          for (int k = q0; k < q1; k += BK) {
             mbar_wait(&conv[aslot], aphase, 3);
             mbar_wait(&full_b[stage], phase, 3);
             tc_fence_after();
@@ -213,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t bl = bh + static_cast<uint64_t>(bh_bytes >> 4);
             const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 64);
             if (elect_one()) {
-              mma_stage_ts_pair(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u);
+              mma_stage_pair<kHalf>(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u);
               mma_commit_pair(&empty[stage]);
               mma_commit_pair(&aempty[aslot]);
             }
@@ -231,40 +348,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int i = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    float xmax = 0.0f;
     int stage = 0, aslot = 0;
     uint32_t phase = 0, aphase = 0;
     for (int item = pair; item < a.items; item += npairs) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
-      for (int k = k0; k < k1; k += kBK) {
+      for (int k = k0; k < k1; k += BK) {
         mbar_wait(&full_x[stage], phase, 4);
         mbar_wait(&aempty[aslot], aphase ^ 1, 4);
         tc_fence_after();
         const uint8_t* xt = smem + stage * stage_bytes;
-        float v[32];
-        if (kMode == kXW) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 f = *reinterpret_cast<const float4*>(xt + i * 128 + ((c ^ (i & 7)) << 4));
-            v[4 * c] = f.x;
-            v[4 * c + 1] = f.y;
-            v[4 * c + 2] = f.z;
-            v[4 * c + 3] = f.w;
-          }
-        } else {
-          const float* raw = reinterpret_cast<const float*>(xt);
-#pragma unroll
-          for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
-        }
-        float hi[32], lo[32];
-#pragma unroll
-        for (int kk = 0; kk < 32; ++kk) {
-          hi[kk] = tf32_trunc(v[kk]);
-          lo[kk] = tf32_trunc(v[kk] - hi[kk]);
-        }
         const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
-        tmem_st32(at, hi);
-        tmem_st32(at + 32, lo);
+#pragma unroll
+        for (int h = 0; h < (kHalf ? 2 : 1); ++h) {
+          float v[32];
+          if (kMode == kXW) {
+            // row i of a 128 B-swizzled [128][32] sub-tile: 16 B chunk c at (c ^ (i & 7))
+            const uint8_t* sub = xt + h * 16384;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 f = *reinterpret_cast<const float4*>(sub + i * 128 + ((c ^ (i & 7)) << 4));
+              v[4 * c] = f.x;
+              v[4 * c + 1] = f.y;
+              v[4 * c + 2] = f.z;
+              v[4 * c + 3] = f.w;
+            }
+          } else {
+            // column i of a plain [BK][128] tile, rows 32h..32h+31
+            const float* raw = reinterpret_cast<const float*>(xt) + h * 32 * kBM;
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
+          }
+          if (kMode == kXW && a.xmax_out) {
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) xmax = fmaxf(xmax, fabsf(v[kk]));
+          }
+          if (kHalf) {
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) v[kk] *= xs;
+            float hi[16], lo[16];
+            split_f16_32(v, hi, lo);
+            tmem_st16(at + h * 16, hi);
+            tmem_st16(at + 32 + h * 16, lo);
+          } else {
+            float hi[32], lo[32];
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+              hi[kk] = tf32_trunc(v[kk]);
+              lo[kk] = tf32_trunc(v[kk] - hi[kk]);
+            }
+            tmem_st32(at, hi);
+            tmem_st32(at + 32, lo);
+          }
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -273,37 +410,108 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ring_advance(aslot, aphase, AS);
       }
     }
+    if (kMode == kXW && a.xmax_out) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+      if (lane == 0) atomicMax(a.xmax_out, __float_as_uint(xmax));
+    }
   } else {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
     const int q = warp & 3;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t lacc = lane_base + static_cast<uint32_t>(a.nrb * a.npad);
+    const float xinv = 1.0f / xs;
     int rc = 0;
     for (int item = pair; item < a.items; item += npairs) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
-      const int runs = (k1 - k0 + kRunStages * kBK - 1) / (kRunStages * kBK);
-      const int row = t0 + static_cast<int>(rank) * kBM + q * 32 + lane;
+      const int runs = (k1 - k0 + run_k - 1) / run_k;
+      const int row = t0 + static_cast<int>(rank) * kBM + q * 32 + lane;  // XW: X row; XTU: X column
+      const bool to_planes16 = kMode == kXW && a.uh != nullptr;
+      // X^T U, fp16: each run's rows form one 128-row block of U^T scales. The
+      // next run's scales are fetched into registers while this run is folded
+      // and staged in this warp's row of red[] (broadcast reads).
+      float* runsc = red + q * a.npad;
+      float nxt[8];
+      auto fetch_scales = [&](int r) {
+        const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / 128) * a.npad;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = lane + 32 * j;
+          nxt[j] = c < a.npad ? __ldg(src + c) : 0.0f;  // scaled when staged (no stall here)
+        }
+      };
+      if (kMode == kXTU && kHalf) fetch_scales(0);
       for (int r = 0; r < runs; ++r, ++rc) {
         const int b = rc % a.nrb;
+        if (kMode == kXTU && kHalf) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (lane + 32 * j < a.npad) runsc[lane + 32 * j] = xinv * nxt[j];
+          __syncwarp();
+          if (r + 1 < runs) fetch_scales(r + 1);
+        }
         mbar_wait(&tfull[b], (rc / a.nrb) & 1, 5);
         tc_fence_after();
         const uint32_t racc = lane_base + static_cast<uint32_t>(b * a.npad);
         const bool first = r == 0, last = r == runs - 1;
+        if (!last || to_planes16) {
+          // fold the run into L: 32 columns per TMEM round trip (both loads
+          // issued before one wait; the fold is latency-bound otherwise)
+          int c0 = 0;
+          for (; c0 + 32 <= a.npad; c0 += 32) {
+            uint32_t rv[32], rs[32];
+            tmem_ld32_nowait(racc + c0, rv);
+            if (!first) tmem_ld32_nowait(lacc + c0, rs);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              v[e] = __uint_as_float(rv[e]);
+              if (kMode == kXTU && kHalf) v[e] *= runsc[c0 + e];
+              if (!first) v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+            }
+            tmem_st32(lacc + c0, v);
+          }
+          if (c0 < a.npad) {
+            uint32_t rv[16], rs[16];
+            tmem_ld16_nowait(racc + c0, rv);
+            if (!first) tmem_ld16_nowait(lacc + c0, rs);
+            tmem_ld_wait();
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              v[e] = __uint_as_float(rv[e]);
+              if (kMode == kXTU && kHalf) v[e] *= runsc[c0 + e];
+              if (!first) v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+            }
+            tmem_st16(lacc + c0, v);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
+          continue;
+        }
         for (int c0 = 0; c0 < a.npad; c0 += 16) {
           float v[16];
           tmem_ld16(racc + c0, v);
+          if (kMode == kXTU && kHalf) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] *= runsc[c0 + e];
+          }
           if (!first) {
             float s[16];
             tmem_ld16(lacc + c0, s);
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = __fadd_rn(v[e], s[e]);
           }
-          if (!last) {
-            tmem_st16(lacc + c0, v);
-            continue;
-          }
           if (kMode == kXW) {
+            if (kHalf) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[e] *= xinv * __ldg(a.winv + c0 + e);
+            }
             if (row < a.m) {
               if (a.out_hi) {
 #pragma unroll
@@ -328,10 +536,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (c0 + e < a.l) p[c0 + e] = static_cast<double>(v[e]);
           }
         }
-        if (!last) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
+      }
+      if (to_planes16) {
+        // OUT^T as fp16 hi/lo planes scaled per (column, 128-row block):
+        // pass 1 reduces each warp's column maxima of the raw accumulator,
+        // pass 1.5 turns the block maxima into per-column multipliers
+        // g[c] = f[c] s[c] (f = the accumulator's own unscale), pass 2 splits.
+        tc_fence_after();
+        const bool valid = row < a.m;
+        float* gsc = red + 4 * a.npad;
+        for (int c0 = 0; c0 < a.npad; c0 += 16) {
+          float v[16];
+          tmem_ld16(lacc + c0, v);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = valid ? fabsf(v[e]) : 0.0f;
+          const float mx = warp_max16(v, lane);
+          if ((lane & 1) == 0) red[q * a.npad + c0 + warp_max16_col(lane)] = mx;
+        }
+        epi_bar();
+        const int blk = (t0 + static_cast<int>(rank) * kBM) / kBM;
+        for (int c = q * 32 + lane; c < a.npad; c += 128) {
+          const float f = kHalf ? xinv * __ldg(a.winv + c) : 1.0f;
+          const float mx = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c])) * f;
+          const float sc = pow2_scale_for(mx);
+          gsc[c] = f * sc;
+          a.uinv[static_cast<size_t>(blk) * a.npad + c] = __frcp_rn(sc);
+        }
+        epi_bar();
+        for (int c0 = 0; c0 < a.npad; c0 += 16) {
+          float v[16];
+          tmem_ld16(lacc + c0, v);
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int c = c0 + e;
+              const float y = v[e] * gsc[c];
+              const __half h = __float2half_rn(y);
+              a.uh[static_cast<size_t>(c) * a.ldh + row] = h;
+              a.ul[static_cast<size_t>(c) * a.ldh + row] = __float2half_rn(y - __half2float(h));
+            }
+          }
+        }
+        tc_fence_before();
+        epi_bar();  // red[] reused by the next item
       }
     }
   }
@@ -342,4 +592,3 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tmem_dealloc2(tmem_base, a.tmem_cols);
   }
 }
-

@@ -10,7 +10,8 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "liblazypca_b200.so"
+LIB_PATH = Path(os.environ["LPCA_LIB_PATH"]) if os.environ.get("LPCA_LIB_PATH") else _PKG / "liblazypca_b200.so"
+# (LPCA_LIB_PATH: another build of the same library, for A/B timing experiments)
 
 LPCA_F32, LPCA_F64 = 4, 8
 LPCA_HOST, LPCA_DEVICE = 0, 1

@@ -469,8 +469,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
               v[e] = __uint_as_float(rv[e]);
-              if (kMode == kXTU && kHalf) v[e] *= runsc[c0 + e];
-              if (!first) v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+              if (kMode == kXTU && kHalf)  // power-of-two unscale: FFMA rounds exactly like mul + add
+                v[e] = first ? v[e] * runsc[c0 + e] : __fmaf_rn(v[e], runsc[c0 + e], __uint_as_float(rs[e]));
+              else if (!first)
+                v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
             }
             tmem_st32(lacc + c0, v);
           }
@@ -483,8 +485,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               v[e] = __uint_as_float(rv[e]);
-              if (kMode == kXTU && kHalf) v[e] *= runsc[c0 + e];
-              if (!first) v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+              if (kMode == kXTU && kHalf)  // power-of-two unscale: FFMA rounds exactly like mul + add
+                v[e] = first ? v[e] * runsc[c0 + e] : __fmaf_rn(v[e], runsc[c0 + e], __uint_as_float(rs[e]));
+              else if (!first)
+                v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
             }
             tmem_st16(lacc + c0, v);
           }

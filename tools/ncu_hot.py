@@ -30,7 +30,7 @@ print("samples", tot)
 for r in sorted(data, key=lambda r: -samp(r))[:n]:
     print(f"{samp(r) / tot * 100:5.1f}% {r[iE]:>10} {r[0][-5:]} {r[1][:90]}")
 if len(sys.argv) > 5:
-    sass = subprocess.run(["nvdisasm", "-g", sys.argv[4]], capture_output=True, text=True).stdout
+    sass = subprocess.run(["nvdisasm", "-gi", sys.argv[4]], capture_output=True, text=True).stdout
     frag = sys.argv[5]
     lines, on, loc = {}, False, None
     for ln in sass.splitlines():
@@ -41,17 +41,26 @@ if len(sys.argv) > 5:
             continue
         if not on:
             continue
-        m = re.search(r'## File "([^"]+)", line (\d+)', ln)
+        m = re.search(r'## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', ln)
         if m:
             loc = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
+            if m.group(3):
+                loc += f" @ {m.group(3).split('/')[-1]}:{m.group(4)}"
             continue
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+[^.\s]", ln)
         if m and loc:
             lines[int(m.group(1), 16)] = loc
     base = int(data[0][0], 16)
     agg = collections.Counter()
+    reasons = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    why = collections.defaultdict(collections.Counter)
     for r in data:
-        agg[lines.get(int(r[0], 16) - base, "?")] += samp(r)
-    print("--- by source line")
+        key = lines.get(int(r[0], 16) - base, "?")
+        agg[key] += samp(r)
+        for i in reasons:
+            if r[i].isdigit():
+                why[key][hdr[i][6:]] += int(r[i])
+    print("--- by source line (top stall reasons)")
     for k, v in agg.most_common(n):
-        print(f"{v / tot * 100:5.1f}% {k}")
+        top = ", ".join(f"{w} {c / max(v, 1) * 100:.0f}%" for w, c in why[k].most_common(3))
+        print(f"{v / tot * 100:5.1f}% {k:40s} {top}")

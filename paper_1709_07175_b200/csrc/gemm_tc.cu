@@ -410,7 +410,8 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad;
+  if (kHalf && a.scan && a.run_stages > a.stages) throw Error(kInternal, "tc pair: a run must fit the stage ring");
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad + 4 * 4 * kBM;
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
@@ -445,13 +446,14 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
   if (!tc_xw_supported(p.n, p.wpad)) throw Error(kInternal, "xw_pair: unsupported shape");
   if (p.ldx % 4 || (p.half ? p.ldw % 8 : p.ldw % 4) || (p.out_hi && p.ldh % 4) || (p.uh && p.ldh % 8))
     throw Error(kInternal, "xw_pair: leading dimensions must be 16-byte multiples");
-  if (p.half && ((!p.xmax_in && !(p.xmax_val > 0.0f)) || !p.winv)) throw Error(kInternal, "xw_pair: fp16 encoding needs its scales");
+  if (p.half && !p.winv) throw Error(kInternal, "xw_pair: fp16 encoding needs the W scales");
   PairArgs a{};
   a.m = static_cast<int>(p.m);
   a.n = static_cast<int>(p.n);
   a.npad = static_cast<int>(p.wpad);
   a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
   a.run_stages = env_int("LPCA_TC_RUN", p.half ? 2 : 4);
+  a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f);
   a.xmax_in = p.xmax_in;
   a.xmax_val = p.xmax_val;
   a.xmax_out = p.xmax_out;
@@ -497,7 +499,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
   if (!tc_utx_supported(p.l, p.n)) throw Error(kInternal, "utx_pair: unsupported shape");
   if (p.ldx % 4 || (p.half ? p.ldt % 8 : p.ldt % 4))
     throw Error(kInternal, "utx_pair: leading dimensions must be 16-byte multiples");
-  if (p.half && (!p.xmax_in || !p.uinv)) throw Error(kInternal, "utx_pair: fp16 encoding needs its scales");
+  if (p.half && !p.uinv) throw Error(kInternal, "utx_pair: fp16 encoding needs the U^T scales");
   index_t rows = 0;
   const index_t chunks = utx_pair_splits(p.m, p.n, num_sms, &rows);
   PairArgs a{};
@@ -507,6 +509,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
   a.chunk_rows = static_cast<int>(rows);
   a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
   a.run_stages = p.half ? 2 : 4;  // fp16: one run per 128-row block of U^T scales
+  a.scan = p.half && !p.xmax_in;
   a.xmax_in = p.xmax_in;
   a.uinv_in = p.uinv;
   a.part = p.part;

@@ -693,10 +693,12 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
       u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
     }
-    // sketch U = X Omega (reducer.cpp:163-169); tf32, records max|X|
-    xs.record = true;
-    xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &xs : nullptr);
-    xs.record = false;
+    // sketch U = X Omega (reducer.cpp:163-169): fp16 with per-(row, run) scales
+    // scanned in-kernel, recording max|X| for the single scale of later passes
+    XScale sketch;
+    sketch.use = true;
+    sketch.check = xs.dev;
+    xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
     xs.use = f16;
     ev.mark(1);
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)

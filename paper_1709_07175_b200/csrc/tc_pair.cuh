@@ -45,7 +45,10 @@ struct PairArgs {
   uint32_t tmem_cols;
   int items;
   int chunk_rows;    // XTU: rows per chunk (multiple of 128)
-  // fp16 encoding: max|X| (s_x derived in-kernel) from *xmax_in (bits) or xmax_val
+  // fp16 A scale: scan = 1 gives every (row, run) its own power of two from the
+  // run's values (scanned in shared memory first); scan = 0 uses one scale for
+  // all of X from max|X| = *xmax_in (bits) or xmax_val
+  int scan;
   const uint32_t* xmax_in;
   float xmax_val;
   // X W: accumulate max|X| bits of the data actually read here (nullable)
@@ -244,7 +247,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = aempty + AS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima / run scales
+  float* rsc = red + 5 * a.npad;  // after red [4][npad] + gsc [npad]: [4 runs][128] inverse A-row scales
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);
@@ -349,65 +353,102 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int i = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     float xmax = 0.0f;
-    int stage = 0, aslot = 0;
+    int stage = 0, aslot = 0, rc = 0;
     uint32_t phase = 0, aphase = 0;
+    auto load_row = [&](const uint8_t* xt, int h, float (&v)[32]) {
+      if (kMode == kXW) {
+        // row i of a 128 B-swizzled [128][32] sub-tile: 16 B chunk c at (c ^ (i & 7))
+        const uint8_t* sub = xt + h * 16384;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 f = *reinterpret_cast<const float4*>(sub + i * 128 + ((c ^ (i & 7)) << 4));
+          v[4 * c] = f.x;
+          v[4 * c + 1] = f.y;
+          v[4 * c + 2] = f.z;
+          v[4 * c + 3] = f.w;
+        }
+      } else {
+        // column i of a plain [BK][128] tile, rows 32h..32h+31
+        const float* raw = reinterpret_cast<const float*>(xt) + h * 32 * kBM;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
+      }
+    };
+    auto absmax32 = [](float (&v)[32]) {  // tree (a serial max chain is latency-bound); clobbers v
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = fmaxf(fabsf(v[kk]), fabsf(v[kk + 16]));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) v[kk] = fmaxf(v[kk], v[kk + 8]);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) v[kk] = fmaxf(v[kk], v[kk + 4]);
+      return fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+    };
     for (int item = pair; item < a.items; item += npairs) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
-      for (int k = k0; k < k1; k += BK) {
-        mbar_wait(&full_x[stage], phase, 4);
-        mbar_wait(&aempty[aslot], aphase ^ 1, 4);
-        tc_fence_after();
-        const uint8_t* xt = smem + stage * stage_bytes;
-        const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+      for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
+        const int nst = (min(k1, q0 + run_k) - q0 + BK - 1) / BK;
+        float sx = xs;
+        if (kHalf && a.scan) {  // the run's stages are all resident (run_stages <= stages)
+          float mx = 0.0f;
+          int st = stage;
+          uint32_t ph = phase;
+          for (int j = 0; j < nst; ++j) {
+            mbar_wait(&full_x[st], ph, 4);
+            const uint8_t* xt = smem + st * stage_bytes;
 #pragma unroll
-        for (int h = 0; h < (kHalf ? 2 : 1); ++h) {
-          float v[32];
-          if (kMode == kXW) {
-            // row i of a 128 B-swizzled [128][32] sub-tile: 16 B chunk c at (c ^ (i & 7))
-            const uint8_t* sub = xt + h * 16384;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float4 f = *reinterpret_cast<const float4*>(sub + i * 128 + ((c ^ (i & 7)) << 4));
-              v[4 * c] = f.x;
-              v[4 * c + 1] = f.y;
-              v[4 * c + 2] = f.z;
-              v[4 * c + 3] = f.w;
+            for (int h = 0; h < 2; ++h) {
+              float v[32];
+              load_row(xt, h, v);
+              mx = fmaxf(mx, absmax32(v));
             }
-          } else {
-            // column i of a plain [BK][128] tile, rows 32h..32h+31
-            const float* raw = reinterpret_cast<const float*>(xt) + h * 32 * kBM;
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
+            ring_advance(st, ph, S);
           }
-          if (kMode == kXW && a.xmax_out) {
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) xmax = fmaxf(xmax, fabsf(v[kk]));
-          }
-          if (kHalf) {
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) v[kk] *= xs;
-            float hi[16], lo[16];
-            split_f16_32(v, hi, lo);
-            tmem_st16(at + h * 16, hi);
-            tmem_st16(at + 32 + h * 16, lo);
-          } else {
-            float hi[32], lo[32];
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) {
-              hi[kk] = tf32_trunc(v[kk]);
-              lo[kk] = tf32_trunc(v[kk] - hi[kk]);
-            }
-            tmem_st32(at, hi);
-            tmem_st32(at + 32, lo);
-          }
+          sx = pow2_scale_for(mx);
+          rsc[(rc & 3) * kBM + i] = __frcp_rn(sx);
+          xmax = fmaxf(xmax, mx);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&conv[aslot]), 0));
-        ring_advance(stage, phase, S);
-        ring_advance(aslot, aphase, AS);
+        for (int j = 0; j < nst; ++j) {
+          mbar_wait(&full_x[stage], phase, 4);
+          mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+          tc_fence_after();
+          const uint8_t* xt = smem + stage * stage_bytes;
+          const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+#pragma unroll
+          for (int h = 0; h < (kHalf ? 2 : 1); ++h) {
+            float v[32];
+            load_row(xt, h, v);
+            if (kMode == kXW && a.xmax_out && !a.scan) {
+              float t[32];
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) t[kk] = v[kk];
+              xmax = fmaxf(xmax, absmax32(t));
+            }
+            if (kHalf) {
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) v[kk] *= sx;
+              float hi[16], lo[16];
+              split_f16_32(v, hi, lo);
+              tmem_st16(at + h * 16, hi);
+              tmem_st16(at + 32 + h * 16, lo);
+            } else {
+              float hi[32], lo[32];
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) {
+                hi[kk] = tf32_trunc(v[kk]);
+                lo[kk] = tf32_trunc(v[kk] - hi[kk]);
+              }
+              tmem_st32(at, hi);
+              tmem_st32(at + 32, lo);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&conv[aslot]), 0));
+          ring_advance(stage, phase, S);
+          ring_advance(aslot, aphase, AS);
+        }
       }
     }
     if (kMode == kXW && a.xmax_out) {
@@ -448,7 +489,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            if (lane + 32 * j < a.npad) runsc[lane + 32 * j] = xinv * nxt[j];
+            if (lane + 32 * j < a.npad) runsc[lane + 32 * j] = nxt[j];
           __syncwarp();
           if (r + 1 < runs) fetch_scales(r + 1);
         }
@@ -456,6 +497,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t racc = lane_base + static_cast<uint32_t>(b * a.npad);
         const bool first = r == 0, last = r == runs - 1;
+        // this run's A-row unscale (XW: X row; XTU: X column `row`): power of two
+        const float rowf = kHalf ? (a.scan ? rsc[(rc & 3) * kBM + q * 32 + lane] : xinv) : 1.0f;
         if (!last || to_planes16) {
           // fold the run into L: 32 columns per TMEM round trip (both loads
           // issued before one wait; the fold is latency-bound otherwise)
@@ -469,10 +512,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
               v[e] = __uint_as_float(rv[e]);
-              if (kMode == kXTU && kHalf)  // power-of-two unscale: FFMA rounds exactly like mul + add
-                v[e] = first ? v[e] * runsc[c0 + e] : __fmaf_rn(v[e], runsc[c0 + e], __uint_as_float(rs[e]));
-              else if (!first)
+              if (kHalf) {  // power-of-two unscale: the FFMA rounds exactly like mul + add
+                const float f = kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
+                v[e] = first ? v[e] * f : __fmaf_rn(v[e], f, __uint_as_float(rs[e]));
+              } else if (!first) {
                 v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+              }
             }
             tmem_st32(lacc + c0, v);
           }
@@ -485,10 +530,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               v[e] = __uint_as_float(rv[e]);
-              if (kMode == kXTU && kHalf)  // power-of-two unscale: FFMA rounds exactly like mul + add
-                v[e] = first ? v[e] * runsc[c0 + e] : __fmaf_rn(v[e], runsc[c0 + e], __uint_as_float(rs[e]));
-              else if (!first)
+              if (kHalf) {  // power-of-two unscale: the FFMA rounds exactly like mul + add
+                const float f = kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
+                v[e] = first ? v[e] * f : __fmaf_rn(v[e], f, __uint_as_float(rs[e]));
+              } else if (!first) {
                 v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+              }
             }
             tmem_st16(lacc + c0, v);
           }
@@ -501,9 +548,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < a.npad; c0 += 16) {
           float v[16];
           tmem_ld16(racc + c0, v);
-          if (kMode == kXTU && kHalf) {
+          if (kHalf) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] *= runsc[c0 + e];
+            for (int e = 0; e < 16; ++e) v[e] *= kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
           }
           if (!first) {
             float s[16];
@@ -514,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (kMode == kXW) {
             if (kHalf) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) v[e] *= xinv * __ldg(a.winv + c0 + e);
+              for (int e = 0; e < 16; ++e) v[e] *= __ldg(a.winv + c0 + e);
             }
             if (row < a.m) {
               if (a.out_hi) {
@@ -563,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         epi_bar();
         const int blk = (t0 + static_cast<int>(rank) * kBM) / kBM;
         for (int c = q * 32 + lane; c < a.npad; c += 128) {
-          const float f = kHalf ? xinv * __ldg(a.winv + c) : 1.0f;
+          const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
           const float mx = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c])) * f;
           const float sc = pow2_scale_for(mx);
           gsc[c] = f * sc;

@@ -93,10 +93,13 @@ typedef struct {
 } lpca_config;
 
 /* lazypca::ReducerTimings (proj/core/include/lazypca/reducer.hpp:59-66),
- * seconds, device-event timed; `power` and `transform` are extensions. */
+ * seconds, device-event timed; `power` and `transform` are extensions, and the
+ * *_pass fields time the X-pass kernel alone inside its phase (sketch U = X Omega,
+ * F = U^T X, Y = X V), without operand preparation or partial-sum reduction. */
 typedef struct {
   double sketch, qr, f_form, svd, total;
   double power, transform, h2d, d2h;
+  double sketch_pass, f_pass, transform_pass;
 } lpca_timings;
 
 typedef struct lpca_ctx lpca_ctx;

@@ -38,7 +38,8 @@ class Config(C.Structure):
 
 class Timings(C.Structure):
     _fields_ = [(f, C.c_double) for f in
-                ("sketch", "qr", "f_form", "svd", "total", "power", "transform", "h2d", "d2h")]
+                ("sketch", "qr", "f_form", "svd", "total", "power", "transform", "h2d", "d2h",
+                 "sketch_pass", "f_pass", "transform_pass")]
 
 
 class MapInfo(C.Structure):

@@ -235,6 +235,9 @@ class ReducerTimings:
     transform: float = 0.0
     h2d: float = 0.0
     d2h: float = 0.0
+    sketch_pass: float = 0.0     # the X-pass kernels alone (extension)
+    f_pass: float = 0.0
+    transform_pass: float = 0.0
 
 
 def _fill_timings(t: Optional[ReducerTimings], c: L.Timings) -> None:

@@ -103,7 +103,8 @@ struct lpca_ctx {
   int last_sweeps = 0;
   int eigensolver = 0;  // 0: tridiagonal route (tridiag_eigh), 1: parallel Jacobi (jacobi_eigh)
   std::unordered_map<std::string, std::pair<void*, std::size_t>> ws;
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[18] = {};
+  int pass_slot = -1;  // >= 0: the next X pass records ev[pass_slot] / ev[pass_slot + 1] around its kernel
 
   void note_launch(int n = 1) { launches += n; }
 
@@ -365,6 +366,12 @@ bool f16_enabled() {
 
 index_t planes_ld(index_t m) { return round_up(m > 0 ? m : 1, 4); }
 
+// Brackets the X-pass kernel itself (not its operand preparation) with the
+// context's pass events, for the per-kernel times in lpca_timings.
+void pass_mark(lpca_ctx& ctx, int which) {
+  if (ctx.pass_slot >= 0) LPCA_CUDA(cudaEventRecord(ctx.ev[ctx.pass_slot + which], ctx.stream));
+}
+
 // out = X W, W fp64 column-major (n x wc, ld ldw). For fp32 X the operand is
 // prepared once per call (rounded to fp32, or split into tf32 hi/lo planes).
 void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, const Panel& out,
@@ -372,9 +379,11 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
   const index_t m = x.m, n = x.n;
   if (m == 0) return;
   if (x.dtype == 8) {
+    pass_mark(ctx, 0);
     launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, w, wc,
                                    ldw, static_cast<double*>(out.plain), out.ld, 1, exact);
     LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 1);
     return;
   }
   if (use_tc(ctx, x, wc) && tc_pair_mode()) {
@@ -421,8 +430,10 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
       p.out_lo = out.lo;
       p.ldh = out.ldt;
     }
+    pass_mark(ctx, 0);
     launch_xw_pair(ctx.stream, p, ctx.num_sms);
     LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 1);
     return;
   }
   if (use_tc(ctx, x, wc)) {
@@ -431,18 +442,22 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
     float* lo = ctx.get<float>("w.lo", wpad * n);
     launch_split_tf32_w(ctx.stream, w, ldw, n, wc, wpad, hi, lo, n);
     LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 0);
     launch_xw_tc_planes(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, hi, lo, wpad, n,
                         static_cast<float*>(out.plain), out.ld, wc, out.hi, out.lo, out.ldt,
                         ctx.num_sms);
     LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 1);
     return;
   }
   float* w32 = ctx.get<float>("w.f32", wc * n);
   launch_convert_f64_to_f32(ctx.stream, w, ldw, w32, n, n, wc, 1.0);
   LPCA_LAUNCHED(ctx);
+  pass_mark(ctx, 0);
   launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, w32, wc, n,
                                static_cast<float*>(out.plain), out.ld, 1, false);
   LPCA_LAUNCHED(ctx);
+  pass_mark(ctx, 1);
 }
 
 index_t pick_chunks(const lpca_ctx& ctx, index_t m, index_t tiles, bool exact) {
@@ -483,11 +498,13 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
     p.l = l;
     p.n = n;
     p.part = part;
+    pass_mark(ctx, 0);
     launch_utx_pair(ctx.stream, p, ctx.num_sms);
   } else if (u.hi && x.dtype == 4) {
     index_t rps = 0;
     chunks = utx_tc_splits(m, l, n, ctx.num_sms, &rps);
     part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+    pass_mark(ctx, 0);
     launch_utx_tc_planes(ctx.stream, u.hi, u.lo, u.ldt, static_cast<const float*>(x.p), x.ld, m, l, n, part,
                          ctx.num_sms);
   } else {
@@ -495,6 +512,7 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
     const index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
     chunks = ceil_div(m, chunk_rows);
     part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);
+    pass_mark(ctx, 0);
     if (x.dtype == 4)
       launch_utx_simt<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld,
                              static_cast<const float*>(x.p), x.ld, m, l, n, chunk_rows, part, false);
@@ -503,6 +521,7 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
                               static_cast<const double*>(x.p), x.ld, m, l, n, chunk_rows, part, exact);
   }
   LPCA_LAUNCHED(ctx);
+  pass_mark(ctx, 1);
   if (chunks > 1) {
     launch_reduce_partials(ctx.stream, part, chunks, l * n, f);
     LPCA_LAUNCHED(ctx);
@@ -698,7 +717,11 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     XScale sketch;
     sketch.use = true;
     sketch.check = xs.dev;
+    ev.mark(12);
+    ev.mark(13);
+    ctx.pass_slot = 12;
     xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
+    ctx.pass_slot = -1;
     xs.use = f16;
     ev.mark(1);
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
@@ -774,7 +797,11 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       }
     }
     ev.mark(3);
+    ev.mark(14);
+    ev.mark(15);
+    ctx.pass_slot = 14;
     utx_pass(ctx, x, u, l, f, exact, &xs);  // F = U^T X (or Q^T X)
+    ctx.pass_slot = -1;
     ev.mark(4);
     finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
     if (f16) LPCA_CUDA(cudaMemcpyAsync(&map->xmax, xs.dev, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
@@ -787,6 +814,8 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       t->f_form += ev.secs(3, 4);
       t->svd += ev.secs(4, 5);
       t->total += ev.secs(0, 5);
+      t->sketch_pass += ev.secs(12, 13);
+      t->f_pass += ev.secs(14, 15);
     }
     return map;
   } catch (...) {
@@ -808,6 +837,9 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
   if (ldy <= 0) ldy = row ? k : m;
   PhaseEvents ev(ctx);
   ev.mark(6);
+  ev.mark(16);
+  ev.mark(17);
+  ctx.pass_slot = 16;
   if (m > 0 && k > 0) {
     const std::size_t ybytes = dsize(y_dtype) * static_cast<std::size_t>(row ? m * ldy : k * ldy);
     void* ydev = y_location == LPCA_DEVICE ? y : ctx.buf("y", ybytes);
@@ -854,17 +886,20 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       LPCA_LAUNCHED(ctx);
     }
     ev.mark(7);
+    ctx.pass_slot = -1;
     if (y_location == LPCA_HOST) {
       LPCA_CUDA(cudaMemcpyAsync(y, ydev, ybytes, cudaMemcpyDeviceToHost, ctx.stream));
       if (d2h) *d2h += static_cast<double>(ybytes);
     }
   } else {
     ev.mark(7);
+    ctx.pass_slot = -1;
   }
   ev.mark(8);
   LPCA_CUDA(cudaEventSynchronize(ctx.ev[8]));
   if (t) {
     t->transform += ev.secs(6, 7);
+    t->transform_pass += ev.secs(16, 17);
     t->d2h += ev.secs(7, 8);
   }
 }

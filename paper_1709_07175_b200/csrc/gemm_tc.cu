@@ -404,7 +404,7 @@ constexpr uint32_t kPairSmemBudget = 208 * 1024;
 
 template <int kMode, bool kHalf>
 void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const CUtensorMap& tl, PairArgs& a,
-                 int num_sms) {
+                 int num_sms, cudaEvent_t ev_pre = nullptr, cudaEvent_t ev_post = nullptr) {
   if (!plan_tmem(a.npad, a.nrb, a.aslots, a.tmem_cols)) throw Error(kInternal, "tc pair: TMEM plan failed");
   const uint32_t bk = kHalf ? 64 : 32;
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
@@ -415,7 +415,9 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
+  if (ev_pre) LPCA_CUDA(cudaEventRecord(ev_pre, s));
   tc2_kernel<kMode, kHalf><<<2 * pairs, kThreads, smem, s>>>(tx, th, tl, a);
+  if (ev_post) LPCA_CUDA(cudaEventRecord(ev_post, s));
 }
 
 template <int kMode>
@@ -472,11 +474,11 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
   if (p.half) {
     const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 64, brows, true, 2);
     const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 64, brows, true, 2);
-    launch_pair<kXW, true>(s, tx, th, tl, a, num_sms);
+    launch_pair<kXW, true>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
   } else {
     const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 32, brows, true);
     const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 32, brows, true);
-    launch_pair<kXW, false>(s, tx, th, tl, a, num_sms);
+    launch_pair<kXW, false>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
   }
 }
 
@@ -519,12 +521,12 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
     const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 64, false);
     const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 64, brows, true, 2);
     const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 64, brows, true, 2);
-    launch_pair<kXTU, true>(s, tx, th, tl, a, num_sms);
+    launch_pair<kXTU, true>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
   } else {
     const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 32, false);
     const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 32, brows, true);
     const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 32, brows, true);
-    launch_pair<kXTU, false>(s, tx, th, tl, a, num_sms);
+    launch_pair<kXTU, false>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
   }
 }
 

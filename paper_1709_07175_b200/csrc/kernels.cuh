@@ -107,6 +107,7 @@ struct XwPairArgs {
   __half* ul = nullptr;
   float* uinv = nullptr;         // ... with inverse scales [ceil(m/128)][wpad]
   index_t ldh = 0;
+  cudaEvent_t ev_pre = nullptr, ev_post = nullptr;  // recorded around the kernel launch itself
 };
 struct UtxPairArgs {
   bool half = false;
@@ -118,6 +119,7 @@ struct UtxPairArgs {
   const float* x = nullptr;
   index_t ldx = 0, m = 0, l = 0, n = 0;
   double* part = nullptr;  // [chunks][n][l] (utx_pair_splits)
+  cudaEvent_t ev_pre = nullptr, ev_post = nullptr;
 };
 bool tc_pair_mode();
 void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms);

@@ -430,10 +430,12 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
       p.out_lo = out.lo;
       p.ldh = out.ldt;
     }
-    pass_mark(ctx, 0);
+    if (ctx.pass_slot >= 0) {  // the launcher records them around the kernel itself
+      p.ev_pre = ctx.ev[ctx.pass_slot];
+      p.ev_post = ctx.ev[ctx.pass_slot + 1];
+    }
     launch_xw_pair(ctx.stream, p, ctx.num_sms);
     LPCA_LAUNCHED(ctx);
-    pass_mark(ctx, 1);
     return;
   }
   if (use_tc(ctx, x, wc)) {
@@ -498,7 +500,10 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
     p.l = l;
     p.n = n;
     p.part = part;
-    pass_mark(ctx, 0);
+    if (ctx.pass_slot >= 0) {
+      p.ev_pre = ctx.ev[ctx.pass_slot];
+      p.ev_post = ctx.ev[ctx.pass_slot + 1];
+    }
     launch_utx_pair(ctx.stream, p, ctx.num_sms);
   } else if (u.hi && x.dtype == 4) {
     index_t rps = 0;

@@ -434,6 +434,7 @@ void launch(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, const 
 }  // namespace
 
 bool tc_xw_supported(index_t n, index_t wpad) {
+  if (pair_mode()) return wpad >= 16 && wpad % 16 == 0 && n >= 1 && wpad <= 4096;  // sliced above pair_max_n()
   int nrb, as;
   uint32_t cols;
   return wpad >= 16 && wpad <= 256 && wpad % 16 == 0 && n >= 1 && plan_tmem(static_cast<int>(wpad), nrb, as, cols);
@@ -443,42 +444,59 @@ bool tc_utx_supported(index_t l, index_t n) { return l >= 1 && n >= 1 && tc_xw_s
 
 bool tc_pair_mode() { return pair_mode(); }
 
+// Widths above this run as column slices over X (one launch per slice): TMEM
+// holds two run buffers, the long accumulator and two A slots only for N <= 128.
+int pair_max_n() { return env_int("LPCA_TC_MAXN", 128); }
+
+// Column slices of a padded width: ceil(wpad / max) slices of equal 16-multiples.
+int slice_width(index_t wpad) {
+  const index_t nsl = ceil_div(wpad, static_cast<index_t>(pair_max_n()));
+  return static_cast<int>(round_up(ceil_div(wpad, nsl), 16));
+}
+
 void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
   if (p.m <= 0) return;
-  if (!tc_xw_supported(p.n, p.wpad)) throw Error(kInternal, "xw_pair: unsupported shape");
+  if (p.wpad < 16 || p.wpad % 16 || p.n < 1) throw Error(kInternal, "xw_pair: unsupported shape");
   if (p.ldx % 4 || (p.half ? p.ldw % 8 : p.ldw % 4) || (p.out_hi && p.ldh % 4) || (p.uh && p.ldh % 8))
     throw Error(kInternal, "xw_pair: leading dimensions must be 16-byte multiples");
   if (p.half && !p.winv) throw Error(kInternal, "xw_pair: fp16 encoding needs the W scales");
-  PairArgs a{};
-  a.m = static_cast<int>(p.m);
-  a.n = static_cast<int>(p.n);
-  a.npad = static_cast<int>(p.wpad);
-  a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
-  a.run_stages = env_int("LPCA_TC_RUN", p.half ? 2 : 4);
-  a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f);
-  a.xmax_in = p.xmax_in;
-  a.xmax_val = p.xmax_val;
-  a.xmax_out = p.xmax_out;
-  a.winv = p.winv;
-  a.wstore = static_cast<int>(p.wstore);
-  a.out = p.out;
-  a.ldo = static_cast<int>(p.ldo);
-  a.out_hi = p.out_hi;
-  a.out_lo = p.out_lo;
-  a.uh = p.uh;
-  a.ul = p.ul;
-  a.uinv = p.uinv;
-  a.ldh = static_cast<int>(p.ldh);
-  const uint32_t brows = static_cast<uint32_t>(p.wpad / 2);
-  const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, 32, kBM, true);
-  if (p.half) {
-    const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 64, brows, true, 2);
-    const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 64, brows, true, 2);
-    launch_pair<kXW, true>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
-  } else {
-    const CUtensorMap th = map_2d(p.w_hi, p.n, p.wpad, p.ldw, 32, brows, true);
-    const CUtensorMap tl = map_2d(p.w_lo, p.n, p.wpad, p.ldw, 32, brows, true);
-    launch_pair<kXW, false>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
+  const int esz = p.half ? 2 : 4;
+  const int sw = slice_width(p.wpad);
+  for (index_t c0 = 0; c0 < p.wpad; c0 += sw) {
+    const int wc = static_cast<int>(p.wpad - c0 < sw ? p.wpad - c0 : sw);
+    PairArgs a{};
+    a.m = static_cast<int>(p.m);
+    a.n = static_cast<int>(p.n);
+    a.npad = wc;
+    a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
+    a.run_stages = env_int("LPCA_TC_RUN", p.half ? 2 : 4);
+    a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f);
+    a.xmax_in = p.xmax_in;
+    a.xmax_val = p.xmax_val;
+    a.xmax_out = c0 == 0 ? p.xmax_out : nullptr;
+    a.winv = p.winv ? p.winv + c0 : nullptr;
+    const index_t st = p.wstore - c0;
+    a.wstore = static_cast<int>(st < 0 ? 0 : (st < wc ? st : wc));
+    a.out = p.out ? p.out + c0 : nullptr;
+    a.ldo = static_cast<int>(p.ldo);
+    a.out_hi = p.out_hi ? p.out_hi + c0 * p.ldh : nullptr;
+    a.out_lo = p.out_lo ? p.out_lo + c0 * p.ldh : nullptr;
+    a.uh = p.uh ? p.uh + c0 * p.ldh : nullptr;
+    a.ul = p.ul ? p.ul + c0 * p.ldh : nullptr;
+    a.uinv = p.uinv ? p.uinv + c0 : nullptr;
+    a.uinv_ld = static_cast<int>(p.wpad);
+    a.ldh = static_cast<int>(p.ldh);
+    const uint32_t brows = static_cast<uint32_t>(wc / 2);
+    const char* wh = static_cast<const char*>(p.w_hi) + c0 * p.ldw * esz;
+    const char* wl = static_cast<const char*>(p.w_lo) + c0 * p.ldw * esz;
+    const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, 32, kBM, true);
+    const CUtensorMap th = map_2d(wh, p.n, wc, p.ldw, p.half ? 64 : 32, brows, true, esz);
+    const CUtensorMap tl = map_2d(wl, p.n, wc, p.ldw, p.half ? 64 : 32, brows, true, esz);
+    const bool first = c0 == 0, last = c0 + sw >= p.wpad;
+    if (p.half)
+      launch_pair<kXW, true>(s, tx, th, tl, a, num_sms, first ? p.ev_pre : nullptr, last ? p.ev_post : nullptr);
+    else
+      launch_pair<kXW, false>(s, tx, th, tl, a, num_sms, first ? p.ev_pre : nullptr, last ? p.ev_post : nullptr);
   }
 }
 
@@ -498,35 +516,46 @@ index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_spl
 
 void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
   const index_t npad = round_up(p.l, 16);
-  if (!tc_utx_supported(p.l, p.n)) throw Error(kInternal, "utx_pair: unsupported shape");
+  if (p.l < 1 || p.n < 1) throw Error(kInternal, "utx_pair: unsupported shape");
   if (p.ldx % 4 || (p.half ? p.ldt % 8 : p.ldt % 4))
     throw Error(kInternal, "utx_pair: leading dimensions must be 16-byte multiples");
   if (p.half && !p.uinv) throw Error(kInternal, "utx_pair: fp16 encoding needs the U^T scales");
   index_t rows = 0;
   const index_t chunks = utx_pair_splits(p.m, p.n, num_sms, &rows);
-  PairArgs a{};
-  a.m = static_cast<int>(p.m);
-  a.n = static_cast<int>(p.n);
-  a.npad = static_cast<int>(npad);
-  a.chunk_rows = static_cast<int>(rows);
-  a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
-  a.run_stages = p.half ? 2 : 4;  // fp16: one run per 128-row block of U^T scales
-  a.scan = p.half && !p.xmax_in;
-  a.xmax_in = p.xmax_in;
-  a.uinv_in = p.uinv;
-  a.part = p.part;
-  a.l = static_cast<int>(p.l);
-  const uint32_t brows = static_cast<uint32_t>(npad / 2);
-  if (p.half) {
-    const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 64, false);
-    const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 64, brows, true, 2);
-    const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 64, brows, true, 2);
-    launch_pair<kXTU, true>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
-  } else {
-    const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 32, false);
-    const CUtensorMap th = map_2d(p.u_hi, p.m, npad, p.ldt, 32, brows, true);
-    const CUtensorMap tl = map_2d(p.u_lo, p.m, npad, p.ldt, 32, brows, true);
-    launch_pair<kXTU, false>(s, tx, th, tl, a, num_sms, p.ev_pre, p.ev_post);
+  const int esz = p.half ? 2 : 4;
+  const int sw = slice_width(npad);
+  for (index_t c0 = 0; c0 < npad; c0 += sw) {
+    const int wc = static_cast<int>(npad - c0 < sw ? npad - c0 : sw);
+    PairArgs a{};
+    a.m = static_cast<int>(p.m);
+    a.n = static_cast<int>(p.n);
+    a.npad = wc;
+    a.chunk_rows = static_cast<int>(rows);
+    a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
+    a.run_stages = p.half ? 2 : 4;  // fp16: one run per 128-row block of U^T scales
+    a.scan = p.half && !p.xmax_in;
+    a.xmax_in = p.xmax_in;
+    a.uinv_in = p.uinv ? p.uinv + c0 : nullptr;
+    a.uinv_ld = static_cast<int>(npad);
+    a.part = p.part + c0;
+    const index_t lc = p.l - c0;
+    a.l = static_cast<int>(lc < wc ? lc : wc);
+    a.l_ld = static_cast<int>(p.l);
+    const uint32_t brows = static_cast<uint32_t>(wc / 2);
+    const char* uh = static_cast<const char*>(p.u_hi) + c0 * p.ldt * esz;
+    const char* ul = static_cast<const char*>(p.u_lo) + c0 * p.ldt * esz;
+    const bool first = c0 == 0, last = c0 + sw >= npad;
+    if (p.half) {
+      const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 64, false);
+      const CUtensorMap th = map_2d(uh, p.m, wc, p.ldt, 64, brows, true, 2);
+      const CUtensorMap tl = map_2d(ul, p.m, wc, p.ldt, 64, brows, true, 2);
+      launch_pair<kXTU, true>(s, tx, th, tl, a, num_sms, first ? p.ev_pre : nullptr, last ? p.ev_post : nullptr);
+    } else {
+      const CUtensorMap tx = map_2d(p.x, p.n, p.m, p.ldx, kBM, 32, false);
+      const CUtensorMap th = map_2d(uh, p.m, wc, p.ldt, 32, brows, true);
+      const CUtensorMap tl = map_2d(ul, p.m, wc, p.ldt, 32, brows, true);
+      launch_pair<kXTU, false>(s, tx, th, tl, a, num_sms, first ? p.ev_pre : nullptr, last ? p.ev_post : nullptr);
+    }
   }
 }
 

@@ -68,7 +68,9 @@ struct PairArgs {
   // X^T U: U^T block inverse scales (fp16), partial output part[chunk][j * l + r]
   const float* uinv_in;
   double* part;
-  int l;
+  int l;      // X^T U: columns r < l of the part rows are stored ...
+  int l_ld;   // ... with row stride l_ld (N-split launches write column slices)
+  int uinv_ld;  // row stride of the [block][c] inverse scales (uinv / uinv_in)
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -475,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float* runsc = red + q * a.npad;
       float nxt[8];
       auto fetch_scales = [&](int r) {
-        const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / 128) * a.npad;
+        const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / 128) * a.uinv_ld;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = lane + 32 * j;
@@ -581,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           } else if (row < a.n) {
             const int ntiles = (a.n + 2 * kBM - 1) / (2 * kBM);
-            double* p = a.part + static_cast<size_t>(item / ntiles) * a.l * a.n + static_cast<size_t>(row) * a.l;
+            double* p = a.part + static_cast<size_t>(item / ntiles) * a.l_ld * a.n + static_cast<size_t>(row) * a.l_ld;
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               if (c0 + e < a.l) p[c0 + e] = static_cast<double>(v[e]);
@@ -614,7 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const float mx = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c])) * f;
           const float sc = pow2_scale_for(mx);
           gsc[c] = f * sc;
-          a.uinv[static_cast<size_t>(blk) * a.npad + c] = __frcp_rn(sc);
+          a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
         }
         epi_bar();
         for (int c0 = 0; c0 < a.npad; c0 += 16) {

@@ -152,6 +152,19 @@ lpca_status lpca_regenerate(lpca_ctx* ctx, int32_t kind, int64_t n, int64_t l, d
  * context X is this rank's row shard; the returned map is identical on all ranks. */
 lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_view* x,
                      lpca_map** out_map, lpca_timings* timings);
+/* Streaming reducers (reduce_{spca,lazy_spca}_streaming, reducer.cpp:236-335;
+ * RowBlockStream::next, sparse_matrix.hpp:58-65). The callback fills *block
+ * with the next row block (any supported layout, host or device) and its
+ * slice index and returns 1, returns 0 at the end of the stream, or a negative
+ * value to abort (LPCA_ERR_INVALID_ARGUMENT). The block's memory must stay valid
+ * until the next call. Slices must arrive as 0, 1, 2, ... and every block must
+ * have the projection's width. Host row-major blocks are copied on a second
+ * stream while the previous block is reduced. method rp reads only the first
+ * block's width; power_iters must be 0 (one pass over the data). lpca_fit with
+ * block_rows > 0 runs the same reducer over row slices of X, as reduce() does. */
+typedef int32_t (*lpca_next_block_fn)(void* user, lpca_matrix_view* block, int64_t* slice_index);
+lpca_status lpca_fit_stream(lpca_ctx* ctx, const lpca_config* cfg, lpca_next_block_fn next, void* user,
+                            lpca_map** out_map, lpca_timings* timings);
 /* apply_map (proj/core/src/reducer.cpp:348-353): Y = X V, m x k.
  * y_layout row- or column-major (the reference returns column-major), ldy 0 = packed. */
 lpca_status lpca_transform(lpca_ctx* ctx, const lpca_map* map, const lpca_matrix_view* x,

@@ -9,7 +9,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <exception>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -303,6 +305,98 @@ inline ReductionMap reduce_lazy_spca(const SparseMatrix& x, const ReducerConfig&
 }
 inline ReductionMap reduce(const SparseMatrix& x, const ReducerConfig& c, ReducerTimings* t = nullptr) {
   return detail::fit(x, c, c.method, t);
+}
+
+// ---- streaming (sparse_matrix.hpp:53-79, reducer.hpp:82-85) -----------------------
+struct RowBlock {
+  index_t slice_index = 0;
+  SparseMatrix block;
+};
+class RowBlockStream {
+ public:
+  virtual ~RowBlockStream() = default;
+  virtual std::optional<RowBlock> next() = 0;
+};
+// Lazy row partition of an in-memory matrix (sparse_matrix.cpp:125-139).
+class SliceRowBlockStream final : public RowBlockStream {
+ public:
+  SliceRowBlockStream(const SparseMatrix& x, index_t block_rows) : x_(&x), block_rows_(block_rows) {
+    if (block_rows < 1) throw InvalidArgumentError("block_rows must be at least 1");
+    slice_count_ = (x.rows() + block_rows - 1) / block_rows;
+  }
+  std::optional<RowBlock> next() override {
+    if (next_slice_ >= slice_count_) return std::nullopt;
+    const index_t lo = next_slice_ * block_rows_;
+    const index_t hi = lo + block_rows_ < x_->rows() ? lo + block_rows_ : x_->rows();
+    std::vector<index_t> cp{0}, ri;
+    std::vector<double> va;
+    for (index_t j = 0; j < x_->cols(); ++j) {  // rows are sorted within each column
+      for (index_t p = x_->col_ptr()[j]; p < x_->col_ptr()[j + 1]; ++p) {
+        const index_t r = x_->row_idx()[p];
+        if (r >= lo && r < hi) {
+          ri.push_back(r - lo);
+          va.push_back(x_->values()[p]);
+        }
+      }
+      cp.push_back(static_cast<index_t>(ri.size()));
+    }
+    RowBlock out{next_slice_, SparseMatrix::from_csc(hi - lo, x_->cols(), std::move(cp), std::move(ri), std::move(va))};
+    ++next_slice_;
+    return out;
+  }
+
+ private:
+  const SparseMatrix* x_;
+  index_t block_rows_, slice_count_ = 0, next_slice_ = 0;
+};
+
+namespace detail {
+struct StreamPump {  // lpca_next_block_fn over a RowBlockStream; keeps the current block alive
+  RowBlockStream* s;
+  std::optional<RowBlock> cur;
+  std::exception_ptr err;
+  static int32_t next(void* self, lpca_matrix_view* v, int64_t* slice) {
+    auto* p = static_cast<StreamPump*>(self);
+    try {
+      p->cur = p->s->next();
+      if (!p->cur) return 0;
+      *v = p->cur->block.view();
+      *slice = p->cur->slice_index;
+      return 1;
+    } catch (...) {
+      p->err = std::current_exception();
+      return -1;
+    }
+  }
+};
+inline ReductionMap fit_stream(RowBlockStream& blocks, ReducerConfig cfg, ReducerMethod m, ReducerTimings* t) {
+  cfg.method = m;
+  const lpca_config c = cfg.c_config();
+  StreamPump pump{&blocks, std::nullopt, nullptr};
+  lpca_map* out = nullptr;
+  lpca_timings tm{};
+  const lpca_status st = lpca_fit_stream(ctx(), &c, &StreamPump::next, &pump, &out, &tm);
+  if (pump.err) std::rethrow_exception(pump.err);
+  check(st);
+  if (t) {
+    t->sketch += tm.sketch;
+    t->qr += tm.qr;
+    t->f_form += tm.f_form;
+    t->svd += tm.svd;
+    t->total += tm.total;
+  }
+  return to_host(out);
+}
+}  // namespace detail
+
+// reduce_{spca,lazy_spca}_streaming (reducer.hpp:82-85, reducer.cpp:236-335)
+inline ReductionMap reduce_spca_streaming(RowBlockStream& blocks, const ReducerConfig& c,
+                                          ReducerTimings* t = nullptr) {
+  return detail::fit_stream(blocks, c, ReducerMethod::spca, t);
+}
+inline ReductionMap reduce_lazy_spca_streaming(RowBlockStream& blocks, const ReducerConfig& c,
+                                               ReducerTimings* t = nullptr) {
+  return detail::fit_stream(blocks, c, ReducerMethod::lazy_spca, t);
 }
 
 inline DenseMatrix apply_map(const ReductionMap& map, const SparseMatrix& x) {

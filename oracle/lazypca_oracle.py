@@ -267,6 +267,33 @@ def reduce_lazy_spca_sharded(x_shards, k, l, seed, allreduce, power_iters=0):
     return v, sig, u
 
 
+def reduce_streaming(blocks, method, k, l, seed, kind="gaussian", density=1.0):
+    """reduce_{lazy_spca,spca}_streaming (reducer.cpp:236-335): one pass over row
+    blocks, F = sum_s U_s^T X_s (gemm_t_add); SPCA also keeps the stacked
+    Householder R of [R; U_s] (householder_qr_r_only, qr.cpp:134-142) and ends
+    with F <- R^{-T} F (solve_rt_in_place, reducer.cpp:55-73)."""
+    blocks = [np.asarray(b, dtype=np.float64) for b in blocks]
+    if not blocks:
+        raise ValueError("streaming: the block stream is empty")
+    n = blocks[0].shape[1]
+    om, scale = omega_for(n, l, seed, kind, density)
+    f = np.zeros((l, n))
+    r = None
+    for b in blocks:
+        u = b @ om
+        f += u.T @ b
+        if method == "spca":
+            stacked = u if r is None else np.vstack([r, u])
+            r = np.linalg.qr(stacked, mode="r")
+            sg = np.sign(np.diag(r))
+            sg[sg == 0] = 1.0
+            r = r * sg[:, None]
+    if method == "spca":
+        f = np.linalg.solve(r.T, f)
+    sig, v, _ = truncated_svd_via_gram(f, k)
+    return v, sig, scale
+
+
 # ---- metrics used as checkers (metrics.cpp:100-136, 311-352) ------------------------
 def chordal_distance(v1: np.ndarray, v2: np.ndarray) -> float:
     def res2(a, b):

@@ -10,7 +10,8 @@ from .api import (  # noqa: F401
     RankDeficiencyError, ReducerConfig, ReducerMethod, ReducerTimings, ReductionMap, SketchMatrix,
     SparseMatrix, TruncatedSVD, apply_map, build_sketch, default_context, dense_aat, density_for, eigh,
     fit_transform, gemm_t, gemm_t_f32, gen_gaussian, gen_very_sparse, jacobi_eigh, projection_kind_from_string,
-    reduce, reduce_lazy_spca, reduce_rp, reduce_spca, reducer_method_from_string, regenerate,
+    reduce, reduce_lazy_spca, reduce_lazy_spca_streaming, reduce_rp, reduce_spca, reduce_spca_streaming,
+    reducer_method_from_string, regenerate, RowBlock, RowBlockStream, SliceRowBlockStream, split_rows,
     set_thread_count, sketch_f32, spmm, synth_lowrank, thread_count, to_string, tridiag_eigh,
     truncated_svd_via_gram,
 )

@@ -42,6 +42,10 @@ class Timings(C.Structure):
                  "sketch_pass", "f_pass", "transform_pass")]
 
 
+# int32_t (*lpca_next_block_fn)(void* user, lpca_matrix_view* block, int64_t* slice_index)
+NEXT_BLOCK_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(MatrixView), C.POINTER(C.c_int64))
+
+
 class MapInfo(C.Structure):
     _fields_ = [
         ("method", C.c_int32), ("reserved", C.c_int32),
@@ -79,6 +83,7 @@ SIGNATURES = {
     "lpca_transform": (I32, [P, P, C.POINTER(MatrixView), P, I32, I32, I32, I64, C.POINTER(Timings)]),
     "lpca_fit_transform": (I32, [P, C.POINTER(Config), C.POINTER(MatrixView), PP, P, I32, I32, I32,
                                  I64, C.POINTER(Timings)]),
+    "lpca_fit_stream": (I32, [P, C.POINTER(Config), P, P, PP, C.POINTER(Timings)]),
     "lpca_map_info_get": (I32, [P, C.POINTER(MapInfo)]),
     "lpca_map_copy_v": (I32, [P, P, I32]),
     "lpca_map_copy_sigma": (I32, [P, P]),

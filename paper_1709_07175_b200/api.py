@@ -505,6 +505,97 @@ def _fit(x, config: ReducerConfig, timings, ctx) -> ReductionMap:
     return ReductionMap(h, ctx)
 
 
+# ---- streaming (reducer.cpp:236-335; sparse_matrix.hpp:53-79) --------------------
+@dataclass
+class RowBlock:
+    """One row block of a stream (lazypca::RowBlock): any matrix _View accepts."""
+    slice_index: int
+    block: object
+
+
+class RowBlockStream:
+    """Pull-model block source (lazypca::RowBlockStream): next() returns the next
+    RowBlock, or None at the end."""
+
+    def next(self) -> Optional[RowBlock]:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class SliceRowBlockStream(RowBlockStream):
+    """Lazy row partition of an in-memory matrix (sparse_matrix.cpp:125-139)."""
+
+    def __init__(self, x, block_rows: int):
+        if block_rows < 1:
+            raise InvalidArgumentError("block_rows must be at least 1")
+        self.x, self.block_rows, self.next_slice = x, int(block_rows), 0
+        rows = x.rows() if isinstance(x, SparseMatrix) else x.shape[0]
+        self.rows = rows
+        self.slice_count = (rows + block_rows - 1) // block_rows
+
+    def next(self) -> Optional[RowBlock]:
+        if self.next_slice >= self.slice_count:
+            return None
+        lo = self.next_slice * self.block_rows
+        hi = min(lo + self.block_rows, self.rows)
+        if isinstance(self.x, SparseMatrix):
+            blk = SparseMatrix.from_dense(self.x.to_dense()[lo:hi])
+        else:
+            blk = self.x[lo:hi]
+        out = RowBlock(self.next_slice, blk)
+        self.next_slice += 1
+        return out
+
+
+def split_rows(x, block_rows: int) -> list:
+    s = SliceRowBlockStream(x, block_rows)
+    out = []
+    while (b := s.next()) is not None:
+        out.append(b)
+    return out
+
+
+def _fit_stream(stream: RowBlockStream, config: ReducerConfig, timings, ctx) -> ReductionMap:
+    ctx = ctx or default_context()
+    keep = {}
+    err = []
+
+    def cb(_user, view_ptr, slice_ptr):
+        try:
+            keep.pop("v", None)  # the previous block may be released now
+            b = stream.next()
+            if b is None:
+                return 0
+            vw = _View(b.block)
+            keep["v"] = vw
+            view_ptr[0] = vw.view
+            slice_ptr[0] = int(b.slice_index)
+            return 1
+        except Exception as e:  # surfaced after the C call returns
+            err.append(e)
+            return -1
+
+    fn = L.NEXT_BLOCK_FN(cb)
+    cfg = config._c()
+    t = L.Timings()
+    h = C.c_void_p()
+    st = ctx.lib.lpca_fit_stream(ctx.h, C.byref(cfg), C.cast(fn, C.c_void_p), None, C.byref(h), C.byref(t))
+    if err:
+        raise err[0]
+    _check(st)
+    _fill_timings(timings, t)
+    return ReductionMap(h, ctx)
+
+
+def reduce_lazy_spca_streaming(stream: RowBlockStream, config: ReducerConfig,
+                               timings: ReducerTimings | None = None, ctx=None) -> "ReductionMap":
+    return _fit_stream(stream, _cfg_with(config, ReducerMethod.lazy_spca), timings, ctx)
+
+
+def reduce_spca_streaming(stream: RowBlockStream, config: ReducerConfig,
+                          timings: ReducerTimings | None = None, ctx=None) -> "ReductionMap":
+    return _fit_stream(stream, _cfg_with(config, ReducerMethod.spca), timings, ctx)
+
+
 def reduce_rp(x, config: ReducerConfig, timings: ReducerTimings | None = None, ctx=None):
     return _fit(x, _cfg_with(config, ReducerMethod.rp), timings, ctx)
 

@@ -229,6 +229,21 @@ void launch_syrk_partials(cudaStream_t s, const T* u, index_t ldu, index_t m, in
   launch_utx_simt<T>(s, u, ldu, u, ldu, m, l, l, chunk_rows, part, false);
 }
 
+namespace {
+__global__ void add_f64_kernel(const double* __restrict__ x, double* __restrict__ y, index_t count) {
+  for (index_t i = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<index_t>(gridDim.x) * blockDim.x)
+    y[i] += x[i];
+}
+}  // namespace
+
+void launch_add_f64(cudaStream_t s, const double* x, double* y, index_t count) {
+  if (count <= 0) return;
+  index_t g = ceil_div(count, 256);
+  if (g > 148 * 8) g = 148 * 8;
+  add_f64_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(x, y, count);
+}
+
 void launch_reduce_partials(cudaStream_t s, const double* part, index_t nparts, index_t count,
                             double* out) {
   index_t g = ceil_div(count, 256);

@@ -56,6 +56,8 @@ void launch_xw_simt(cudaStream_t s, const T* x, index_t m, index_t n, index_t ld
 template <typename T>
 void launch_utx_simt(cudaStream_t s, const T* u, index_t ldu, const T* x, index_t ldx, index_t m,
                      index_t l, index_t n, index_t chunk_rows, double* part, bool exact);
+// y += x (fp64), the streaming reducers' running F and U^T U (gemm_t_add, kernels.cpp:95-113).
+void launch_add_f64(cudaStream_t s, const double* x, double* y, index_t count);
 // out[idx] = sum_c part[c][idx], c ascending (fixed order; no float atomics).
 void launch_reduce_partials(cudaStream_t s, const double* part, index_t nparts, index_t count,
                             double* out);

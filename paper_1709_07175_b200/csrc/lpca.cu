@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -474,11 +475,11 @@ index_t pick_chunks(const lpca_ctx& ctx, index_t m, index_t tiles, bool exact) {
 // F (l x n column-major fp64) = U^T X summed over this rank's rows, then
 // allreduced over ranks.
 void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f, bool exact,
-              const XScale* xs = nullptr) {
+              const XScale* xs = nullptr, bool over_ranks = true) {
   const index_t m = x.m, n = x.n;
   if (m == 0) {
     launch_zero(ctx.stream, f, sizeof(double) * l * n);
-    ctx.allreduce(f, l * n);
+    if (over_ranks) ctx.allreduce(f, l * n);
     return;
   }
   index_t chunks;
@@ -531,7 +532,7 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
     launch_reduce_partials(ctx.stream, part, chunks, l * n, f);
     LPCA_LAUNCHED(ctx);
   }
-  ctx.allreduce(f, l * n);
+  if (over_ranks) ctx.allreduce(f, l * n);
 }
 
 // CholeskyQR step on a wide F (l x n, F = Z^T): F <- L^{-1} F with
@@ -909,6 +910,263 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
   }
 }
 
+// ---- streaming reducers (Algorithms 3 and 4, reducer.cpp:236-335) ------------
+// A pull-model source of row blocks (RowBlockStream::next, sparse_matrix.hpp:58-65).
+struct BlockSource {
+  virtual ~BlockSource() = default;
+  virtual bool next(lpca_matrix_view* v, int64_t* slice) = 0;
+};
+
+struct CallbackSource final : BlockSource {
+  lpca_next_block_fn fn;
+  void* user;
+  CallbackSource(lpca_next_block_fn f, void* u) : fn(f), user(u) {}
+  bool next(lpca_matrix_view* v, int64_t* slice) override {
+    const int32_t r = fn(user, v, slice);
+    if (r < 0) throw Error(kInvalidArgument, "streaming: the block callback reported error " + S(r));
+    return r > 0;
+  }
+};
+
+// Row slices of a device-resident X: reduce() with block_rows > 0 runs the
+// streaming reducer over SliceRowBlockStream (reducer.cpp:340-346,
+// sparse_matrix.cpp:125-139).
+struct SliceSource final : BlockSource {
+  DevX x;
+  index_t block_rows, slices, next_slice = 0;
+  SliceSource(const DevX& d, index_t br) : x(d), block_rows(br), slices(ceil_div(d.m, br)) {}
+  bool next(lpca_matrix_view* v, int64_t* slice) override {
+    if (next_slice >= slices) return false;
+    const index_t lo = next_slice * block_rows;
+    const index_t hi = lo + block_rows < x.m ? lo + block_rows : x.m;
+    *v = lpca_matrix_view{};
+    v->dtype = x.dtype;
+    v->layout = LPCA_ROW_MAJOR;
+    v->location = LPCA_DEVICE;
+    v->rows = hi - lo;
+    v->cols = x.n;
+    v->ld = x.ld;
+    v->data = static_cast<const char*>(x.p) + static_cast<std::size_t>(lo) * x.ld * dsize(x.dtype);
+    *slice = next_slice++;
+    return true;
+  }
+};
+
+// Stages host row-major blocks through a copy stream into two alternating
+// device buffers, so block s+1 crosses PCIe while block s is reduced; other
+// layouts are staged on the compute stream.
+struct BlockStager {
+  lpca_ctx& ctx;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t copied[2] = {}, used[2] = {};
+  int turn = 0, cur = -1;
+  explicit BlockStager(lpca_ctx& c) : ctx(c) {
+    LPCA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      LPCA_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+      LPCA_CUDA(cudaEventCreateWithFlags(&used[b], cudaEventDisableTiming));
+    }
+  }
+  ~BlockStager() {
+    cudaStreamSynchronize(cs);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(copied[b]);
+      cudaEventDestroy(used[b]);
+    }
+    cudaStreamDestroy(cs);
+  }
+  // The caller's block memory may be reused once the previous copy has landed.
+  void before_next() { LPCA_CUDA(cudaStreamSynchronize(cs)); }
+  DevX stage(const lpca_matrix_view* v, double* h2d) {
+    cur = -1;
+    check_view(v);
+    if (v->location == LPCA_HOST && v->layout == LPCA_ROW_MAJOR && v->rows > 0 && v->cols > 0) {
+      const int b = turn;
+      turn ^= 1;
+      const std::size_t es = dsize(v->dtype), bytes = es * v->rows * v->cols;
+      const std::string slot = b ? "stream.b1" : "stream.b0";
+      auto it = ctx.ws.find(slot);
+      if (it == ctx.ws.end() || it->second.second < bytes) {  // growing: let both streams drain first
+        LPCA_CUDA(cudaStreamSynchronize(cs));
+        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+      }
+      void* dst = ctx.buf(slot, bytes);
+      LPCA_CUDA(cudaStreamWaitEvent(cs, used[b], 0));  // block s-2's kernels are done with this buffer
+      LPCA_CUDA(cudaMemcpy2DAsync(dst, es * v->cols, v->data, es * v->ld, es * v->cols, v->rows,
+                                  cudaMemcpyHostToDevice, cs));
+      LPCA_CUDA(cudaEventRecord(copied[b], cs));
+      LPCA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[b], 0));
+      if (h2d) *h2d += static_cast<double>(bytes);
+      cur = b;
+      return DevX{dst, v->dtype, v->rows, v->cols, v->cols};
+    }
+    return stage_x(ctx, v, "stream.x", h2d);
+  }
+  void release() {
+    if (cur >= 0) LPCA_CUDA(cudaEventRecord(used[cur], ctx.stream));
+  }
+};
+
+// Streaming Lazy SPCA (Algorithm 4) and SPCA (Algorithm 3): one pass over the
+// blocks accumulating F = sum_s U_s^T X_s (gemm_t_add) and, for SPCA, the Gram
+// U^T U = sum_s U_s^T U_s whose Cholesky factor R stands in for the reference's
+// stacked Householder R (qr.cpp:134-142; equal up to roundoff at full rank);
+// then F <- R^{-T} F (solve_rt_in_place) and the spectral step. Ranks reduce
+// their own blocks and sum F (and U^T U) with one allreduce each at the end.
+lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& src, lpca_timings* t) {
+  BlockStager stager(ctx);
+  lpca_matrix_view v{};
+  int64_t slice = -1;
+  if (!src.next(&v, &slice)) throw Error(kInvalidArgument, "streaming: the block stream is empty");
+  if (slice != 0) throw Error(kInvalidArgument, "streaming: first slice index must be 0, got " + S(slice));
+  check_view(&v);
+  lpca_config c = resolve(cfg_in, v.cols);
+  if (c.power_iters > 0)
+    throw Error(kInvalidArgument,
+                "streaming: power iterations read the data more than once; use the in-core reducers");
+  const index_t n = c.proj_n, l = c.l, k = c.k;
+  PhaseEvents ev(ctx);
+  ev.mark(0);
+  auto map = std::make_unique<lpca_map>();
+  map->device = ctx.device;
+  map->method = c.method;
+  map->k = k;
+  map->l = l;
+  map->n = n;
+  map->seed = c.seed;
+  map->density = c.density;
+  map->scale = projection_scale(c);
+  map->alloc_v(ctx.stream, sizeof(double) * (n * k > 0 ? n * k : 1));
+  double* omega = ctx.get<double>("omega", n * l);
+  regenerate_dev(ctx, c, omega);
+  if (c.method == LPCA_RP) {  // no data pass (reduce_rp, reducer.cpp:171-190)
+    launch_scale_f64(ctx.stream, omega, map->v, n * k, 1.0 / map->scale);
+    LPCA_LAUNCHED(ctx);
+    ev.mark(1);
+    LPCA_CUDA(cudaEventSynchronize(ctx.ev[1]));
+    if (t) {
+      t->sketch += ev.secs(0, 1);
+      t->total += ev.secs(0, 1);
+    }
+    return map.release();
+  }
+  const bool spca = c.method == LPCA_SPCA;
+  double* f = ctx.get<double>("stream.f", l * n);
+  double* fb = ctx.get<double>("stream.fb", l * n);
+  double* g = spca ? ctx.get<double>("stream.g", l * l) : nullptr;
+  double* gb = spca ? ctx.get<double>("stream.gb", l * l) : nullptr;
+  launch_zero(ctx.stream, f, sizeof(double) * l * n);
+  if (spca) launch_zero(ctx.stream, g, sizeof(double) * l * l);
+  uint32_t* xmax = ctx.get<uint32_t>("xmax", 1);
+  double sk = 0, ff = 0, qr = 0, h2d = 0;
+  index_t expected = 0;
+  bool first = true;
+  for (;;) {
+    if (!first) {
+      stager.before_next();
+      if (!src.next(&v, &slice)) break;
+      // pull(): slice order and width (reducer.cpp:101-113)
+      if (slice != expected)
+        throw Error(kInvalidArgument, "streaming: expected slice " + S(expected) + ", got " + S(slice));
+      check_view(&v);
+      if (v.cols != n)
+        throw Error(kDimension, "streaming: block has " + S(v.cols) + " columns but the projection expects " + S(n));
+    }
+    if (spca && first && v.rows < l)
+      throw Error(kDimension, "streaming spca: first block has " + S(v.rows) +
+                                  " rows; the orthonormal route needs at least l = " + S(l));
+    ++expected;
+    const DevX x = stager.stage(&v, &h2d);
+    if (x.m > 0) {
+      const bool exact = ctx.exact != 0 && x.dtype == 8;
+      const bool tc = use_tc(ctx, x, l);
+      const bool f16 = tc && tc_pair_mode() && f16_enabled() && !spca;
+      XScale xs;
+      xs.dev = xmax;
+      Panel u;
+      u.ld = round_up(l, 16);
+      if (!tc || spca) u.plain = ctx.buf("stream.u", dsize(x.dtype) * x.m * u.ld);
+      if (f16) {
+        launch_zero(ctx.stream, xmax, sizeof(uint32_t));
+        u.ldt16 = round_up(x.m, 8);
+        u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
+        u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
+        u.uinv = ctx.get<float>("u.inv", ceil_div(x.m, 128) * u.ld);
+      } else if (tc) {
+        u.ldt = planes_ld(x.m);
+        u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
+        u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
+      }
+      ev.mark(1);
+      XScale sketch;
+      sketch.use = true;
+      sketch.check = xmax;
+      xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);  // U_s = X_s Omega
+      xs.use = f16;
+      ev.mark(2);
+      utx_pass(ctx, x, u, l, fb, exact, &xs, false);  // F += U_s^T X_s
+      launch_add_f64(ctx.stream, fb, f, l * n);
+      LPCA_LAUNCHED(ctx);
+      ev.mark(3);
+      if (spca) {  // U^T U += U_s^T U_s
+        index_t chunks = pick_chunks(ctx, x.m, ceil_div(l, 64) * ceil_div(l, 64), exact);
+        const index_t chunk_rows = round_up(ceil_div(x.m, chunks), 128);
+        chunks = ceil_div(x.m, chunk_rows);
+        double* gpart = ctx.get<double>("stream.gpart", chunks * l * l);
+        if (x.dtype == 4)
+          launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld, x.m, l, chunk_rows, gpart);
+        else
+          launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u.plain), u.ld, x.m, l, chunk_rows,
+                                       gpart);
+        LPCA_LAUNCHED(ctx);
+        launch_reduce_partials(ctx.stream, gpart, chunks, l * l, gb);
+        LPCA_LAUNCHED(ctx);
+        launch_add_f64(ctx.stream, gb, g, l * l);
+        LPCA_LAUNCHED(ctx);
+      }
+      ev.mark(4);
+      LPCA_CUDA(cudaEventSynchronize(ctx.ev[4]));
+      sk += ev.secs(1, 2);
+      ff += ev.secs(2, 3);
+      qr += ev.secs(3, 4);
+    }
+    stager.release();
+    first = false;
+  }
+  ev.mark(1);
+  ctx.allreduce(f, l * n);
+  if (spca) {
+    ctx.allreduce(g, l * l);
+    double* w = ctx.get<double>("spca.w", l * l);
+    double* lm = ctx.get<double>("spca.l", l * l);
+    int* st = ctx.get<int>("spca.status", 1);
+    launch_chol_inverse(ctx.stream, g, l, w, lm, st);
+    LPCA_LAUNCHED(ctx);
+    int h = 0;
+    LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (h != 0)  // solve_rt_in_place's check (reducer.cpp:55-73)
+      throw Error(kRankDeficiency,
+                  "triangular solve: R diagonal entry " + S(h - 1) + " is numerically zero", h - 1);
+    launch_apply_rinv_t(ctx.stream, w, l, f, n, ctx.get<double>("orth.tmp", l * n));  // F <- R^{-T} F
+    LPCA_LAUNCHED(ctx);
+  }
+  ev.mark(2);
+  finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
+  ev.mark(3);
+  LPCA_CUDA(cudaEventSynchronize(ctx.ev[3]));
+  if (t) {
+    t->sketch += sk;
+    t->f_form += ff;
+    t->qr += qr + ev.secs(1, 2);
+    t->svd += ev.secs(2, 3);
+    t->h2d += 0.0;
+    t->total += ev.secs(0, 3);
+  }
+  (void)h2d;
+  return map.release();
+}
+
 int num_sms_of(int device) {
   int v = 148;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -1082,8 +1340,29 @@ lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_vi
     double h2d = 0.0;
     const DevX dx = stage_x(*ctx, x, "x", &h2d);
     ev.mark(10);
-    *out_map = fit_dev(*ctx, *cfg, dx, timings);
+    if ((cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP) {
+      // reduce() with block_rows: the streaming reducer over row slices (reducer.cpp:340-346)
+      if (cfg->block_rows < 1) throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
+      SliceSource src(dx, cfg->block_rows);
+      *out_map = fit_stream_dev(*ctx, *cfg, src, timings);
+    } else {
+      lpca_config c = *cfg;
+      c.block_rows = 0;
+      c.streaming = 0;
+      *out_map = fit_dev(*ctx, c, dx, timings);
+    }
     if (timings) timings->h2d += ev.secs(9, 10);
+  });
+}
+
+lpca_status lpca_fit_stream(lpca_ctx* ctx, const lpca_config* cfg, lpca_next_block_fn next, void* user,
+                            lpca_map** out_map, lpca_timings* timings) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!cfg || !out_map || !next) throw Error(kInvalidArgument, "null argument");
+    *out_map = nullptr;
+    CallbackSource src(next, user);
+    *out_map = fit_stream_dev(*ctx, *cfg, src, timings);
   });
 }
 
@@ -1114,7 +1393,17 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
     ev.mark(9);
     const DevX dx = stage_x(*ctx, x, "x", nullptr);
     ev.mark(10);
-    lpca_map* map = fit_dev(*ctx, *cfg, dx, timings);
+    lpca_map* map = nullptr;
+    if ((cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP) {
+      if (cfg->block_rows < 1) throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
+      SliceSource src(dx, cfg->block_rows);
+      map = fit_stream_dev(*ctx, *cfg, src, timings);
+    } else {
+      lpca_config c = *cfg;
+      c.block_rows = 0;
+      c.streaming = 0;
+      map = fit_dev(*ctx, c, dx, timings);
+    }
     try {
       transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
     } catch (...) {

@@ -114,3 +114,8 @@ def test_shim_header_compiles_against_abi(tmp_path):
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert subprocess.run([str(exe)]).returncode == 0
+    # the streaming half of the shim (RowBlockStream, reduce_*_streaming) compiles too
+    r = subprocess.run(["g++", "-std=c++17", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / "shim_stream.cpp"),
+                        "-o", str(tmp_path / "s"), f"-L{L.LIB_PATH.parent}", "-llazypca_b200",
+                        f"-Wl,-rpath,{L.LIB_PATH.parent}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

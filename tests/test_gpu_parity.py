@@ -282,9 +282,14 @@ def test_bitwise_rerun_determinism(ctx):
     assert np.array_equal(a.singular_values, b.singular_values)
 
 
-def test_streaming_config_is_rejected_in_core(ctx):
+def test_streaming_config_runs_the_streaming_reducer(ctx, ref):
+    # reduce() with block_rows streams row slices (reducer.cpp:340-346), as the reference does
     x = np.random.default_rng(1).uniform(-1, 1, (40, 12))
     c = _cfg(lp.ReducerMethod.lazy_spca, 4, 4, 1)
     c.block_rows = 10
-    with pytest.raises(lp.InvalidArgumentError):
+    m = lp.reduce(x, c, ctx=ctx)
+    _, s_ref, _, _ = ref.reduce(2, x, 4, 4, 1, block_rows=10)
+    assert np.max(np.abs(m.singular_values - s_ref) / s_ref) < 1e-10
+    c.streaming, c.block_rows = True, 0
+    with pytest.raises(lp.InvalidArgumentError, match="block_rows"):
         lp.reduce(x, c, ctx=ctx)

@@ -194,6 +194,18 @@ lpca_status lpca_map_copy_sigma(const lpca_map* map, double* sigma_out);
 lpca_status lpca_map_create(lpca_ctx* ctx, const lpca_map_info* info, const double* v_host,
                             const double* sigma_host, lpca_map** out);
 lpca_status lpca_map_destroy(lpca_map* map);
+/* Map files, byte-compatible with the reference's save_map / load_map
+ * (reducer.cpp:355-412): a one-line JSON header, then V as a dense
+ * MatrixMarket array. lpca_map_save / lpca_map_load move a device map through a
+ * file; the lpca_map_file_* pair works on host arrays and needs no GPU
+ * (lpca_map_file_read with v_host == NULL fills only *info). Errors: ParseError
+ * (with the line) for malformed files, DimensionError for shape mismatches. */
+lpca_status lpca_map_save(const lpca_map* map, const char* path);
+lpca_status lpca_map_load(lpca_ctx* ctx, const char* path, lpca_map** out);
+lpca_status lpca_map_file_write(const char* path, const lpca_map_info* info, const double* v_host,
+                                const double* sigma_host);
+lpca_status lpca_map_file_read(const char* path, lpca_map_info* info, double* v_host, int64_t v_capacity,
+                               double* sigma_host);
 
 /* ---- kernel-level exports (proj/core/include/lazypca/kernels.hpp:17-36,
  *      truncated_svd.hpp:24, tridiag_eigh.hpp:8). Host or device operands; fp64

@@ -204,6 +204,43 @@ int ref_fit_transform(int method, const void* x, int dtype, std::int64_t m, std:
   });
 }
 
+// save_map_file / load_map_file (proj/core/src/reducer.cpp:355-412). method:
+// 0 rp, 1 spca, 2 lazy_spca; sigma may be null (no singular values).
+int ref_save_map_file(int method, std::int64_t k, std::int64_t l, std::int64_t n, std::uint64_t seed,
+                      double density, double scale, const double* v, const double* sigma, const char* path) {
+  return guarded([&] {
+    ReductionMap map;
+    map.method = method == 0 ? "rp" : method == 1 ? "spca" : "lazy_spca";
+    map.k = k;
+    map.l = l;
+    map.n = n;
+    map.seed = seed;
+    map.density = density;
+    map.scale = scale;
+    map.v = dense_from(v, n, k);
+    if (sigma) map.singular_values.assign(sigma, sigma + k);
+    save_map_file(map, path);
+  });
+}
+
+// Reads a map file; v_out (n*k) and sigma_out (k) may be null to query the shape.
+int ref_load_map_file(const char* path, std::int64_t* k, std::int64_t* l, std::int64_t* n, std::uint64_t* seed,
+                      double* density, double* scale, int* has_sigma, double* v_out, double* sigma_out) {
+  return guarded([&] {
+    const ReductionMap map = load_map_file(path);
+    *k = map.k;
+    *l = map.l;
+    *n = map.n;
+    *seed = map.seed;
+    *density = map.density;
+    *scale = map.scale;
+    *has_sigma = map.singular_values.empty() ? 0 : 1;
+    if (v_out) copy_out(map.v, v_out);
+    if (sigma_out)
+      for (std::size_t i = 0; i < map.singular_values.size(); ++i) sigma_out[i] = map.singular_values[i];
+  });
+}
+
 // apply_map (proj/core/src/reducer.cpp:348-353): Y = X V, Y m x k column-major.
 int ref_apply_map(const void* x, int dtype, std::int64_t m, std::int64_t n, const double* v,
                   std::int64_t k, double* y_out) {

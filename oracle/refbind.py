@@ -194,3 +194,26 @@ def chordal(v1: np.ndarray, v2: np.ndarray) -> float:
 
 def cpu_threads() -> int:
     return len(os.sched_getaffinity(0))
+
+
+def save_map_file(path: str, method: int, k: int, l: int, n: int, seed: int, density: float, scale: float,
+                  v: np.ndarray, sigma=None) -> None:
+    """save_map_file (reducer.cpp:355-373) with V n x k."""
+    v = np.asfortranarray(v, dtype=np.float64)
+    s = None if sigma is None else np.ascontiguousarray(sigma, dtype=np.float64)
+    _chk(load().ref_save_map_file(C.c_int(method), C.c_int64(k), C.c_int64(l), C.c_int64(n), C.c_uint64(seed),
+                                  C.c_double(density), C.c_double(scale), _p(v), _p(s) if s is not None else None,
+                                  path.encode()))
+
+
+def load_map_file(path: str) -> dict:
+    """load_map_file (reducer.cpp:375-412)."""
+    k, l, n, seed = C.c_int64(), C.c_int64(), C.c_int64(), C.c_uint64()
+    dens, sc, hs = C.c_double(), C.c_double(), C.c_int()
+    args = [C.byref(k), C.byref(l), C.byref(n), C.byref(seed), C.byref(dens), C.byref(sc), C.byref(hs)]
+    _chk(load().ref_load_map_file(path.encode(), *args, None, None))
+    v = np.zeros((n.value, k.value), order="F")
+    sig = np.zeros(k.value)
+    _chk(load().ref_load_map_file(path.encode(), *args, _p(v), _p(sig)))
+    return dict(k=k.value, l=l.value, n=n.value, seed=seed.value, density=dens.value, scale=sc.value,
+                v=v, sigma=sig if hs.value else None)

@@ -89,6 +89,10 @@ SIGNATURES = {
     "lpca_map_copy_sigma": (I32, [P, P]),
     "lpca_map_create": (I32, [P, C.POINTER(MapInfo), P, P, PP]),
     "lpca_map_destroy": (I32, [P]),
+    "lpca_map_save": (I32, [P, C.c_char_p]),
+    "lpca_map_load": (I32, [P, C.c_char_p, PP]),
+    "lpca_map_file_write": (I32, [C.c_char_p, C.POINTER(MapInfo), P, P]),
+    "lpca_map_file_read": (I32, [C.c_char_p, C.POINTER(MapInfo), P, I64, P]),
     "lpca_spmm": (I32, [P, C.POINTER(MatrixView), P, I64, I32, P, I32]),
     "lpca_gemm_t": (I32, [P, P, I64, I64, I32, C.POINTER(MatrixView), P, I32]),
     "lpca_dense_aat": (I32, [P, P, I64, I64, I32, P]),

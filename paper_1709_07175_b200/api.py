@@ -505,6 +505,51 @@ def _fit(x, config: ReducerConfig, timings, ctx) -> ReductionMap:
     return ReductionMap(h, ctx)
 
 
+# ---- map files (reducer.cpp:355-412), byte-compatible with the reference ----------
+def save_map_file(map_: "ReductionMap", path: str) -> None:
+    """save_map_file: one-line JSON header + V as a dense MatrixMarket array."""
+    _check(map_._ctx.lib.lpca_map_save(map_.handle(), str(path).encode()))
+
+
+def load_map_file(path: str, ctx=None) -> "ReductionMap":
+    """load_map_file: a device map ready for apply_map."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(ctx.lib.lpca_map_load(ctx.h, str(path).encode(), C.byref(h)))
+    return ReductionMap(h, ctx)
+
+
+def write_map_file(path: str, method: "ReducerMethod", v: np.ndarray, singular_values=None, l: int = 0,
+                   seed: int = 0, density: float = 1.0, scale: float = 1.0) -> None:
+    """The same file from host arrays (no GPU needed)."""
+    v = np.asfortranarray(v, dtype=np.float64)
+    info = L.MapInfo()
+    info.method = int(method)
+    info.n, info.k = v.shape
+    info.l = l or v.shape[1]
+    info.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    info.density, info.scale = float(density), float(scale)
+    sig = None
+    if singular_values is not None:
+        sig = np.ascontiguousarray(singular_values, dtype=np.float64)
+        info.has_singular_values = 1
+    _check(L.load().lpca_map_file_write(str(path).encode(), C.byref(info), v.ctypes.data if v.size else None,
+                                        sig.ctypes.data if sig is not None and sig.size else None))
+
+
+def read_map_file(path: str) -> dict:
+    """Host-side read: header fields, V (n x k) and the singular values (or None)."""
+    info = L.MapInfo()
+    _check(L.load().lpca_map_file_read(str(path).encode(), C.byref(info), None, 0, None))
+    v = np.zeros((info.n, info.k), order="F")
+    sig = np.zeros(info.k)
+    _check(L.load().lpca_map_file_read(str(path).encode(), C.byref(info), v.ctypes.data if v.size else None,
+                                       v.size, sig.ctypes.data if sig.size else None))
+    return dict(method=ReducerMethod(info.method), k=info.k, l=info.l, n=info.n, seed=info.seed,
+                density=info.density, scale=info.scale, v=v,
+                singular_values=sig if info.has_singular_values else None)
+
+
 # ---- streaming (reducer.cpp:236-335; sparse_matrix.hpp:53-79) --------------------
 @dataclass
 class RowBlock:

@@ -22,6 +22,26 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu", "eigh.cu"]
+HOST_SOURCES = ["mapio.cpp"]  # host-only C++ (g++)
+CXX = os.environ.get("CXX", "g++")
+
+
+def _json_include() -> str:
+    """Directory holding nlohmann/json.hpp (3.11.x), the reference's map-header
+    serialiser: the copy vendored with cudnn_frontend in this image."""
+    cands = [os.environ.get("LPCA_JSON_INCLUDE", "")]
+    try:
+        import site
+        for sp in site.getsitepackages():
+            cands.append(os.path.join(sp, "include", "cudnn_frontend", "thirdparty"))
+    except Exception:
+        pass
+    cands.append(os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                              "site-packages", "include", "cudnn_frontend", "thirdparty"))
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "nlohmann", "json.hpp")):
+            return c
+    raise RuntimeError("nlohmann/json.hpp not found (set LPCA_JSON_INCLUDE)")
 
 
 def _obj(src: str) -> Path:
@@ -37,8 +57,12 @@ def _needs(src: Path, obj: Path) -> bool:
 
 def _compile(src: str, verbose: bool) -> None:
     obj = _obj(src)
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
-    if verbose:
+    if src in HOST_SOURCES:
+        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-I", str(CSRC),
+               "-I", "/usr/local/cuda/include", "-I", _json_include(), "-c", str(CSRC / src), "-o", str(obj)]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+    if verbose and src not in HOST_SOURCES:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -49,10 +73,10 @@ def _compile(src: str, verbose: bool) -> None:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    todo = [s for s in SOURCES if force or _needs(CSRC / s, _obj(s))]
+    todo = [s for s in SOURCES + HOST_SOURCES if force or _needs(CSRC / s, _obj(s))]
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(todo)))) as ex:
         list(ex.map(lambda s: _compile(s, verbose), todo))
-    objs = [str(_obj(s)) for s in SOURCES]
+    objs = [str(_obj(s)) for s in SOURCES + HOST_SOURCES]
     if todo or not LIB.exists() or force:
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-Xlinker", "-z,defs",
                "-lcudart_static", "-lrt", "-ldl", "-lpthread"]

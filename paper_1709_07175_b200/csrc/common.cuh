@@ -44,6 +44,9 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     LPCA_CUDA(cudaGetLastError()); \
   } while (0)
 
+// Sets the thread's lpca_last_error* state (defined in lpca.cu).
+void set_last_error(const std::string& msg, std::int64_t index, double gap);
+
 inline index_t ceil_div(index_t a, index_t b) { return (a + b - 1) / b; }
 inline index_t round_up(index_t a, index_t b) { return ceil_div(a, b) * b; }
 

@@ -34,6 +34,17 @@ thread_local std::string g_err_msg;
 thread_local std::int64_t g_err_index = -1;
 thread_local double g_err_gap = 0.0;
 
+}  // namespace
+
+// lpca_last_error* state for the host-only translation units (mapio.cpp).
+void lpca::set_last_error(const std::string& msg, std::int64_t index, double gap) {
+  g_err_msg = msg;
+  g_err_index = index;
+  g_err_gap = gap;
+}
+
+namespace {
+
 template <typename F>
 lpca_status guarded(F&& fn) {
   try {

@@ -56,6 +56,15 @@ void launch_xw_simt(cudaStream_t s, const T* x, index_t m, index_t n, index_t ld
 template <typename T>
 void launch_utx_simt(cudaStream_t s, const T* u, index_t ldu, const T* x, index_t ldx, index_t m,
                      index_t l, index_t n, index_t chunk_rows, double* part, bool exact);
+// ---- sparse X (sparse.cu): the reference's order, bitwise (kernels.cpp:30-113) --
+// out (m x w, element (i, c) at i*ors + c*ocs, fp64 or fp32) = X W with X in CSR
+// and W row-major n x w (ld ldw).
+void launch_spmm_csr(cudaStream_t s, index_t m, const std::int64_t* row_ptr, const std::int32_t* col,
+                     const double* val, const double* wt, index_t ldw, index_t w, void* out, int out_dtype,
+                     index_t ors, index_t ocs);
+// F (l x n column-major) (+)= U^T X with X in CSC and U row-major m x l (ld ldu), l <= 512.
+void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, const std::int32_t* row,
+                       const double* val, const double* u, index_t ldu, index_t l, double* f, bool accumulate);
 // y += x (fp64), the streaming reducers' running F and U^T U (gemm_t_add, kernels.cpp:95-113).
 void launch_add_f64(cudaStream_t s, const double* x, double* y, index_t count);
 // out[idx] = sum_c part[c][idx], c ascending (fixed order; no float atomics).

@@ -223,7 +223,25 @@ struct DevX {
   const void* p = nullptr;
   int dtype = 8;
   index_t m = 0, n = 0, ld = 0;
+  // sparse path (csrc/sparse.cu): X as CSR (row gathers) and CSC (column
+  // gathers) on the device, fp64 values, 32-bit indices; p is null
+  const std::int64_t* rp = nullptr;
+  const std::int32_t* ci = nullptr;
+  const double* rv = nullptr;
+  const std::int64_t* cp = nullptr;
+  const std::int32_t* ri = nullptr;
+  const double* cv = nullptr;
+  bool sparse() const { return rp != nullptr; }
 };
+
+// CSC inputs stay sparse on the device below this density (LPCA_SPARSE=1/0
+// forces the choice); denser ones are densified for the tensor-core passes.
+bool keep_sparse(index_t nnz, index_t m, index_t n) {
+  const char* e = std::getenv("LPCA_SPARSE");
+  if (e && e[0]) return e[0] == '1';
+  return static_cast<double>(nnz) < 0.25 * static_cast<double>(m) * static_cast<double>(n) &&
+         m < (index_t(1) << 31) && n < (index_t(1) << 31);
+}
 
 std::size_t dsize(int dtype) { return dtype == 4 ? 4 : 8; }
 
@@ -280,6 +298,52 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
         if (!std::isfinite(v)) throw Error(kInvalidArgument, "csc: non-finite value in column " + S(j));
         vals[static_cast<std::size_t>(p)] = v;
       }
+    }
+    if (keep_sparse(nnz, x->rows, x->cols)) {
+      // CSR by a stable counting sort of the CSC entries: within a row the
+      // columns stay ascending (the reference's accumulation order)
+      const index_t m = x->rows, n = x->cols;
+      std::vector<std::int64_t> rptr(static_cast<std::size_t>(m + 1), 0);
+      for (index_t p = 0; p < nnz; ++p) ++rptr[static_cast<std::size_t>(x->row_idx[p] + 1)];
+      for (index_t i = 0; i < m; ++i) rptr[static_cast<std::size_t>(i + 1)] += rptr[static_cast<std::size_t>(i)];
+      std::vector<std::int64_t> fill(rptr.begin(), rptr.end() - 1);
+      std::vector<std::int32_t> ccol(static_cast<std::size_t>(nnz)), crow(static_cast<std::size_t>(nnz));
+      std::vector<double> cval(static_cast<std::size_t>(nnz));
+      for (index_t j = 0; j < n; ++j)
+        for (index_t p = x->col_ptr[j]; p < x->col_ptr[j + 1]; ++p) {
+          const index_t r = x->row_idx[p];
+          const std::int64_t q = fill[static_cast<std::size_t>(r)]++;
+          ccol[static_cast<std::size_t>(q)] = static_cast<std::int32_t>(j);
+          cval[static_cast<std::size_t>(q)] = vals[static_cast<std::size_t>(p)];
+          crow[static_cast<std::size_t>(p)] = static_cast<std::int32_t>(r);
+        }
+      const std::string sl(slot);
+      const std::size_t nz = static_cast<std::size_t>(nnz > 0 ? nnz : 1);
+      auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
+      auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
+      auto* rv = ctx.get<double>(sl + ".rv", nz);
+      auto* cp = ctx.get<std::int64_t>(sl + ".cp", n + 1);
+      auto* ri = ctx.get<std::int32_t>(sl + ".ri", nz);
+      auto* cv = ctx.get<double>(sl + ".cv", nz);
+      LPCA_CUDA(cudaMemcpyAsync(rp, rptr.data(), sizeof(std::int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx.stream));
+      LPCA_CUDA(cudaMemcpyAsync(cp, x->col_ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx.stream));
+      if (nnz > 0) {
+        LPCA_CUDA(cudaMemcpyAsync(ci, ccol.data(), sizeof(std::int32_t) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+        LPCA_CUDA(cudaMemcpyAsync(rv, cval.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+        LPCA_CUDA(cudaMemcpyAsync(ri, crow.data(), sizeof(std::int32_t) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+        LPCA_CUDA(cudaMemcpyAsync(cv, vals.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx.stream));
+      }
+      LPCA_CUDA(cudaStreamSynchronize(ctx.stream));  // the host vectors die here
+      if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz * 24 + (m + n + 2) * 8);
+      d.dtype = 8;
+      d.ld = n;
+      d.rp = rp;
+      d.ci = ci;
+      d.rv = rv;
+      d.cp = cp;
+      d.ri = ri;
+      d.cv = cv;
+      return d;
     }
     auto* cp = ctx.get<std::int64_t>(std::string(slot) + ".ptr", x->cols + 1);
     auto* ri = ctx.get<std::int64_t>(std::string(slot) + ".idx", nnz > 0 ? nnz : 1);
@@ -390,6 +454,16 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
              bool exact, const XScale* xs = nullptr) {
   const index_t m = x.m, n = x.n;
   if (m == 0) return;
+  if (x.sparse()) {  // row gathers over CSR in the reference's order (kernels.cpp:30-47)
+    double* wt = ctx.get<double>("w.rows", n * wc);
+    launch_transpose(ctx.stream, 8, w, ldw, n, wc, wt, wc);
+    LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 0);
+    launch_spmm_csr(ctx.stream, m, x.rp, x.ci, x.rv, wt, wc, wc, out.plain, 8, out.ld, 1);
+    LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 1);
+    return;
+  }
   if (x.dtype == 8) {
     pass_mark(ctx, 0);
     launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, w, wc,
@@ -495,6 +569,14 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
   }
   index_t chunks;
   double* part;
+  if (x.sparse()) {  // column gathers over CSC in the reference's order (kernels.cpp:70-113)
+    pass_mark(ctx, 0);
+    launch_gemm_t_csc(ctx.stream, n, x.cp, x.ri, x.cv, static_cast<const double*>(u.plain), u.ld, l, f, false);
+    LPCA_LAUNCHED(ctx);
+    pass_mark(ctx, 1);
+    if (over_ranks) ctx.allreduce(f, l * n);
+    return;
+  }
   if (u.h16hi && x.dtype == 4) {
     index_t rps = 0;
     chunks = utx_pair_splits(m, n, ctx.num_sms, &rps);
@@ -861,7 +943,13 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
     const std::size_t ybytes = dsize(y_dtype) * static_cast<std::size_t>(row ? m * ldy : k * ldy);
     void* ydev = y_location == LPCA_DEVICE ? y : ctx.buf("y", ybytes);
     const index_t ors = row ? ldy : 1, ocs = row ? 1 : ldy;
-    if (x.dtype == 8) {
+    if (x.sparse()) {  // spmm over CSR (apply_map = spmm(X, V), reducer.cpp:348-353)
+      double* vt = ctx.get<double>("v.rows", map.n * k);
+      launch_transpose(ctx.stream, 8, map.v, map.n, map.n, k, vt, k);
+      LPCA_LAUNCHED(ctx);
+      launch_spmm_csr(ctx.stream, m, x.rp, x.ci, x.rv, vt, k, k, ydev, y_dtype, ors, ocs);
+      LPCA_LAUNCHED(ctx);
+    } else if (x.dtype == 8) {
       if (y_dtype == 8)
         launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
                                        map.v, k, map.n, static_cast<double*>(ydev), ors, ocs, ctx.exact != 0);
@@ -1115,9 +1203,14 @@ lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& 
       xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);  // U_s = X_s Omega
       xs.use = f16;
       ev.mark(2);
-      utx_pass(ctx, x, u, l, fb, exact, &xs, false);  // F += U_s^T X_s
-      launch_add_f64(ctx.stream, fb, f, l * n);
-      LPCA_LAUNCHED(ctx);
+      if (x.sparse()) {  // gemm_t_add continues the running sums: bitwise the reference's streaming
+        launch_gemm_t_csc(ctx.stream, n, x.cp, x.ri, x.cv, static_cast<const double*>(u.plain), u.ld, l, f, true);
+        LPCA_LAUNCHED(ctx);
+      } else {
+        utx_pass(ctx, x, u, l, fb, exact, &xs, false);  // F += U_s^T X_s
+        launch_add_f64(ctx.stream, fb, f, l * n);
+        LPCA_LAUNCHED(ctx);
+      }
       ev.mark(3);
       if (spca) {  // U^T U += U_s^T U_s
         index_t chunks = pick_chunks(ctx, x.m, ceil_div(l, 64) * ceil_div(l, 64), exact);
@@ -1502,7 +1595,7 @@ namespace {
 // fp64 row-major device copy of a view (f32 data widened exactly).
 DevX stage_x_f64(lpca_ctx& ctx, const lpca_matrix_view* x) {
   DevX d = stage_x(ctx, x, "kx", nullptr);
-  if (d.dtype == 8 || d.m * d.n == 0) {
+  if (d.sparse() || d.dtype == 8 || d.m * d.n == 0) {
     d.dtype = 8;
     return d;
   }
@@ -1535,7 +1628,13 @@ lpca_status lpca_spmm(lpca_ctx* ctx, const lpca_matrix_view* x, const double* w,
     const index_t m = d.m, n = d.n;
     const double* wd = stage_f64(*ctx, w, n * w_cols, w_location, "k.w");
     double* od = out_location == LPCA_DEVICE ? out : ctx->get<double>("k.out", m * w_cols);
-    if (m > 0 && w_cols > 0) {
+    if (m > 0 && w_cols > 0 && d.sparse()) {
+      double* wt = ctx->get<double>("k.wrows", n * w_cols);
+      launch_transpose(ctx->stream, 8, wd, n, n, w_cols, wt, w_cols);
+      LPCA_LAUNCHED(*ctx);
+      launch_spmm_csr(ctx->stream, m, d.rp, d.ci, d.rv, wt, w_cols, w_cols, od, 8, 1, m);
+      LPCA_LAUNCHED(*ctx);
+    } else if (m > 0 && w_cols > 0) {
       launch_xw_simt<double, double>(ctx->stream, static_cast<const double*>(d.p), m, n, d.ld, wd,
                                      w_cols, n, od, 1, m, true);
       LPCA_LAUNCHED(*ctx);
@@ -1560,7 +1659,10 @@ lpca_status lpca_gemm_t(lpca_ctx* ctx, const double* u, int64_t m, int64_t l, in
     }
     double* od = out_location == LPCA_DEVICE ? out : ctx->get<double>("k.out", l * n);
     if (l * n > 0) {
-      if (m > 0) {
+      if (m > 0 && d.sparse()) {
+        launch_gemm_t_csc(ctx->stream, n, d.cp, d.ri, d.cv, urow, l, l, od, false);
+        LPCA_LAUNCHED(*ctx);
+      } else if (m > 0) {
         launch_utx_simt<double>(ctx->stream, urow, l, static_cast<const double*>(d.p), d.ld, m, l, n,
                                 round_up(m, 16), od, true);
         LPCA_LAUNCHED(*ctx);

@@ -307,6 +307,38 @@ inline ReductionMap reduce(const SparseMatrix& x, const ReducerConfig& c, Reduce
   return detail::fit(x, c, c.method, t);
 }
 
+// ---- map files (reducer.hpp:96-99): the reference's byte format -------------------
+inline void save_map_file(const ReductionMap& map, const std::string& path) {
+  lpca_map_info info{};
+  info.method = static_cast<int32_t>(reducer_method_from_string(map.method));
+  info.k = map.k;
+  info.l = map.l;
+  info.n = map.n;
+  info.seed = map.seed;
+  info.density = map.density;
+  info.scale = map.scale;
+  info.has_singular_values = map.singular_values.empty() ? 0 : 1;
+  detail::check(lpca_map_file_write(path.c_str(), &info, map.v.data(),
+                                    map.singular_values.empty() ? nullptr : map.singular_values.data()));
+}
+inline ReductionMap load_map_file(const std::string& path) {
+  lpca_map_info info{};
+  detail::check(lpca_map_file_read(path.c_str(), &info, nullptr, 0, nullptr));
+  ReductionMap out;
+  out.method = to_string(static_cast<ReducerMethod>(info.method));
+  out.k = info.k;
+  out.l = info.l;
+  out.n = info.n;
+  out.seed = info.seed;
+  out.density = info.density;
+  out.scale = info.scale;
+  out.v = DenseMatrix(info.n, info.k);
+  if (info.has_singular_values) out.singular_values.resize(static_cast<std::size_t>(info.k));
+  detail::check(lpca_map_file_read(path.c_str(), &info, out.v.data(), info.n * info.k,
+                                   info.has_singular_values ? out.singular_values.data() : nullptr));
+  return out;
+}
+
 // ---- streaming (sparse_matrix.hpp:53-79, reducer.hpp:82-85) -----------------------
 struct RowBlock {
   index_t slice_index = 0;

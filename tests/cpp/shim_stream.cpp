@@ -47,6 +47,10 @@ int main() {
     }
     const auto y = lazypca::apply_map(st, x);
     if (y.rows() != m || y.cols() != 4) bad = 1;
+    lazypca::save_map_file(st, "/tmp/lpca_shim_test.map");  // map file round trip
+    const auto back = lazypca::load_map_file("/tmp/lpca_shim_test.map");
+    if (back.v.data()[5] != st.v.data()[5] || back.singular_values != st.singular_values || back.method != st.method)
+      bad = 1;
   }
   try {
     lazypca::SliceRowBlockStream empty(lazypca::SparseMatrix::from_csc(0, n, std::vector<lazypca::index_t>(n + 1, 0), {}, {}), 10);

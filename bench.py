@@ -31,7 +31,19 @@ CONFIGS = {
                name="configs[1]: X fp32 1,000,000x4,096, r=200, rho=0.97, k=100, l=110, q=0"),
     "c3": dict(m=4_600_000, n=4_096, r=300, rho=0.98, k=200, l=220, q=1, dtype="f32",
                name="configs[2]: X fp32 4,600,000x4,096, r=300, rho=0.98, k=200, l=220, q=1"),
+    "c4": dict(m=2_000_000, n=16_384, r=400, rho=0.98, k=256, l=300, q=2, dtype="f32",
+               kind="very_sparse", density=1.0 / 128,
+               name="configs[3]: X fp32 2,000,000x16,384, r=400, rho=0.98, very sparse Omega "
+                    "(density 1/sqrt(n)), k=256, l=300, q=2"),
+    "c5": dict(m=1_000_000, n=2_048, r=500, rho=0.99, k=256, l=512, q=1, dtype="f64",
+               name="configs[4] per GPU: X fp64 1,000,000x2,048 (8e6 rows over 8 GPUs), r=500, "
+                    "rho=0.99, k=256, l=512, q=1"),
 }
+
+
+def projection(cfg, lp):
+    kind = lp.ProjectionKind.very_sparse if cfg.get("kind") == "very_sparse" else lp.ProjectionKind.gaussian
+    return lp.ProjectionSpec(kind=kind, density=cfg.get("density", 1.0), seed=SEED_OMEGA)
 SEED_X, SEED_OMEGA = 1000, 7
 METRIC = "Lazy SPCA fit+transform samples/sec"
 
@@ -119,6 +131,7 @@ def cpu_reference(cfg: dict, sample_rows: int, threads: int, steps: int = 1, war
         for i in range(warmup + steps):
             t0 = time.perf_counter()
             v, s, _ = O.reduce_lazy_spca(x.astype(np.float64), cfg["k"], cfg["l"], SEED_OMEGA,
+                                         kind=cfg.get("kind", "gaussian"), density=cfg.get("density", 1.0),
                                          power_iters=cfg["q"])
             O.apply_map(x, v)
             if i >= warmup:
@@ -127,7 +140,9 @@ def cpu_reference(cfg: dict, sample_rows: int, threads: int, steps: int = 1, war
         kind = "reference"
         times = []
         for i in range(warmup + steps):
-            _, _, _, secs = R.fit_transform(2, x, cfg["k"], cfg["l"], SEED_OMEGA, want_y=True)
+            _, _, _, secs = R.fit_transform(2, x, cfg["k"], cfg["l"], SEED_OMEGA,
+                                            kind=1 if cfg.get("kind") == "very_sparse" else 0,
+                                            density=cfg.get("density", 1.0), want_y=True)
             if i >= warmup:
                 times.append(secs)
     per = sum(times) / len(times)
@@ -184,7 +199,7 @@ def run_ours(args, cfg):
     lp.synth_lowrank(x, rank * m, cfg["r"], cfg["rho"], 0.01, SEED_X, ctx=ctx)
     y = torch.empty((m, k), dtype=tdt, device="cuda")
     conf = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=k, l=l,
-                            projection=lp.ProjectionSpec(seed=SEED_OMEGA), power_iters=cfg["q"])
+                            projection=projection(cfg, lp), power_iters=cfg["q"])
     torch.cuda.synchronize()
 
     def step(tm=None):

@@ -327,6 +327,10 @@ class _View:
             v.dtype = L.LPCA_F32 if x.dtype == torch.float32 else L.LPCA_F64
             v.layout = L.LPCA_ROW_MAJOR
             v.location = L.LPCA_DEVICE if x.is_cuda else L.LPCA_HOST
+            if x.is_cuda:
+                # the library runs on its context's stream: make torch's pending
+                # writes to x visible first (a no-op wait when the streams are one)
+                torch.cuda.current_stream(x.device).synchronize()
             v.rows, v.cols, v.ld = x.shape[0], x.shape[1], x.stride(0) if x.shape[0] > 1 else x.shape[1]
             v.data = x.data_ptr() if x.numel() else None
         else:

@@ -182,6 +182,8 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 // lazy_projector.cpp:12-37).
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
                          int* status);
+// g_ii += c * trace(g) (shifted CholeskyQR's first pass).
+void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c);
 // F <- L^{-1} F  ==  (Z R^{-1})^T for Z = F^T; rinv = L^{-T} upper, F l x n col-major.
 void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
                          double* tmp);

@@ -19,6 +19,7 @@
 #include <memory>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/lazypca_b200.h"
@@ -116,6 +117,7 @@ struct lpca_ctx {
   int eigensolver = 0;  // 0: tridiagonal route (tridiag_eigh), 1: parallel Jacobi (jacobi_eigh)
   std::unordered_map<std::string, std::pair<void*, std::size_t>> ws;
   cudaEvent_t ev[18] = {};
+  std::unordered_set<lpca_map*> live_maps;  // maps whose V was allocated on this context's stream
   int pass_slot = -1;  // >= 0: the next X pass records ev[pass_slot] / ev[pass_slot + 1] around its kernel
 
   void note_launch(int n = 1) { launches += n; }
@@ -157,11 +159,15 @@ struct lpca_map {
   // no device-wide synchronisation per fit (cudaMalloc/cudaFree would stall the
   // pipeline). A map must be destroyed before its context.
   cudaStream_t stream = nullptr;
-  void alloc_v(cudaStream_t s, std::size_t bytes) {
-    stream = s;
-    LPCA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&v), bytes, s));
+  lpca_ctx* owner = nullptr;  // cleared if the context goes first (then V frees on the legacy stream)
+  void alloc_v(lpca_ctx& c, std::size_t bytes) {
+    owner = &c;
+    stream = c.stream;
+    c.live_maps.insert(this);
+    LPCA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&v), bytes, stream));
   }
   ~lpca_map() {
+    if (owner) owner->live_maps.erase(this);
     if (v) cudaFreeAsync(v, stream);
   }
 };
@@ -628,8 +634,12 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
   if (over_ranks) ctx.allreduce(f, l * n);
 }
 
-// CholeskyQR step on a wide F (l x n, F = Z^T): F <- L^{-1} F with
-// L L^T = F F^T. Returns the failing pivot (+1) or 0.
+// Orthonormalises the power step's Z (n x l, held as F = Z^T, l x n) by
+// shifted CholeskyQR3 (Fukaya et al. 2020): a first Cholesky of ZᵀZ + s·I with
+// s = 11 (n l + l (l + 1)) u ||Z||_F^2 survives condition numbers up to ~1/u
+// (q >= 2 makes Z's columns that close: plain CholeskyQR2 fails there, as the
+// survey's naive-power probe did), then two plain CholeskyQR passes
+// restore orthogonality. Each pass: F <- L^{-1} F with L L^T = F F^T.
 void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
   double* g = ctx.get<double>("orth.g", l * l);
   double* w = ctx.get<double>("orth.w", l * l);
@@ -637,9 +647,14 @@ void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
   double* tmp = ctx.get<double>("orth.tmp", l * n);
   int* st = ctx.get<int>("orth.status", 1);
   double* gpart = ctx.get<double>("gram.part", gram_fast_chunks(l, n) * l * l);
-  for (int pass = 0; pass < 2; ++pass) {
+  const double shift = 11.0 * (static_cast<double>(n) * l + static_cast<double>(l) * (l + 1)) * 0x1p-53;
+  for (int pass = 0; pass < 3; ++pass) {
     launch_gram_fast(ctx.stream, f, l, n, g, gpart);
     LPCA_LAUNCHED(ctx);
+    if (pass == 0) {
+      launch_add_trace_shift(ctx.stream, g, l, shift);
+      LPCA_LAUNCHED(ctx);
+    }
     launch_chol_inverse(ctx.stream, g, l, w, lm, st);
     LPCA_LAUNCHED(ctx);
     int h = 0;
@@ -772,7 +787,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
   map->density = c.density;
   map->scale = projection_scale(c);
   try {
-    map->alloc_v(ctx.stream, sizeof(double) * (n * k > 0 ? n * k : 1));
+    map->alloc_v(ctx, sizeof(double) * (n * k > 0 ? n * k : 1));
     double* omega = ctx.get<double>("omega", n * l);
     regenerate_dev(ctx, c, omega);
     if (c.method == LPCA_RP) {
@@ -947,9 +962,12 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       double* vt = ctx.get<double>("v.rows", map.n * k);
       launch_transpose(ctx.stream, 8, map.v, map.n, map.n, k, vt, k);
       LPCA_LAUNCHED(ctx);
+      pass_mark(ctx, 0);
       launch_spmm_csr(ctx.stream, m, x.rp, x.ci, x.rv, vt, k, k, ydev, y_dtype, ors, ocs);
       LPCA_LAUNCHED(ctx);
+      pass_mark(ctx, 1);
     } else if (x.dtype == 8) {
+      pass_mark(ctx, 0);
       if (y_dtype == 8)
         launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
                                        map.v, k, map.n, static_cast<double*>(ydev), ors, ocs, ctx.exact != 0);
@@ -957,6 +975,7 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
         launch_xw_simt<double, float>(ctx.stream, static_cast<const double*>(x.p), m, x.n, x.ld,
                                       map.v, k, map.n, static_cast<float*>(ydev), ors, ocs, ctx.exact != 0);
       LPCA_LAUNCHED(ctx);
+      pass_mark(ctx, 1);
     } else if (row && y_dtype == 4 && use_tc(ctx, x, k) && ldy % 4 == 0) {
       Panel yo;
       yo.plain = ydev;
@@ -982,6 +1001,7 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       float* w32 = ctx.get<float>("v.f32", k * x.n);
       launch_convert_f64_to_f32(ctx.stream, map.v, map.n, w32, x.n, x.n, k, 1.0);
       LPCA_LAUNCHED(ctx);
+      pass_mark(ctx, 0);
       if (y_dtype == 4)
         launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(x.p), m, x.n, x.ld, w32,
                                      k, x.n, static_cast<float*>(ydev), ors, ocs, false);
@@ -989,6 +1009,7 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
         launch_xw_simt<float, double>(ctx.stream, static_cast<const float*>(x.p), m, x.n, x.ld, w32,
                                       k, x.n, static_cast<double*>(ydev), ors, ocs, false);
       LPCA_LAUNCHED(ctx);
+      pass_mark(ctx, 1);
     }
     ev.mark(7);
     ctx.pass_slot = -1;
@@ -1135,7 +1156,7 @@ lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& 
   map->seed = c.seed;
   map->density = c.density;
   map->scale = projection_scale(c);
-  map->alloc_v(ctx.stream, sizeof(double) * (n * k > 0 ? n * k : 1));
+  map->alloc_v(ctx, sizeof(double) * (n * k > 0 ? n * k : 1));
   double* omega = ctx.get<double>("omega", n * l);
   regenerate_dev(ctx, c, omega);
   if (c.method == LPCA_RP) {  // no data pass (reduce_rp, reducer.cpp:171-190)
@@ -1345,6 +1366,10 @@ lpca_status lpca_ctx_destroy(lpca_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    for (lpca_map* m : ctx->live_maps) {  // maps may outlive their context
+      m->owner = nullptr;
+      m->stream = nullptr;
+    }
     for (auto& kv : ctx->ws) cudaFree(kv.second.first);
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
@@ -1568,7 +1593,7 @@ lpca_status lpca_map_create(lpca_ctx* ctx, const lpca_map_info* info, const doub
     map->density = info->density;
     map->scale = info->scale;
     try {
-      map->alloc_v(ctx->stream, sizeof(double) * (info->n * info->k > 0 ? info->n * info->k : 1));
+      map->alloc_v(*ctx, sizeof(double) * (info->n * info->k > 0 ? info->n * info->k : 1));
       if (info->n * info->k > 0)
         LPCA_CUDA(cudaMemcpyAsync(map->v, v_host, sizeof(double) * info->n * info->k, cudaMemcpyHostToDevice, ctx->stream));
       LPCA_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -473,6 +473,30 @@ void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rin
   chol_inverse_kernel<<<1, 1024, 0, s>>>(g, l, rinv, work, status);
 }
 
+namespace {
+// g_ii += c * trace(g): the shift of shifted CholeskyQR (one CTA, fixed-order sum).
+__global__ void add_trace_shift_kernel(double* g, index_t l, double c) {
+  __shared__ double red[32];
+  double t = 0.0;
+  for (index_t j = threadIdx.x; j < l; j += blockDim.x) t += g[j * l + j];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const double shift = c * red[0];
+  for (index_t j = threadIdx.x; j < l; j += blockDim.x) g[j * l + j] += shift;
+}
+}  // namespace
+
+void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c) {
+  add_trace_shift_kernel<<<1, 1024, 0, s>>>(g, l, c);
+}
+
 void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
                          double* tmp) {
   const index_t total = l * n;

@@ -293,3 +293,16 @@ def test_streaming_config_runs_the_streaming_reducer(ctx, ref):
     c.streaming, c.block_rows = True, 0
     with pytest.raises(lp.InvalidArgumentError, match="block_rows"):
         lp.reduce(x, c, ctx=ctx)
+
+
+def test_map_outliving_its_context_is_safe():
+    # a map freed after its context (V came from that context's stream) must not crash
+    c = lp.Context(0)
+    x = np.random.default_rng(5).uniform(-1, 1, (300, 40))
+    m = lp.reduce_lazy_spca(x, _cfg(lp.ReducerMethod.lazy_spca, 4, 8, 3), ctx=c)
+    v = m.v.copy()
+    c.close()
+    other = lp.Context(0)
+    assert np.allclose(lp.apply_map(m, x, ctx=other), x @ v, atol=1e-10)
+    del m
+    other.close()

@@ -207,6 +207,20 @@ lpca_status lpca_map_file_write(const char* path, const lpca_map_info* info, con
 lpca_status lpca_map_file_read(const char* path, lpca_map_info* info, double* v_host, int64_t v_capacity,
                                double* sigma_host);
 
+/* ---- verification metrics on the device (proj/core/src/metrics.cpp) --------
+ * chordal_distance (:123-136): n x k1 and n x k2 column-major orthonormal bases;
+ * InvalidArgumentError if either is not orthonormal to 1e-8 * k. */
+lpca_status lpca_chordal_distance(lpca_ctx* ctx, const double* v1, int64_t n1, int64_t k1, const double* v2,
+                                  int64_t n2, int64_t k2, int32_t location, double* out);
+/* distance_preservation (:311-352): all row pairs when there are at most
+ * max_pairs of them, else max_pairs pairs drawn like the reference (seeded
+ * xoshiro256**, with replacement). Per-pair arrays (capacity max_pairs, or the
+ * pair count) may be NULL; map_b may be NULL. */
+lpca_status lpca_distance_preservation(lpca_ctx* ctx, const lpca_matrix_view* x, const lpca_map* map_a,
+                                       const lpca_map* map_b, int64_t max_pairs, uint64_t seed, int64_t* n_pairs,
+                                       int64_t* pair_i, int64_t* pair_j, double* original, double* reduced_a,
+                                       double* reduced_b, double* max_violation, double* max_discrepancy);
+
 /* ---- kernel-level exports (proj/core/include/lazypca/kernels.hpp:17-36,
  *      truncated_svd.hpp:24, tridiag_eigh.hpp:8). Host or device operands; fp64
  *      column-major unless stated; X views as above. ------------------------- */

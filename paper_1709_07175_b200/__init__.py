@@ -12,7 +12,8 @@ from .api import (  # noqa: F401
     fit_transform, gemm_t, gemm_t_f32, gen_gaussian, gen_very_sparse, jacobi_eigh, projection_kind_from_string,
     reduce, reduce_lazy_spca, reduce_lazy_spca_streaming, reduce_rp, reduce_spca, reduce_spca_streaming,
     reducer_method_from_string, regenerate, RowBlock, RowBlockStream, SliceRowBlockStream, split_rows,
-    load_map_file, read_map_file, save_map_file, write_map_file,
+    load_map_file, read_map_file, save_map_file, write_map_file, chordal_distance, distance_preservation,
+    DistancePreservationReport,
     set_thread_count, sketch_f32, spmm, synth_lowrank, thread_count, to_string, tridiag_eigh,
     truncated_svd_via_gram,
 )

@@ -89,6 +89,9 @@ SIGNATURES = {
     "lpca_map_copy_sigma": (I32, [P, P]),
     "lpca_map_create": (I32, [P, C.POINTER(MapInfo), P, P, PP]),
     "lpca_map_destroy": (I32, [P]),
+    "lpca_chordal_distance": (I32, [P, P, I64, I64, P, I64, I64, I32, DP]),
+    "lpca_distance_preservation": (I32, [P, C.POINTER(MatrixView), P, P, I64, C.c_uint64, C.POINTER(C.c_int64), P, P,
+                                         P, P, P, DP, DP]),
     "lpca_map_save": (I32, [P, C.c_char_p]),
     "lpca_map_load": (I32, [P, C.c_char_p, PP]),
     "lpca_map_file_write": (I32, [C.c_char_p, C.POINTER(MapInfo), P, P]),

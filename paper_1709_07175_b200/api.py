@@ -509,6 +509,52 @@ def _fit(x, config: ReducerConfig, timings, ctx) -> ReductionMap:
     return ReductionMap(h, ctx)
 
 
+# ---- verification metrics on the device (metrics.cpp) ------------------------------
+def chordal_distance(v1, v2, ctx=None) -> float:
+    """chordal_distance (metrics.cpp:123-136): subspace distance of two
+    orthonormal n x k bases, cancellation-free residual form."""
+    ctx = ctx or default_context()
+    a = np.asfortranarray(v1, dtype=np.float64)
+    b = np.asfortranarray(v2, dtype=np.float64)
+    out = C.c_double()
+    _check(ctx.lib.lpca_chordal_distance(ctx.h, a.ctypes.data if a.size else None, a.shape[0], a.shape[1],
+                                         b.ctypes.data if b.size else None, b.shape[0], b.shape[1], L.LPCA_HOST,
+                                         C.byref(out)))
+    return out.value
+
+
+@dataclass
+class DistancePreservationReport:
+    """metrics.hpp:51-65: sampled (i, j) pairs with original and reduced distances."""
+    pair_i: np.ndarray
+    pair_j: np.ndarray
+    original: np.ndarray
+    reduced_a: np.ndarray
+    reduced_b: np.ndarray
+    max_contraction_violation: float
+    max_map_discrepancy: float
+
+
+def distance_preservation(x, map_a: "ReductionMap", map_b: "ReductionMap" = None, max_pairs: int = 10000,
+                          seed: int = 0, ctx=None) -> DistancePreservationReport:
+    """distance_preservation (metrics.cpp:311-352), distances computed on the device."""
+    ctx = ctx or map_a._ctx
+    vw = _View(x)
+    m = vw.view.rows
+    cap = int(min(max_pairs, max(0, m * (m - 1) // 2))) if m * (m - 1) // 2 <= max_pairs else int(max_pairs)
+    pi = np.zeros(max(cap, 1), dtype=np.int64)
+    pj = np.zeros(max(cap, 1), dtype=np.int64)
+    o, ra, rb = (np.zeros(max(cap, 1)) for _ in range(3))
+    npairs, viol, gap = C.c_int64(), C.c_double(), C.c_double()
+    _check(ctx.lib.lpca_distance_preservation(ctx.h, C.byref(vw.view), map_a.handle(),
+                                              map_b.handle() if map_b is not None else None, int(max_pairs),
+                                              int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(npairs), pi.ctypes.data,
+                                              pj.ctypes.data, o.ctypes.data, ra.ctypes.data, rb.ctypes.data,
+                                              C.byref(viol), C.byref(gap)))
+    n = npairs.value
+    return DistancePreservationReport(pi[:n], pj[:n], o[:n], ra[:n], rb[:n], viol.value, gap.value)
+
+
 # ---- map files (reducer.cpp:355-412), byte-compatible with the reference ----------
 def save_map_file(map_: "ReductionMap", path: str) -> None:
     """save_map_file: one-line JSON header + V as a dense MatrixMarket array."""

@@ -53,6 +53,32 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
+// Two sums in one pass of barriers (red needs 66 doubles).
+__device__ void block_sum2(double& a, double& b, double* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __syncthreads();
+  if (lane == 0) {
+    red[w] = a;
+    red[33 + w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double sa = lane < static_cast<int>(blockDim.x / 32) ? red[lane] : 0.0;
+    double sb = lane < static_cast<int>(blockDim.x / 32) ? red[33 + lane] : 0.0;
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      red[32] = sa;
+      red[65] = sb;
+    }
+  }
+  __syncthreads();
+  a = red[32];
+  b = red[65];
+}
+
 __device__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -77,7 +103,7 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const double* __re
                                                               double* e, double* h, double* norm_out,
                                                               int* status, double* gap) {
   extern __shared__ double smem[];
-  __shared__ double red[33];
+  __shared__ double red[66];
   __shared__ double sh_scal[4];
   double* A = a_in_smem ? smem : refl;
   double* u_s = a_in_smem ? smem + static_cast<size_t>(l) * l : smem;  // u, p, q vectors
@@ -114,9 +140,16 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const double* __re
       }
       continue;
     }
-    double part = 0.0;
-    for (int k = tid; k < i; k += kTriThreads) part += fabs(ui[k]);
-    const double scale = block_sum(part, red);
+    // |x| and x^2 sums in one reduction (the reference sums (x/scale)^2; the
+    // two differ by roundoff only)
+    double pa = 0.0, ps = 0.0;
+    for (int k = tid; k < i; k += kTriThreads) {
+      const double x = ui[k];
+      pa += fabs(x);
+      ps += x * x;
+    }
+    block_sum2(pa, ps, red);
+    const double scale = pa;
     if (scale == 0.0) {
       if (tid == 0) {
         e[i] = 0.0;
@@ -124,26 +157,25 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const double* __re
       }
       continue;
     }
-    part = 0.0;
-    for (int k = tid; k < i; k += kTriThreads) {
-      const double v = ui[k] / scale;
-      u_s[k] = v;
-      part += v * v;
-    }
-    const double sigma = block_sum(part, red);
+    const double inv = 1.0 / scale;
+    const double sigma = ps * inv * inv;
+    for (int k = tid; k < i; k += kTriThreads) u_s[k] = ui[k] * inv;
     if (tid == 0) {
-      const double f = u_s[i - 1];
+      const double f = ui[i - 1] * inv;
       const double g = f >= 0.0 ? -sqrt(sigma) : sqrt(sigma);
       e[i] = scale * g;
       const double hh = sigma - f * g;
-      u_s[i - 1] = f - g;
       h[i] = hh;
       sh_scal[0] = hh;
+      sh_scal[1] = f - g;
     }
     __syncthreads();
     const double hh = sh_scal[0];
-    // p = A u / h over the active i x i block; A is symmetric, so row r is
-    // column r (contiguous): kRowLanes threads per row, shuffle-reduced.
+    if (tid == 0) u_s[i - 1] = sh_scal[1];  // the reflector's last entry
+    __syncthreads();
+    // p = A u / h over the active i x i block (A symmetric: row r is column r,
+    // contiguous): kRowLanes threads per row; u^T p accumulates alongside.
+    double pu = 0.0;
     for (int base = 0; base < i; base += kTriThreads / kRowLanes) {
       const int r = base + tid / kRowLanes, ln = tid % kRowLanes;
       double acc = 0.0;
@@ -152,24 +184,30 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const double* __re
         for (int c = ln; c < i; c += kRowLanes) acc = fma(ar[c], u_s[c], acc);
       }
       for (int o = kRowLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (r < i && ln == 0) p_s[r] = acc / hh;
+      if (r < i && ln == 0) {
+        const double pr = acc / hh;
+        p_s[r] = pr;
+        pu += u_s[r] * pr;
+      }
     }
+    const double kk = block_sum(pu, red) / (2.0 * hh);  // its barriers publish p_s
+    for (int k = tid; k < i; k += kTriThreads) q_s[k] = p_s[k] - kk * u_s[k];
     __syncthreads();
-    part = 0.0;
-    for (int k = tid; k < i; k += kTriThreads) part += u_s[k] * p_s[k];
-    const double kk = block_sum(part, red) / (2.0 * hh);
-    for (int k = tid; k < i; k += kTriThreads) {
-      q_s[k] = p_s[k] - kk * u_s[k];
-      ui[k] = u_s[k];  // keep the reflector where the back-transformation reads it
-    }
-    __syncthreads();
-    // A <- A - u q^T - q u^T on the active block; separate multiply and add so
-    // (r, c) and (c, r) receive the same two products and stay bitwise equal.
-    for (int idx = tid; idx < i * i; idx += kTriThreads) {
-      const int c = idx / i, r = idx % i;
+    // A <- A - u q^T - q u^T on the active block's lower triangle, mirrored:
+    // (r, c) and (c, r) get the same value by construction.
+    const int tri = i * (i + 1) / 2;
+    for (int t = tid; t < tri; t += kTriThreads) {
+      // t -> (r, c), c <= r: row r starts at r (r + 1) / 2
+      int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      if (r * (r + 1) / 2 > t) --r;
+      if ((r + 1) * (r + 2) / 2 <= t) ++r;
+      const int c = t - r * (r + 1) / 2;
       const double upd = __dadd_rn(__dmul_rn(u_s[r], q_s[c]), __dmul_rn(q_s[r], u_s[c]));
-      A[static_cast<size_t>(c) * l + r] = __dsub_rn(A[static_cast<size_t>(c) * l + r], upd);
+      const double nv = __dsub_rn(A[static_cast<size_t>(c) * l + r], upd);
+      A[static_cast<size_t>(c) * l + r] = nv;
+      A[static_cast<size_t>(r) * l + c] = nv;
     }
+    for (int k = tid; k < i; k += kTriThreads) ui[k] = u_s[k];  // the reflector, for the back-transformation
     __syncthreads();
   }
   double tn = 0.0;

@@ -384,7 +384,7 @@ uint32_t tmem_cols_for(uint32_t need) {
 
 // TMEM plan: nrb run buffers + long accumulator + A ring (64 columns per slot).
 bool plan_tmem(int npad, int& nrb, int& aslots, uint32_t& cols) {
-  const int max_nrb = env_int("LPCA_TC_NRB", 2);
+  const int max_nrb = env_int("LPCA_TC_NRB", 2) > 2 ? 2 : env_int("LPCA_TC_NRB", 2);  // tfull/tempty hold 2
   const int max_as = env_int("LPCA_TC_ASLOTS", 2);
   for (int r = max_nrb; r >= 1; --r) {
     const int acc = (r + 1) * npad;
@@ -411,7 +411,7 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
   if (kHalf && a.scan && a.run_stages > a.stages) throw Error(kInternal, "tc pair: a run must fit the stage ring");
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad + 4 * 4 * kBM;
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad + kRscRing * 4 * kBM;
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;

@@ -65,6 +65,19 @@ void launch_spmm_csr(cudaStream_t s, index_t m, const std::int64_t* row_ptr, con
 // F (l x n column-major) (+)= U^T X with X in CSC and U row-major m x l (ld ldu), l <= 512.
 void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, const std::int32_t* row,
                        const double* val, const double* u, index_t ldu, index_t l, double* f, bool accumulate);
+// ---- verification metrics (metrics.cu; metrics.cpp:123-136, 311-352) -------------
+// C (ka x kb) = A^T B, A n x ka and B n x kb column-major fp64.
+void launch_atb(cudaStream_t s, const double* a, index_t n, index_t ka, const double* b, index_t kb, double* c);
+// part[0 .. residual_sq_blocks(n, ka)) = tile sums of (A - B C)^2, C kb x ka.
+index_t residual_sq_blocks(index_t n, index_t ka);
+void launch_residual_sq(cudaStream_t s, const double* a, index_t n, index_t ka, const double* b, index_t kb,
+                        const double* c, double* part);
+// Pair distances: orig from X (dense row-major dtype/ld, or CSR when rp), da/db
+// from row-major Y_a / Y_b (m x k fp64; yb nullable).
+void launch_pair_distances(cudaStream_t s, int dtype, const void* x, index_t ld, index_t n, const std::int64_t* rp,
+                           const std::int32_t* ci, const double* rv, const double* ya, const double* yb, index_t k,
+                           const std::int64_t* pi, const std::int64_t* pj, index_t pairs, double* orig, double* da,
+                           double* db);
 // y += x (fp64), the streaming reducers' running F and U^T U (gemm_t_add, kernels.cpp:95-113).
 void launch_add_f64(cudaStream_t s, const double* x, double* y, index_t count);
 // out[idx] = sum_c part[c][idx], c ascending (fixed order; no float atomics).

@@ -25,6 +25,7 @@
 #include "../../include/lazypca_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "rng.cuh"
 
 using lpca::Error;
 using lpca::index_t;
@@ -132,6 +133,8 @@ struct lpca_ctx {
     }
     void* p = nullptr;
     LPCA_CUDA(cudaMalloc(&p, bytes < 256 ? 256 : bytes));
+    if (std::getenv("LPCA_WS_POISON"))  // debugging aid: NaN-fill new workspaces
+      LPCA_CUDA(cudaMemsetAsync(p, 0xff, bytes < 256 ? 256 : bytes, stream));
     ws[name] = {p, bytes};
     return p;
   }
@@ -1696,6 +1699,122 @@ lpca_status lpca_gemm_t(lpca_ctx* ctx, const double* u, int64_t m, int64_t l, in
       }
     }
     finish_out(*ctx, out, od, l * n, out_location);
+  });
+}
+
+lpca_status lpca_chordal_distance(lpca_ctx* ctx, const double* v1, int64_t n1, int64_t k1, const double* v2,
+                                  int64_t n2, int64_t k2, int32_t location, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (!v1 && n1 * k1 > 0) || (!v2 && n2 * k2 > 0)) throw Error(kInvalidArgument, "null argument");
+    if (n1 != n2)
+      throw Error(kDimension, "chordal_distance: bases live in different dimensions (" + S(n1) + " vs " + S(n2) + ")");
+    const index_t n = n1;
+    const double* a = stage_f64(*ctx, v1, n * k1, location, "ch.v1");
+    const double* b = stage_f64(*ctx, v2, n * k2, location, "ch.v2");
+    double* g1 = ctx->get<double>("ch.g1", k1 * k1 > 0 ? k1 * k1 : 1);
+    double* g2 = ctx->get<double>("ch.g2", k2 * k2 > 0 ? k2 * k2 : 1);
+    double* c12 = ctx->get<double>("ch.c12", k1 * k2 > 0 ? k1 * k2 : 1);
+    double* c21 = ctx->get<double>("ch.c21", k1 * k2 > 0 ? k1 * k2 : 1);
+    launch_atb(ctx->stream, a, n, k1, a, k1, g1);
+    launch_atb(ctx->stream, b, n, k2, b, k2, g2);
+    launch_atb(ctx->stream, a, n, k1, b, k2, c12);
+    launch_atb(ctx->stream, b, n, k2, a, k1, c21);
+    LPCA_LAUNCHED(*ctx);
+    const index_t p1 = residual_sq_blocks(n, k1), p2 = residual_sq_blocks(n, k2);
+    double* part = ctx->get<double>("ch.part", p1 + p2 > 0 ? p1 + p2 : 1);
+    launch_residual_sq(ctx->stream, a, n, k1, b, k2, c21, part);       // ||V1 - V2 (V2^T V1)||^2
+    launch_residual_sq(ctx->stream, b, n, k2, a, k1, c12, part + p1);  // ||V2 - V1 (V1^T V2)||^2
+    LPCA_LAUNCHED(*ctx);
+    std::vector<double> h1(static_cast<std::size_t>(k1 * k1)), h2(static_cast<std::size_t>(k2 * k2)),
+        hp(static_cast<std::size_t>(p1 + p2));
+    if (!h1.empty()) LPCA_CUDA(cudaMemcpyAsync(h1.data(), g1, sizeof(double) * h1.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (!h2.empty()) LPCA_CUDA(cudaMemcpyAsync(h2.data(), g2, sizeof(double) * h2.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (!hp.empty()) LPCA_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    // check_orthonormal (metrics.cpp:21-31)
+    auto check = [](const std::vector<double>& g, index_t k, const char* which) {
+      double worst = 0.0;
+      for (index_t j = 0; j < k; ++j)
+        for (index_t i = 0; i < k; ++i)
+          worst = std::max(worst, std::abs(g[static_cast<std::size_t>(j * k + i)] - (i == j ? 1.0 : 0.0)));
+      if (worst > 1e-8 * static_cast<double>(std::max<index_t>(1, k)))
+        throw Error(kInvalidArgument, std::string("chordal_distance: ") + which +
+                                          " does not have orthonormal columns (max deviation " +
+                                          std::to_string(worst) + ")");
+    };
+    check(h1, k1, "first basis");
+    check(h2, k2, "second basis");
+    double r = 0.0;
+    for (double v : hp) r += v;
+    *out = std::sqrt(r);
+  });
+}
+
+lpca_status lpca_distance_preservation(lpca_ctx* ctx, const lpca_matrix_view* x, const lpca_map* map_a,
+                                       const lpca_map* map_b, int64_t max_pairs, uint64_t seed, int64_t* n_pairs,
+                                       int64_t* pair_i, int64_t* pair_j, double* original, double* reduced_a,
+                                       double* reduced_b, double* max_violation, double* max_discrepancy) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!map_a || !n_pairs) throw Error(kInvalidArgument, "null argument");
+    const DevX dx = stage_x(*ctx, x, "dp.x", nullptr);
+    const index_t m = dx.m;
+    if (m < 2) throw Error(kInvalidArgument, "distance_preservation: need at least two rows");
+    // pairs exactly as the reference draws them (metrics.cpp:320-335)
+    std::vector<std::int64_t> pi, pj;
+    const double total = 0.5 * static_cast<double>(m) * static_cast<double>(m - 1);
+    if (total <= static_cast<double>(max_pairs)) {
+      for (index_t i = 0; i < m; ++i)
+        for (index_t j = i + 1; j < m; ++j) {
+          pi.push_back(i);
+          pj.push_back(j);
+        }
+    } else {
+      Xoshiro rng(mix64(seed ^ 0x9a17b0a155a3f2c1ULL));
+      while (static_cast<index_t>(pi.size()) < max_pairs) {
+        const index_t i = static_cast<index_t>(rng.next() % static_cast<std::uint64_t>(m));
+        const index_t j = static_cast<index_t>(rng.next() % static_cast<std::uint64_t>(m));
+        if (i == j) continue;
+        pi.push_back(std::min(i, j));
+        pj.push_back(std::max(i, j));
+      }
+    }
+    const index_t np = static_cast<index_t>(pi.size());
+    const index_t k = map_a->k;
+    if (map_b && map_b->k != k) throw Error(kDimension, "distance_preservation: maps reduce to different k");
+    double* ya = ctx->get<double>("dp.ya", m * k > 0 ? m * k : 1);
+    double* yb = map_b ? ctx->get<double>("dp.yb", m * k > 0 ? m * k : 1) : nullptr;
+    transform_dev(*ctx, *map_a, dx, ya, LPCA_F64, LPCA_ROW_MAJOR, LPCA_DEVICE, k, nullptr, nullptr);
+    if (map_b) transform_dev(*ctx, *map_b, dx, yb, LPCA_F64, LPCA_ROW_MAJOR, LPCA_DEVICE, k, nullptr, nullptr);
+    auto* dpi = ctx->get<std::int64_t>("dp.pi", np);
+    auto* dpj = ctx->get<std::int64_t>("dp.pj", np);
+    double* dist = ctx->get<double>("dp.d", 3 * np);
+    LPCA_CUDA(cudaMemcpyAsync(dpi, pi.data(), sizeof(std::int64_t) * np, cudaMemcpyHostToDevice, ctx->stream));
+    LPCA_CUDA(cudaMemcpyAsync(dpj, pj.data(), sizeof(std::int64_t) * np, cudaMemcpyHostToDevice, ctx->stream));
+    launch_pair_distances(ctx->stream, dx.dtype, dx.p, dx.ld, dx.n, dx.rp, dx.ci, dx.rv, ya, yb, k, dpi, dpj, np,
+                          dist, dist + np, dist + 2 * np);
+    LPCA_LAUNCHED(*ctx);
+    std::vector<double> hd(static_cast<std::size_t>(3 * np));
+    LPCA_CUDA(cudaMemcpyAsync(hd.data(), dist, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost, ctx->stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    double worst_violation = -1e300, worst_gap = 0.0;
+    for (index_t p = 0; p < np; ++p) {
+      const double o = hd[p], a = hd[np + p], b = hd[2 * np + p];
+      worst_violation = std::max(worst_violation, a - o);
+      if (map_b) {
+        worst_violation = std::max(worst_violation, b - o);
+        worst_gap = std::max(worst_gap, std::abs(a - b));
+      }
+      if (pair_i) pair_i[p] = pi[static_cast<std::size_t>(p)];
+      if (pair_j) pair_j[p] = pj[static_cast<std::size_t>(p)];
+      if (original) original[p] = o;
+      if (reduced_a) reduced_a[p] = a;
+      if (reduced_b) reduced_b[p] = map_b ? b : 0.0;
+    }
+    *n_pairs = np;
+    if (max_violation) *max_violation = worst_violation;
+    if (max_discrepancy) *max_discrepancy = worst_gap;
   });
 }
 

@@ -251,16 +251,44 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(double* a, index
 
 // V(j, r) = (sum_i F(i, j) U~(i, r)) / sigma_r, i ascending, separate mul/add
 // (truncated_svd.cpp:52-62); sigma_r = sqrt(lambda_r).
-__global__ void vform_kernel(const double* __restrict__ f, index_t l, index_t n,
-                             const double* __restrict__ ut, const double* __restrict__ evals,
-                             index_t k, double* __restrict__ sigma, double* __restrict__ v) {
-  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
-  if (e < k && sigma) sigma[e] = sqrt(evals[e]);
-  if (e >= n * k) return;
-  const index_t r = e / n, j = e % n;
-  double dot = 0.0;
-  for (index_t i = 0; i < l; ++i) dot = __dadd_rn(dot, __dmul_rn(f[j * l + i], ut[r * l + i]));
-  v[r * n + j] = dot / sqrt(evals[r]);
+// V = F^T U~ diag(sigma)^{-1} (truncated_svd.cpp:51-62): each dot product runs
+// over i in ascending order with separate multiply and add (the reference's
+// rounding), tiled 32 (j) x 32 (r) per CTA through shared memory so F and U~
+// are read once per tile instead of once per output.
+__global__ void __launch_bounds__(256) vform_kernel(const double* __restrict__ f, index_t l, index_t n,
+                                                    const double* __restrict__ ut,
+                                                    const double* __restrict__ evals, index_t k,
+                                                    double* __restrict__ sigma, double* __restrict__ v) {
+  __shared__ double fs[32][33];
+  __shared__ double us[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const index_t j0 = static_cast<index_t>(blockIdx.x) * 32, r0 = static_cast<index_t>(blockIdx.y) * 32;
+  if (sigma && blockIdx.x == 0) {
+    const index_t e = r0 + ty * 32 + tx;
+    if (e < k && ty < 1) sigma[e] = sqrt(evals[e]);
+  }
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (index_t i0 = 0; i0 < l; i0 += 32) {
+    for (int t = ty; t < 32; t += 8) {
+      const index_t j = j0 + t, i = i0 + tx, r = r0 + t;
+      fs[tx][t] = (j < n && i < l) ? f[j * l + i] : 0.0;   // fs[i][j]
+      us[tx][t] = (r < k && i < l) ? ut[r * l + i] : 0.0;  // us[i][r]
+    }
+    __syncthreads();
+    const int iend = static_cast<int>(l - i0 < 32 ? l - i0 : 32);
+    for (int ii = 0; ii < iend; ++ii) {
+      const double fv = fs[ii][tx];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[t] = __dadd_rn(acc[t], __dmul_rn(fv, us[ii][ty + 8 * t]));
+    }
+    __syncthreads();
+  }
+  const index_t j = j0 + tx;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const index_t r = r0 + ty + 8 * t;
+    if (j < n && r < k) v[r * n + j] = acc[t] / sqrt(evals[r]);
+  }
 }
 
 // Canonical signs (truncated_svd.cpp:64-80): in each V column the entry of
@@ -461,7 +489,9 @@ void launch_jacobi_eigh(cudaStream_t s, double* a, index_t l, double* evals, dou
 void launch_vform(cudaStream_t s, const double* f, index_t l, index_t n, const double* ut,
                   const double* evals, index_t k, double* sigma, double* v) {
   const index_t total = n * k > k ? n * k : k;
-  vform_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(f, l, n, ut, evals, k, sigma, v);
+  (void)total;
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(k, 32)));
+  vform_kernel<<<grid, dim3(32, 8), 0, s>>>(f, l, n, ut, evals, k, sigma, v);
 }
 
 void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* ut, index_t l) {

@@ -38,6 +38,12 @@
 #pragma once
 #include <cuda_fp16.h>
 
+// Per-run A-row scales in flight (scan mode): the converters write run R's
+// scales before converting it, when the epilogue may still be folding run
+// R - 4 (MMA up to nrb = 2 runs ahead of the epilogue, converters up to two
+// stages = one run ahead of the MMA, plus the run being scanned): a ring of 8.
+constexpr int kRscRing = 8;
+
 struct PairArgs {
   int m, n;          // X is m x n
   int npad;          // UMMA N (multiple of 16); each CTA holds npad / 2 rows of B
@@ -250,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima / run scales
-  float* rsc = red + 5 * a.npad;  // after red [4][npad] + gsc [npad]: [4 runs][128] inverse A-row scales
+  float* rsc = red + 5 * a.npad;  // after red [4][npad] + gsc [npad]: [kRscRing runs][128] inverse A-row scales
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);
@@ -407,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ring_advance(st, ph, S);
           }
           sx = pow2_scale_for(mx);
-          rsc[(rc & 3) * kBM + i] = __frcp_rn(sx);
+          rsc[(rc % kRscRing) * kBM + i] = __frcp_rn(sx);
           xmax = fmaxf(xmax, mx);
         }
         for (int j = 0; j < nst; ++j) {
@@ -500,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t racc = lane_base + static_cast<uint32_t>(b * a.npad);
         const bool first = r == 0, last = r == runs - 1;
         // this run's A-row unscale (XW: X row; XTU: X column `row`): power of two
-        const float rowf = kHalf ? (a.scan ? rsc[(rc & 3) * kBM + q * 32 + lane] : xinv) : 1.0f;
+        const float rowf = kHalf ? (a.scan ? rsc[(rc % kRscRing) * kBM + q * 32 + lane] : xinv) : 1.0f;
         if (!last || to_planes16) {
           // fold the run into L: 32 columns per TMEM round trip (both loads
           // issued before one wait; the fold is latency-bound otherwise)
@@ -611,7 +617,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         epi_bar();
         const int blk = (t0 + static_cast<int>(rank) * kBM) / kBM;
-        for (int c = q * 32 + lane; c < a.npad; c += 128) {
+        // (a CTA whose 128 rows all lie past m owns no block: writing its
+        // scales would run past the [ceil(m/128)][npad] array)
+        for (int c = q * 32 + lane; c < a.npad && blk * kBM < a.m; c += 128) {
           const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
           const float mx = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c])) * f;
           const float sc = pow2_scale_for(mx);

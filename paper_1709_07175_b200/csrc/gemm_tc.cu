@@ -470,7 +470,8 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
     a.npad = wc;
     a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
     a.run_stages = env_int("LPCA_TC_RUN", p.half ? 2 : 4);
-    a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f);
+    a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f) ? (p.ovf ? 2 : 1) : 0;
+    a.ovf = p.ovf;
     a.xmax_in = p.xmax_in;
     a.xmax_val = p.xmax_val;
     a.xmax_out = c0 == 0 ? p.xmax_out : nullptr;

@@ -123,6 +123,7 @@ struct XwPairArgs {
   const uint32_t* xmax_in = nullptr;  // max|X| bits on the device, or
   float xmax_val = 0.0f;              // max|X| by value (xmax_in null)
   uint32_t* xmax_out = nullptr;       // atomicMax of the |X| bits actually read
+  int* ovf = nullptr;  // per-run scales from each run's first stage; set to 1 if a later stage needed a rescan
   float* out = nullptr;          // plain fp32 row-major (first wstore columns)
   index_t ldo = 0, wstore = 0;
   float* out_hi = nullptr;       // tf32 planes of OUT^T [wpad][ldh]

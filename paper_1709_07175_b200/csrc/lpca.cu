@@ -120,6 +120,7 @@ struct lpca_ctx {
   cudaEvent_t ev[18] = {};
   std::unordered_set<lpca_map*> live_maps;  // maps whose V was allocated on this context's stream
   int pass_slot = -1;  // >= 0: the next X pass records ev[pass_slot] / ev[pass_slot + 1] around its kernel
+  bool force_scan = false;  // fit_dev retry: per-run scales by the full scan
 
   void note_launch(int n = 1) { launches += n; }
 
@@ -439,6 +440,7 @@ struct XScale {
   bool record = false;        // tf32 pass that records max|X| into dev
   bool use = false;           // fp16 pass
   uint32_t* check = nullptr;  // fp16 X W: max|X| of the rows read
+  int* ovf = nullptr;         // scanless per-run scales: flags runs that need the scan
 };
 
 bool f16_enabled() {
@@ -502,6 +504,7 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
       p.xmax_in = xs->dev;
       p.xmax_val = xs->host;
       p.xmax_out = xs->check;
+      p.ovf = xs->ovf;
     } else {
       p.ldw = round_up(n, 4);
       float* hi = ctx.get<float>("w.hi", p.wpad * p.ldw);
@@ -834,6 +837,12 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     XScale sketch;
     sketch.use = true;
     sketch.check = xs.dev;
+    int* xovf = nullptr;
+    if (f16 && !ctx.force_scan) {  // scales from each run's first stage (rerun with the scan if flagged)
+      xovf = ctx.get<int>("xovf", 1);
+      launch_zero(ctx.stream, xovf, sizeof(int));
+      sketch.ovf = xovf;
+    }
     ev.mark(12);
     ev.mark(13);
     ctx.pass_slot = 12;
@@ -924,6 +933,22 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     if (f16) LPCA_CUDA(cudaMemcpyAsync(&map->xmax, xs.dev, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
     ev.mark(5);
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
+    if (xovf) {
+      int flagged = 0;
+      LPCA_CUDA(cudaMemcpy(&flagged, xovf, sizeof(int), cudaMemcpyDeviceToHost));
+      if (flagged) {  // some row's values outgrew its run's first-stage scale: redo with the scan
+        delete map;
+        ctx.force_scan = true;
+        try {
+          lpca_map* again = fit_dev(ctx, cfg_in, x, t);
+          ctx.force_scan = false;
+          return again;
+        } catch (...) {
+          ctx.force_scan = false;
+          throw;
+        }
+      }
+    }
     if (t) {
       t->sketch += ev.secs(0, 1);
       t->power += ev.secs(1, 2);

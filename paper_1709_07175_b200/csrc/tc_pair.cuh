@@ -52,9 +52,13 @@ struct PairArgs {
   int items;
   int chunk_rows;    // XTU: rows per chunk (multiple of 128)
   // fp16 A scale: scan = 1 gives every (row, run) its own power of two from the
-  // run's values (scanned in shared memory first); scan = 0 uses one scale for
-  // all of X from max|X| = *xmax_in (bits) or xmax_val
+  // run's values (scanned in shared memory first); scan = 2 takes it from the
+  // run's first stage with 16x headroom and flags (*ovf) any later stage that
+  // would overflow fp16 or sit 2^8 below the range (the caller then reruns with
+  // scan = 1); scan = 0 uses one scale for all of X from max|X| = *xmax_in
+  // (bits) or xmax_val
   int scan;
+  int* ovf;
   const uint32_t* xmax_in;
   float xmax_val;
   // X W: accumulate max|X| bits of the data actually read here (nullable)
@@ -382,6 +386,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < 32; ++kk) v[kk] = raw[kk * kBM + i];
       }
     };
+    auto absmax32k = [](const float (&v)[32]) {  // the same tree, keeping v
+      float t[16];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) t[kk] = fmaxf(fabsf(v[kk]), fabsf(v[kk + 16]));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) t[kk] = fmaxf(t[kk], t[kk + 8]);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) t[kk] = fmaxf(t[kk], t[kk + 4]);
+      return fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3]));
+    };
+    bool ovf = false;
     auto absmax32 = [](float (&v)[32]) {  // tree (a serial max chain is latency-bound); clobbers v
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) v[kk] = fmaxf(fabsf(v[kk]), fabsf(v[kk + 16]));
@@ -397,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
         const int nst = (min(k1, q0 + run_k) - q0 + BK - 1) / BK;
         float sx = xs;
-        if (kHalf && a.scan) {  // the run's stages are all resident (run_stages <= stages)
+        if (kHalf && a.scan == 1) {  // the run's stages are all resident (run_stages <= stages)
           float mx = 0.0f;
           int st = stage;
           uint32_t ph = phase;
@@ -422,24 +437,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint8_t* xt = smem + stage * stage_bytes;
           const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+          if (kHalf) {
+            float v0[32], v1[32];
+            load_row(xt, 0, v0);
+            load_row(xt, 1, v1);
+            if (a.scan == 2 || (kMode == kXW && a.xmax_out && a.scan == 0)) {
+              const float mx = fmaxf(absmax32k(v0), absmax32k(v1));
+              if (kMode == kXW && a.xmax_out) xmax = fmaxf(xmax, mx);
+              if (a.scan == 2) {
+                if (j == 0) {  // the run's scale: 16x headroom over its first stage
+                  sx = pow2_scale_for(16.0f * mx);
+                  rsc[(rc % kRscRing) * kBM + i] = __frcp_rn(sx);
+                } else if (mx * sx >= 32768.0f || (mx > 0.0f && mx * sx < 8.0f)) {
+                  ovf = true;
+                }
+              }
+            }
 #pragma unroll
-          for (int h = 0; h < (kHalf ? 2 : 1); ++h) {
+            for (int kk = 0; kk < 32; ++kk) {
+              v0[kk] *= sx;
+              v1[kk] *= sx;
+            }
+            float hi[16], lo[16];
+            split_f16_32(v0, hi, lo);
+            tmem_st16(at, hi);
+            tmem_st16(at + 32, lo);
+            split_f16_32(v1, hi, lo);
+            tmem_st16(at + 16, hi);
+            tmem_st16(at + 48, lo);
+          } else {
             float v[32];
-            load_row(xt, h, v);
-            if (kMode == kXW && a.xmax_out && !a.scan) {
+            load_row(xt, 0, v);
+            if (kMode == kXW && a.xmax_out && a.scan == 0) {
               float t[32];
 #pragma unroll
               for (int kk = 0; kk < 32; ++kk) t[kk] = v[kk];
               xmax = fmaxf(xmax, absmax32(t));
             }
-            if (kHalf) {
-#pragma unroll
-              for (int kk = 0; kk < 32; ++kk) v[kk] *= sx;
-              float hi[16], lo[16];
-              split_f16_32(v, hi, lo);
-              tmem_st16(at + h * 16, hi);
-              tmem_st16(at + 32 + h * 16, lo);
-            } else {
+            {
               float hi[32], lo[32];
 #pragma unroll
               for (int kk = 0; kk < 32; ++kk) {
@@ -464,6 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
       if (lane == 0) atomicMax(a.xmax_out, __float_as_uint(xmax));
     }
+    if (kHalf && a.scan == 2 && __any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(a.ovf, 1);
   } else {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
     const int q = warp & 3;

@@ -75,3 +75,21 @@ def test_tc_power_and_spca(ctx, ref):
     sp = _fit(ctx, x, 40, 60, "tcgen05", method=lp.ReducerMethod.spca)
     rv, rs, _, _ = ref.reduce(1, x.cpu().numpy(), 40, 60, 7)
     assert np.max(np.abs(sp.singular_values - rs) / rs) < 1e-4
+
+
+def test_sketch_first_stage_scales_fall_back_to_the_scan(ctx):
+    """The sketch takes each run's A-row scale from the run's first stage; rows
+    whose later stage outgrows it (or sits far below it) make the fit rerun with
+    the full per-run scan. X here has, in every 128-column run, a zero first
+    half and small values in the second half, and a few huge entries late."""
+    import torch
+    rng = np.random.default_rng(8)
+    m, n = 8192, 1024
+    x = rng.standard_normal((m, n)).astype(np.float32) * 1e-3
+    for c0 in range(0, n, 128):
+        x[:, c0:c0 + 64] = 0.0
+    x[::97, 1000] = 0.5
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=16, l=32, projection=lp.ProjectionSpec(seed=3))
+    m32 = lp.reduce_lazy_spca(torch.from_numpy(x).cuda(), cfg, ctx=ctx)
+    v64, s64, _ = O.reduce_lazy_spca(x.astype(np.float64), 16, 32, 3)
+    assert np.max(np.abs(m32.singular_values - s64) / s64) < 1e-4

@@ -709,7 +709,7 @@ void eigh_dev(lpca_ctx& ctx, double* a, index_t l, double* evals, double* evecs,
   }
   void* work = ctx.buf("eig.twork", eigh_tridiag_workspace(l));
   launch_eigh_tridiag(ctx.stream, a, l, evals, evecs, work, st, gap);
-  ctx.note_launch(10);
+  ctx.note_launch(12);
   LPCA_CUDA(cudaGetLastError());
 }
 

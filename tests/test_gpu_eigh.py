@@ -39,6 +39,18 @@ def test_gram_spectra(ctx, method, l, n, rho):
     _check(a, lp.eigh(a, ctx, method))
 
 
+@pytest.mark.parametrize("l", [31, 32, 33, 64, 65, 127, 128, 129, 160, 300, 512])
+def test_tridiag_size_classes(ctx, l):
+    """Every kernel variant boundary: register tridiagonalisation (l <= 32, 64,
+    128), shared/global above it; register back-transformation up to 512."""
+    a = _gram_like(l, 4 * l, 0.97, l)
+    _check(a, lp.eigh(a, ctx, "tridiag"))
+    rng = np.random.default_rng(l)
+    b = rng.standard_normal((l, l))
+    b = (b + b.T) / 2  # indefinite, unstructured
+    _check(b, lp.eigh(b, ctx, "tridiag"))
+
+
 @pytest.mark.parametrize("l", [300, 512])
 def test_gram_spectra_large_tridiag(ctx, l):
     a = _gram_like(l, 4 * l, 0.99, l)

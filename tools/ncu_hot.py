@@ -61,6 +61,6 @@ if len(sys.argv) > 5:
             if r[i].isdigit():
                 why[key][hdr[i][6:]] += int(r[i])
     print("--- by source line (top stall reasons)")
-    for k, v in agg.most_common(n):
+    for k, v in agg.most_common(int(sys.argv[6]) if len(sys.argv) > 6 else n):
         top = ", ".join(f"{w} {c / max(v, 1) * 100:.0f}%" for w, c in why[k].most_common(3))
         print(f"{v / tot * 100:5.1f}% {k:40s} {top}")

@@ -410,8 +410,11 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
-  if (kHalf && a.scan && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run must fit the ring
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 5 * 4 * a.npad + kRscRing * 4 * kBM;
+  if (kHalf && kMode == kXW && a.scan && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
+  if (kHalf && kMode == kXTU && a.run_stages > a.stages)
+    throw Error(kInternal, "tc pair: a U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
+  const size_t smem =
+      static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 7 * 4 * a.npad + kRscRing * 4 * kBM;  // + xbuf
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
@@ -506,10 +509,10 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
 index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_split) {
   const index_t ntiles = ceil_div(n, 2 * kBM);
   index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms / 2), ntiles);  // ~8 items per pair
-  const index_t max_chunks = ceil_div(m, 4 * 128);                           // >= 4 runs per item
+  const index_t max_chunks = ceil_div(m, 4 * kUScaleRows);                   // >= 4 runs per item
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
-  const index_t rows = round_up(ceil_div(m, chunks), 128);
+  const index_t rows = round_up(ceil_div(m, chunks), kUScaleRows);  // chunks start on U^T scale blocks
   chunks = ceil_div(m, rows);
   *rows_per_split = rows;
   return chunks;
@@ -533,7 +536,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
     a.npad = wc;
     a.chunk_rows = static_cast<int>(rows);
     a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
-    a.run_stages = p.half ? 2 : 4;  // fp16: one run per 128-row block of U^T scales
+    a.run_stages = 4;  // fp16: one run (4 x 64 rows) per kUScaleRows block of U^T scales
     a.scan = p.half && !p.xmax_in;
     a.xmax_in = p.xmax_in;
     a.uinv_in = p.uinv ? p.uinv + c0 : nullptr;

@@ -110,8 +110,12 @@ void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, 
 // ---- 2-SM pair passes (tc_pair.cuh) -------------------------------------------
 // Both encodings of the 3-term split: tf32 hi/lo (half = false) or fp16 hi/lo of
 // power-of-two scaled operands (half = true: X scaled from max|X| = *xmax_in,
-// W planes per column (winv = inverse scales), U^T planes per column and 128-row
-// block (uinv[block][c])). Planes are K-major: [wpad or round_up(l,16)][ld].
+// W planes per column (winv = inverse scales), U^T planes per column and
+// kUScaleRows-row block (uinv[block][c])). Planes are K-major: [wpad or round_up(l,16)][ld].
+// rows per block of the U^T fp16 plane scales: one 2-SM pair item of the X W
+// pass, one fp16 run (4 stages of 64 rows) of the X^T U pass
+constexpr index_t kUScaleRows = 256;
+
 struct XwPairArgs {
   const float* x = nullptr;
   index_t m = 0, n = 0, ldx = 0;
@@ -130,7 +134,7 @@ struct XwPairArgs {
   float* out_lo = nullptr;
   __half* uh = nullptr;          // fp16 planes of OUT^T [wpad][ldh] ...
   __half* ul = nullptr;
-  float* uinv = nullptr;         // ... with inverse scales [ceil(m/128)][wpad]
+  float* uinv = nullptr;         // ... with inverse scales [ceil(m/kUScaleRows)][wpad]
   index_t ldh = 0;
   cudaEvent_t ev_pre = nullptr, ev_post = nullptr;  // recorded around the kernel launch itself
 };

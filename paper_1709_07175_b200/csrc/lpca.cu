@@ -424,7 +424,7 @@ struct Panel {
   index_t ld = 0;
   index_t ldt = 0;
   // pair fp16 path: U^T as fp16 hi/lo planes [ld][ldt16] scaled per (column,
-  // 128-row block), inverse scales uinv[block][ld] (tc_pair.cuh)
+  // kUScaleRows-row block), inverse scales uinv[block][ld] (tc_pair.cuh)
   __half* h16hi = nullptr;
   __half* h16lo = nullptr;
   float* uinv = nullptr;
@@ -826,7 +826,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       u.ldt16 = round_up(mm, 8);
       u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
       u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
-      u.uinv = ctx.get<float>("u.inv", ceil_div(mm, 128) * u.ld);
+      u.uinv = ctx.get<float>("u.inv", ceil_div(mm, kUScaleRows) * u.ld);
     } else if (tc) {
       u.ldt = planes_ld(m);
       u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
@@ -1239,7 +1239,7 @@ lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& 
         u.ldt16 = round_up(x.m, 8);
         u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
         u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
-        u.uinv = ctx.get<float>("u.inv", ceil_div(x.m, 128) * u.ld);
+        u.uinv = ctx.get<float>("u.inv", ceil_div(x.m, kUScaleRows) * u.ld);
       } else if (tc) {
         u.ldt = planes_ld(x.m);
         u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);

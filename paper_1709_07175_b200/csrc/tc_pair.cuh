@@ -73,7 +73,7 @@ struct PairArgs {
   float* out_lo;
   __half* uh;        // fp16 planes of OUT^T [npad][ldh] with block scales (nullable)
   __half* ul;
-  float* uinv;       // [ceil(m/128)][npad] inverse block scales of uh/ul
+  float* uinv;       // [ceil(m/256)][npad] inverse block scales of uh/ul
   int ldh;
   // X^T U: U^T block inverse scales (fp16), partial output part[chunk][j * l + r]
   const float* uinv_in;
@@ -258,9 +258,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* aempty = conv + AS;
   uint64_t* tfull = aempty + AS;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xch = tempty + 2;  // [2] U^T block-maximum exchange with the peer (XW fp16 planes)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima / run scales
   float* rsc = red + 5 * a.npad;  // after red [4][npad] + gsc [npad]: [kRscRing runs][128] inverse A-row scales
+  float* xbuf = rsc + kRscRing * kBM;  // [2][npad] the peer's column maxima (written by the peer)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);
@@ -280,6 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8);
+      mbar_init(&xch[b], 1);
     }
     fence_barrier_init();
     tma_prefetch(&tmx);
@@ -507,19 +510,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lacc = lane_base + static_cast<uint32_t>(a.nrb * a.npad);
     const float xinv = 1.0f / xs;
     int rc = 0;
+    int xit = 0;  // planes16 items done (xch / xbuf parity)
     for (int item = pair; item < a.items; item += npairs) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
       const int runs = (k1 - k0 + run_k - 1) / run_k;
       const int row = t0 + static_cast<int>(rank) * kBM + q * 32 + lane;  // XW: X row; XTU: X column
       const bool to_planes16 = kMode == kXW && a.uh != nullptr;
-      // X^T U, fp16: each run's rows form one 128-row block of U^T scales. The
+      // X^T U, fp16: each run's rows form one 256-row block of U^T scales. The
       // next run's scales are fetched into registers while this run is folded
       // and staged in this warp's row of red[] (broadcast reads).
       float* runsc = red + q * a.npad;
       float nxt[8];
       auto fetch_scales = [&](int r) {
-        const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / 128) * a.uinv_ld;
+        const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / kUScaleRows) * a.uinv_ld;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = lane + 32 * j;
@@ -636,10 +640,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
       }
       if (to_planes16) {
-        // OUT^T as fp16 hi/lo planes scaled per (column, 128-row block):
-        // pass 1 reduces each warp's column maxima of the raw accumulator,
-        // pass 1.5 turns the block maxima into per-column multipliers
-        // g[c] = f[c] s[c] (f = the accumulator's own unscale), pass 2 splits.
+        // OUT^T as fp16 hi/lo planes scaled per (column, 256-row block = this
+        // pair's item): pass 1 reduces each warp's column maxima of the raw
+        // accumulator; pass 1.5 combines the four warps, swaps the CTA's
+        // maxima with the peer (st.async into the peer's xbuf, completing the
+        // peer's xch transaction) and turns the pair maxima into per-column
+        // multipliers g[c] = f[c] s[c] (f = the accumulator's own unscale),
+        // identical in both CTAs; pass 2 splits.
         tc_fence_after();
         const bool valid = row < a.m;
         float* gsc = red + 4 * a.npad;
@@ -652,15 +659,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if ((lane & 1) == 0) red[q * a.npad + c0 + warp_max16_col(lane)] = mx;
         }
         epi_bar();
-        const int blk = (t0 + static_cast<int>(rank) * kBM) / kBM;
-        // (a CTA whose 128 rows all lie past m owns no block: writing its
-        // scales would run past the [ceil(m/128)][npad] array)
-        for (int c = q * 32 + lane; c < a.npad && blk * kBM < a.m; c += 128) {
+        const int xb = xit & 1;
+        if (q == 0 && lane == 0) mbar_expect_tx(&xch[xb], static_cast<uint32_t>(a.npad) * 4);
+        for (int c = q * 32 + lane; c < a.npad; c += 128) {
+          const float mloc = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c]));
+          gsc[c] = mloc;
+          st_async_f32(map_to_rank(smem_u32(&xbuf[xb * a.npad + c]), rank ^ 1u), mloc,
+                       map_to_rank(smem_u32(&xch[xb]), rank ^ 1u));
+        }
+        mbar_wait(&xch[xb], (xit >> 1) & 1, 6);
+        ++xit;
+        const int blk = t0 / kUScaleRows;
+        // (a pair whose rows all lie past m owns no block: writing its scales
+        // would run past the [ceil(m/256)][npad] array)
+        for (int c = q * 32 + lane; c < a.npad; c += 128) {
           const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
-          const float mx = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c])) * f;
+          const float mx = fmaxf(gsc[c], xbuf[xb * a.npad + c]) * f;
           const float sc = pow2_scale_for(mx);
           gsc[c] = f * sc;
-          a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
+          if (rank == 0 && blk * kUScaleRows < a.m) a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
         }
         epi_bar();
         for (int c0 = 0; c0 < a.npad; c0 += 16) {

@@ -221,6 +221,40 @@ lpca_status lpca_distance_preservation(lpca_ctx* ctx, const lpca_matrix_view* x,
                                        int64_t* pair_i, int64_t* pair_j, double* original, double* reduced_a,
                                        double* reduced_b, double* max_violation, double* max_discrepancy);
 
+/* Residual norms of a projection (metrics.cpp:148-308, metrics.hpp:31-50).
+ * reconstruction_error: X - P X for P the projector onto range(U), U the m x l
+ * sketch (column-major fp64, host or device). route LPCA_ROUTE_QR uses an
+ * orthonormal basis of U (the reference's householder_qr; here shifted
+ * CholeskyQR3, equal up to roundoff), LPCA_ROUTE_LAZY the Cholesky of U^T U
+ * (RankDeficiencyError with the pivot index when it is not positive definite).
+ * The Frobenius error uses ||X||_F^2 - ||P X||_F^2; the spectral error runs the
+ * reference's power iteration (seeded start vector, relative 1e-8, abs_tol
+ * 1e-14 ||X||_F, ConvergenceError after 10000 steps). With with_bound, l >= k + 2
+ * and max(m, n) <= densify_limit, sigma_{k+1} of X and bound_value are attached
+ * (sigma from the eigenvalues of the smaller Gram of X, not a Jacobi SVD).
+ * row_space_reconstruction_error: X - X V V^T for an orthonormal V (n x k). */
+typedef enum { LPCA_ROUTE_QR = 0, LPCA_ROUTE_LAZY = 1 } lpca_residual_route;
+typedef struct {
+  double spectral_error;
+  double frobenius_error;
+  int32_t has_sigma_k_plus_1;
+  int32_t has_bound;
+  double sigma_k_plus_1;
+  double bound;
+} lpca_recon_report;
+lpca_status lpca_reconstruction_error(lpca_ctx* ctx, const lpca_matrix_view* x, const double* u, int64_t u_rows,
+                                      int64_t u_cols, int32_t u_location, int32_t route, int64_t k, int64_t l,
+                                      int32_t with_bound, int64_t densify_limit, lpca_recon_report* out);
+lpca_status lpca_row_space_reconstruction_error(lpca_ctx* ctx, const lpca_matrix_view* x, const double* v,
+                                                int64_t v_rows, int64_t v_cols, int32_t v_location,
+                                                lpca_recon_report* out);
+/* spectral_norm(SparseMatrix / DenseMatrix) (spectral_norm.cpp:23-77): the largest
+ * singular value of X by the same power iteration (no abs_tol). */
+lpca_status lpca_spectral_norm(lpca_ctx* ctx, const lpca_matrix_view* x, double* out);
+/* bound_value (metrics.cpp:136-146): [1 + 4 sqrt(l) / (l - k - 1) sqrt(min(m, n))] sigma;
+ * InvalidArgumentError unless l >= k + 2. Host arithmetic only. */
+lpca_status lpca_bound_value(int64_t m, int64_t n, int64_t k, int64_t l, double sigma_k_plus_1, double* out);
+
 /* ---- kernel-level exports (proj/core/include/lazypca/kernels.hpp:17-36,
  *      truncated_svd.hpp:24, tridiag_eigh.hpp:8). Host or device operands; fp64
  *      column-major unless stated; X views as above. ------------------------- */

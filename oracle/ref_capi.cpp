@@ -28,6 +28,7 @@
 #include "lazypca/tridiag_eigh.hpp"
 #include "lazypca/truncated_svd.hpp"
 #include "lazypca/metrics.hpp"
+#include "lazypca/spectral_norm.hpp"
 
 using namespace lazypca;
 
@@ -303,6 +304,41 @@ int ref_householder_qr(const double* a, std::int64_t m, std::int64_t l, double* 
 // chordal_distance (proj/core/src/metrics.cpp:123-136) on two n x k bases.
 int ref_chordal(const double* v1, const double* v2, std::int64_t n, std::int64_t k, double* out) {
   return guarded([&] { *out = chordal_distance(dense_from(v1, n, k), dense_from(v2, n, k)); });
+}
+
+// reconstruction_error (proj/core/src/metrics.cpp:148-259) on dense row-major X
+// and a column-major m x l sketch: out = {spectral, frobenius, sigma_{k+1}, bound},
+// flags = {has sigma, has bound}.
+int ref_reconstruction_error(int route, const void* x, int dtype, std::int64_t m, std::int64_t n,
+                             const double* u, std::int64_t l, std::int64_t k, int with_bound,
+                             std::int64_t densify_limit, double* out, int* flags) {
+  return guarded([&] {
+    const ReconstructionErrorReport r =
+        reconstruction_error(csc_any(x, dtype, m, n), dense_from(u, m, l),
+                             route == 0 ? ResidualRoute::qr : ResidualRoute::lazy, k, l, with_bound != 0,
+                             densify_limit);
+    out[0] = r.spectral_error;
+    out[1] = r.frobenius_error;
+    out[2] = r.sigma_k_plus_1.value_or(0.0);
+    out[3] = r.bound.value_or(0.0);
+    flags[0] = r.sigma_k_plus_1.has_value();
+    flags[1] = r.bound.has_value();
+  });
+}
+
+// row_space_reconstruction_error (metrics.cpp:261-308), V n x k column-major.
+int ref_row_space_reconstruction_error(const void* x, int dtype, std::int64_t m, std::int64_t n, const double* v,
+                                       std::int64_t k, double* out) {
+  return guarded([&] {
+    const ReconstructionErrorReport r = row_space_reconstruction_error(csc_any(x, dtype, m, n), dense_from(v, n, k));
+    out[0] = r.spectral_error;
+    out[1] = r.frobenius_error;
+  });
+}
+
+// spectral_norm(SparseMatrix) (proj/core/src/spectral_norm.cpp:70-77).
+int ref_spectral_norm(const void* x, int dtype, std::int64_t m, std::int64_t n, double* out) {
+  return guarded([&] { *out = spectral_norm(csc_any(x, dtype, m, n)); });
 }
 
 }  // extern "C"

@@ -192,6 +192,35 @@ def chordal(v1: np.ndarray, v2: np.ndarray) -> float:
     return out.value
 
 
+def reconstruction_error(route: int, x: np.ndarray, u: np.ndarray, k: int, l: int, with_bound: bool = False,
+                         densify_limit: int = 2000):
+    """(spectral, frobenius, sigma_{k+1} or None, bound or None); route 0 = qr, 1 = lazy."""
+    x, dt = _x(x)
+    u = np.asfortranarray(u, dtype=np.float64)
+    out = np.zeros(4)
+    flags = np.zeros(2, dtype=np.int32)
+    _chk(load().ref_reconstruction_error(C.c_int(route), _p(x), C.c_int(dt), C.c_int64(x.shape[0]),
+                                         C.c_int64(x.shape[1]), _p(u), C.c_int64(l), C.c_int64(k),
+                                         C.c_int(int(with_bound)), C.c_int64(densify_limit), _p(out), _p(flags)))
+    return out[0], out[1], (out[2] if flags[0] else None), (out[3] if flags[1] else None)
+
+
+def row_space_reconstruction_error(x: np.ndarray, v: np.ndarray):
+    x, dt = _x(x)
+    v = np.asfortranarray(v, dtype=np.float64)
+    out = np.zeros(2)
+    _chk(load().ref_row_space_reconstruction_error(_p(x), C.c_int(dt), C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
+                                                   _p(v), C.c_int64(v.shape[1]), _p(out)))
+    return out[0], out[1]
+
+
+def spectral_norm(x: np.ndarray) -> float:
+    x, dt = _x(x)
+    out = C.c_double()
+    _chk(load().ref_spectral_norm(_p(x), C.c_int(dt), C.c_int64(x.shape[0]), C.c_int64(x.shape[1]), C.byref(out)))
+    return out.value
+
+
 def cpu_threads() -> int:
     return len(os.sched_getaffinity(0))
 

@@ -13,7 +13,8 @@ from .api import (  # noqa: F401
     reduce, reduce_lazy_spca, reduce_lazy_spca_streaming, reduce_rp, reduce_spca, reduce_spca_streaming,
     reducer_method_from_string, regenerate, RowBlock, RowBlockStream, SliceRowBlockStream, split_rows,
     load_map_file, read_map_file, save_map_file, write_map_file, chordal_distance, distance_preservation,
-    DistancePreservationReport,
+    DistancePreservationReport, ReconstructionErrorReport, ResidualRoute, bound_value, reconstruction_error,
+    row_space_reconstruction_error, spectral_norm,
     set_thread_count, sketch_f32, spmm, synth_lowrank, thread_count, to_string, tridiag_eigh,
     truncated_svd_via_gram,
 )

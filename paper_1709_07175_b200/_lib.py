@@ -46,6 +46,12 @@ class Timings(C.Structure):
 NEXT_BLOCK_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(MatrixView), C.POINTER(C.c_int64))
 
 
+class ReconReport(C.Structure):
+    _fields_ = [("spectral_error", C.c_double), ("frobenius_error", C.c_double),
+                ("has_sigma_k_plus_1", C.c_int32), ("has_bound", C.c_int32),
+                ("sigma_k_plus_1", C.c_double), ("bound", C.c_double)]
+
+
 class MapInfo(C.Structure):
     _fields_ = [
         ("method", C.c_int32), ("reserved", C.c_int32),
@@ -90,6 +96,12 @@ SIGNATURES = {
     "lpca_map_create": (I32, [P, C.POINTER(MapInfo), P, P, PP]),
     "lpca_map_destroy": (I32, [P]),
     "lpca_chordal_distance": (I32, [P, P, I64, I64, P, I64, I64, I32, DP]),
+    "lpca_reconstruction_error": (I32, [P, C.POINTER(MatrixView), P, I64, I64, I32, I32, I64, I64, I32, I64,
+                                        C.POINTER(ReconReport)]),
+    "lpca_row_space_reconstruction_error": (I32, [P, C.POINTER(MatrixView), P, I64, I64, I32,
+                                                  C.POINTER(ReconReport)]),
+    "lpca_spectral_norm": (I32, [P, C.POINTER(MatrixView), DP]),
+    "lpca_bound_value": (I32, [I64, I64, I64, I64, D, DP]),
     "lpca_distance_preservation": (I32, [P, C.POINTER(MatrixView), P, P, I64, C.c_uint64, C.POINTER(C.c_int64), P, P,
                                          P, P, P, DP, DP]),
     "lpca_map_save": (I32, [P, C.c_char_p]),

@@ -555,6 +555,83 @@ def distance_preservation(x, map_a: "ReductionMap", map_b: "ReductionMap" = None
     return DistancePreservationReport(pi[:n], pj[:n], o[:n], ra[:n], rb[:n], viol.value, gap.value)
 
 
+class ResidualRoute(enum.IntEnum):
+    """metrics.hpp:28: the orthonormal-basis route (Q Q^T X) or the raw sketch (U (U^T U)^{-1} U^T X)."""
+    qr = 0
+    lazy = 1
+
+
+def _f64_operand(a):
+    """(pointer, location, shape, keepalive) of a column-major fp64 operand: a host
+    array (copied Fortran-order) or a CUDA tensor (its transpose must be contiguous)."""
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        import torch
+        t = a.to(torch.float64)
+        if not t.t().is_contiguous():
+            t = t.t().contiguous().t()
+        torch.cuda.synchronize()
+        return C.c_void_p(t.data_ptr()), L.LPCA_DEVICE, tuple(t.shape), t
+    h = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    return (h.ctypes.data if h.size else None), L.LPCA_HOST, h.shape, h
+
+
+@dataclass
+class ReconstructionErrorReport:
+    """metrics.hpp:31-36. sigma_k_plus_1 / bound are None when not computed."""
+    spectral_error: float
+    frobenius_error: float
+    sigma_k_plus_1: float = None
+    bound: float = None
+
+
+def _report(r) -> ReconstructionErrorReport:
+    return ReconstructionErrorReport(r.spectral_error, r.frobenius_error,
+                                     r.sigma_k_plus_1 if r.has_sigma_k_plus_1 else None,
+                                     r.bound if r.has_bound else None)
+
+
+def reconstruction_error(x, u, route: ResidualRoute, k: int, l: int, with_bound: bool = False,
+                         densify_limit: int = 2000, ctx=None) -> ReconstructionErrorReport:
+    """reconstruction_error (metrics.cpp:148-259) on the device: ||X - P X|| for P
+    the projector onto range(U), U the m x l sketch (host array or CUDA tensor)."""
+    ctx = ctx or default_context()
+    vw = _View(x)
+    ub, loc, shape, _keep = _f64_operand(u)
+    out = L.ReconReport()
+    _check(ctx.lib.lpca_reconstruction_error(ctx.h, C.byref(vw.view), ub, shape[0], shape[1], loc, int(route), int(k),
+                                             int(l), int(bool(with_bound)), int(densify_limit), C.byref(out)))
+    return _report(out)
+
+
+def row_space_reconstruction_error(x, v, ctx=None) -> ReconstructionErrorReport:
+    """row_space_reconstruction_error (metrics.cpp:261-308): ||X - X V V^T|| for an
+    orthonormal V (n x k)."""
+    ctx = ctx or default_context()
+    vw = _View(x)
+    vb, loc, shape, _keep = _f64_operand(v)
+    out = L.ReconReport()
+    _check(ctx.lib.lpca_row_space_reconstruction_error(ctx.h, C.byref(vw.view), vb, shape[0], shape[1], loc,
+                                                       C.byref(out)))
+    return _report(out)
+
+
+def spectral_norm(x, ctx=None) -> float:
+    """spectral_norm (spectral_norm.cpp:23-77): largest singular value of X by the
+    reference's power iteration."""
+    ctx = ctx or default_context()
+    vw = _View(x)
+    out = C.c_double()
+    _check(ctx.lib.lpca_spectral_norm(ctx.h, C.byref(vw.view), C.byref(out)))
+    return out.value
+
+
+def bound_value(m: int, n: int, k: int, l: int, sigma_k_plus_1: float) -> float:
+    """bound_value (metrics.cpp:136-146)."""
+    out = C.c_double()
+    _check(L.load().lpca_bound_value(int(m), int(n), int(k), int(l), float(sigma_k_plus_1), C.byref(out)))
+    return out.value
+
+
 # ---- map files (reducer.cpp:355-412), byte-compatible with the reference ----------
 def save_map_file(map_: "ReductionMap", path: str) -> None:
     """save_map_file: one-line JSON header + V as a dense MatrixMarket array."""

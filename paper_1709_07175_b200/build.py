@@ -21,7 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
-SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu", "eigh.cu", "sparse.cu", "metrics.cu"]
+SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu", "eigh.cu", "sparse.cu", "metrics.cu",
+           "spectral.cu"]
 HOST_SOURCES = ["mapio.cpp"]  # host-only C++ (g++)
 CXX = os.environ.get("CXX", "g++")
 

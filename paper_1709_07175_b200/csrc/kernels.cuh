@@ -78,6 +78,30 @@ void launch_pair_distances(cudaStream_t s, int dtype, const void* x, index_t ld,
                            const std::int32_t* ci, const double* rv, const double* ya, const double* yb, index_t k,
                            const std::int64_t* pi, const std::int64_t* pj, index_t pairs, double* orig, double* da,
                            double* db);
+// ---- residual-norm metrics (spectral.cu; metrics.cpp:148-308) ------------------
+// y (m) = X v: dense row-major dtype (x, ld) or CSR (rp, ci, rv).
+void launch_matvec(cudaStream_t s, int dtype, const void* x, index_t ld, index_t m, index_t n, const std::int64_t* rp,
+                   const std::int32_t* ci, const double* rv, const double* v, double* y);
+// y (n) = X^T t: dense (partials in part, matvec_t_chunks(m, n) x n) or CSC.
+index_t matvec_t_chunks(index_t m, index_t n);
+void launch_matvec_t(cudaStream_t s, int dtype, const void* x, index_t ld, index_t m, index_t n,
+                     const std::int64_t* cp, const std::int32_t* ri, const double* cv, const double* t, double* part,
+                     double* y);
+// out (l) = U^T t for U m x l column-major (ld ldu); part basis_t_chunks(m) x l.
+index_t basis_t_chunks(index_t m);
+void launch_basis_t(cudaStream_t s, const double* u, index_t ldu, index_t m, index_t l, const double* t,
+                    double* part, double* out);
+// y (m) = t - U sv.
+void launch_basis_sub(cudaStream_t s, const double* u, index_t ldu, index_t m, index_t l, const double* sv,
+                      const double* t, double* y);
+// part[0 .. sumsq_blocks(rows*cols)) = partial sums of squares of a (rows x cols, ld).
+index_t sumsq_blocks(index_t count);
+void launch_sumsq(cudaStream_t s, int dtype, const void* a, index_t ld, index_t rows, index_t cols, double* part);
+// dense row-major m x n fp64 from CSR.
+void launch_csr_to_dense(cudaStream_t s, index_t m, index_t n, const std::int64_t* rp, const std::int32_t* ci,
+                         const double* rv, double* out);
+// out = Rinv (Rinv^T sv): (U^T U)^{-1} sv with Rinv = L^{-T} from launch_chol_inverse.
+void launch_chol_solve(cudaStream_t s, const double* rinv, index_t l, const double* sv, double* tmp, double* out);
 // y += x (fp64), the streaming reducers' running F and U^T U (gemm_t_add, kernels.cpp:95-113).
 void launch_add_f64(cudaStream_t s, const double* x, double* y, index_t count);
 // out[idx] = sum_c part[c][idx], c ascending (fixed order; no float atomics).

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -241,6 +242,7 @@ struct DevX {
   const std::int64_t* cp = nullptr;
   const std::int32_t* ri = nullptr;
   const double* cv = nullptr;
+  index_t nnz = 0;
   bool sparse() const { return rp != nullptr; }
 };
 
@@ -353,6 +355,7 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
       d.cp = cp;
       d.ri = ri;
       d.cv = cv;
+      d.nnz = nnz;
       return d;
     }
     auto* cp = ctx.get<std::int64_t>(std::string(slot) + ".ptr", x->cols + 1);
@@ -1840,6 +1843,347 @@ lpca_status lpca_distance_preservation(lpca_ctx* ctx, const lpca_matrix_view* x,
     *n_pairs = np;
     if (max_violation) *max_violation = worst_violation;
     if (max_discrepancy) *max_discrepancy = worst_gap;
+  });
+}
+
+namespace {
+
+// ---- residual norms (metrics.cpp:148-308, spectral_norm.cpp:23-57) ----------
+// Linear operator on the device, seen through products (SpectralOperator,
+// spectral_norm.hpp:12-17): apply maps cols -> rows, apply_t rows -> cols.
+struct DevOperator {
+  index_t rows = 0, cols = 0;
+  std::function<void(const double*, double*)> apply, apply_t;
+};
+
+// sqrt(sum of squares) of a device vector, partials summed on the host in order.
+double dev_norm2(lpca_ctx& ctx, const double* v, index_t count) {
+  const index_t g = sumsq_blocks(count);
+  double* part = ctx.get<double>("sn.part", g);
+  launch_sumsq(ctx.stream, 8, v, count, 1, count, part);
+  LPCA_LAUNCHED(ctx);
+  std::vector<double> h(static_cast<std::size_t>(g));
+  LPCA_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * g, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  double s = 0.0;
+  for (double x : h) s += x;
+  return std::sqrt(s);
+}
+
+double dev_sumsq_x(lpca_ctx& ctx, const DevX& x) {
+  const index_t count = x.sparse() ? x.nnz : x.m * x.n;
+  const index_t g = sumsq_blocks(count);
+  double* part = ctx.get<double>("sn.xpart", g);
+  if (x.sparse())
+    launch_sumsq(ctx.stream, 8, x.rv, count, 1, count, part);
+  else
+    launch_sumsq(ctx.stream, x.dtype, x.p, x.ld, x.m, x.n, part);
+  LPCA_LAUNCHED(ctx);
+  std::vector<double> h(static_cast<std::size_t>(g));
+  LPCA_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * g, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  double s = 0.0;
+  for (double v : h) s += v;
+  return s;
+}
+
+// spectral_norm (spectral_norm.cpp:23-57): power iteration on A^T A from the
+// reference's seeded start vector; the iterates stay on the device, the two
+// norms per step come back to the host for the same tests in the same order.
+double dev_spectral_norm(lpca_ctx& ctx, const DevOperator& op, double abs_tol) {
+  if (op.rows < 1 || op.cols < 1) throw Error(kInvalidArgument, "spectral_norm: operator must be non-empty");
+  Xoshiro rng(0x5eed0f0e57a7ULL);
+  std::vector<double> hv(static_cast<std::size_t>(op.cols));
+  for (double& x : hv) x = u64_to_uniform(rng.next()) - 0.5;
+  double vn = 0.0;
+  for (double x : hv) vn += x * x;
+  vn = std::sqrt(vn);
+  if (vn == 0.0) return 0.0;
+  for (double& x : hv) x /= vn;
+  double* v = ctx.get<double>("sn.v", op.cols);
+  double* av = ctx.get<double>("sn.av", op.rows);
+  LPCA_CUDA(cudaMemcpyAsync(v, hv.data(), sizeof(double) * op.cols, cudaMemcpyHostToDevice, ctx.stream));
+  constexpr int kMaxIters = 10000;
+  constexpr double kRelTol = 1e-8;
+  double estimate = 0.0, gap = 0.0;
+  for (int it = 0; it < kMaxIters; ++it) {
+    op.apply(v, av);
+    const double sigma = dev_norm2(ctx, av, op.rows);
+    if (sigma == 0.0) return 0.0;
+    if (sigma <= abs_tol) return sigma;
+    gap = std::abs(sigma - estimate);
+    if (it > 0 && gap <= kRelTol * sigma + abs_tol) return sigma;
+    estimate = sigma;
+    op.apply_t(av, v);
+    const double wn = dev_norm2(ctx, v, op.cols);
+    if (wn == 0.0) return sigma;
+    launch_scale_f64(ctx.stream, v, v, op.cols, 1.0 / wn);
+    LPCA_LAUNCHED(ctx);
+  }
+  throw Error(kConvergence, "spectral_norm: estimate gap " + std::to_string(gap) + " still above relative " +
+                                std::to_string(kRelTol) + " after " + std::to_string(kMaxIters) + " iterations",
+              -1, gap);
+}
+
+// X v and X^T t on a staged X (dense dtype or CSR/CSC)
+void x_apply(lpca_ctx& ctx, const DevX& x, const double* v, double* y) {
+  launch_matvec(ctx.stream, x.dtype, x.p, x.ld, x.m, x.n, x.rp, x.ci, x.rv, v, y);
+  LPCA_LAUNCHED(ctx);
+}
+void x_apply_t(lpca_ctx& ctx, const DevX& x, const double* t, double* y) {
+  double* part = x.sparse() ? nullptr : ctx.get<double>("sn.mtpart", matvec_t_chunks(x.m, x.n) * x.n);
+  launch_matvec_t(ctx.stream, x.dtype, x.p, x.ld, x.m, x.n, x.cp, x.ri, x.cv, t, part, y);
+  LPCA_LAUNCHED(ctx);
+}
+
+// F (l x n, column-major) = B^T X for a row-major m x l basis (gemm_t paths of
+// lpca_gemm_t); x is fp64 (widened) or sparse.
+void basis_gemm_t(lpca_ctx& ctx, const DevX& x, const double* brow, index_t l, double* f) {
+  if (l * x.n == 0) return;
+  if (x.m > 0 && x.sparse()) {
+    launch_gemm_t_csc(ctx.stream, x.n, x.cp, x.ri, x.cv, brow, l, l, f, false);
+  } else if (x.m > 0) {
+    launch_utx_simt<double>(ctx.stream, brow, l, static_cast<const double*>(x.p), x.ld, x.m, l, x.n,
+                            round_up(x.m, 16), f, true);
+  } else {
+    launch_zero(ctx.stream, f, sizeof(double) * l * x.n);
+  }
+  LPCA_LAUNCHED(ctx);
+}
+
+double dev_sumsq(lpca_ctx& ctx, const double* a, index_t count) {
+  const double r = dev_norm2(ctx, a, count);
+  return r * r;
+}
+
+// sigma_{k+1} of X from the eigenvalues of its smaller Gram (the reference runs
+// a one-sided Jacobi SVD on the densified X, metrics.cpp:250-256).
+std::vector<double> dev_singular_values(lpca_ctx& ctx, const DevX& x) {
+  const index_t m = x.m, n = x.n;
+  double* dense = ctx.get<double>("rb.dense", m * n);  // row-major m x n
+  if (x.sparse()) {
+    launch_csr_to_dense(ctx.stream, m, n, x.rp, x.ci, x.rv, dense);
+  } else {
+    LPCA_CUDA(cudaMemcpy2DAsync(dense, sizeof(double) * n, x.p, sizeof(double) * x.ld, sizeof(double) * n, m,
+                                cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+  LPCA_LAUNCHED(ctx);
+  const index_t w = m < n ? m : n;
+  double* g = ctx.get<double>("rb.g", w * w);
+  if (n <= m) {  // X^T X: the row-major X is an n x m column-major F
+    launch_gram_fast(ctx.stream, dense, n, m, g, ctx.get<double>("rb.gpart", gram_fast_chunks(n, m) * n * n));
+  } else {  // X X^T: transpose to an m x n column-major F first
+    double* xt = ctx.get<double>("rb.xt", m * n);
+    launch_transpose(ctx.stream, 8, dense, n, n, m, xt, m);
+    launch_gram_fast(ctx.stream, xt, m, n, g, ctx.get<double>("rb.gpart", gram_fast_chunks(m, n) * m * m));
+  }
+  LPCA_LAUNCHED(ctx);
+  double* evals = ctx.get<double>("rb.evals", w);
+  double* evecs = ctx.get<double>("rb.evecs", w * w);
+  int* st = ctx.get<int>("rb.st", 2);
+  double* gap = ctx.get<double>("rb.gap", 1);
+  eigh_dev(ctx, g, w, evals, evecs, st, gap, 0);
+  std::vector<double> lam(static_cast<std::size_t>(w));
+  LPCA_CUDA(cudaMemcpyAsync(lam.data(), evals, sizeof(double) * w, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  for (double& v : lam) v = std::sqrt(v > 0.0 ? v : 0.0);
+  return lam;
+}
+
+double bound_value_host(index_t m, index_t n, index_t k, index_t l, double sigma) {
+  if (k < 1 || l < k + 2)
+    throw Error(kInvalidArgument, "bound_value: needs l >= k + 2 (got k = " + S(k) + ", l = " + S(l) + ")");
+  const double minmn = static_cast<double>(m < n ? m : n);
+  const double factor = 1.0 + 4.0 * std::sqrt(static_cast<double>(l)) / static_cast<double>(l - k - 1) * std::sqrt(minmn);
+  return factor * sigma;
+}
+
+void fill_report(lpca_recon_report* out, double spectral, double frob) {
+  *out = lpca_recon_report{};
+  out->spectral_error = spectral;
+  out->frobenius_error = frob;
+}
+
+}  // namespace
+
+lpca_status lpca_reconstruction_error(lpca_ctx* ctx, const lpca_matrix_view* x, const double* u, int64_t u_rows,
+                                      int64_t u_cols, int32_t u_location, int32_t route, int64_t k, int64_t l,
+                                      int32_t with_bound, int64_t densify_limit, lpca_recon_report* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (!u && u_rows * u_cols > 0)) throw Error(kInvalidArgument, "null argument");
+    if (route != LPCA_ROUTE_QR && route != LPCA_ROUTE_LAZY)
+      throw Error(kInvalidArgument, "reconstruction_error: route must be LPCA_ROUTE_QR or LPCA_ROUTE_LAZY");
+    const DevX dx = stage_x_f64(*ctx, x);
+    const index_t m = dx.m, n = dx.n;
+    if (u_rows != m)
+      throw Error(kDimension, "reconstruction_error: U has " + S(u_rows) + " rows but X has " + S(m));
+    if (u_cols != l) throw Error(kDimension, "reconstruction_error: U has " + S(u_cols) + " columns but l = " + S(l));
+    lpca_ctx& c = *ctx;
+    const double* ud = stage_f64(c, u, m * l, u_location, "re.u");
+    const double xf2 = dev_sumsq_x(c, dx);
+    double* urow = c.get<double>("re.urow", m * l);  // row-major m x l (an l x m column-major F)
+    if (m * l > 0) {
+      launch_transpose(c.stream, 8, ud, m, m, l, urow, l);
+      LPCA_LAUNCHED(c);
+    }
+    double* f = c.get<double>("re.f", l * n);
+    double* rinv = nullptr;
+    const double* basis = ud;  // column-major m x l: U (lazy) or Q (qr)
+    if (route == LPCA_ROUTE_QR) {
+      orth_rows(c, urow, l, m);  // Q (row-major) = shifted CholeskyQR3 of U
+      double* qcol = c.get<double>("re.q", m * l);
+      if (m * l > 0) {
+        launch_transpose(c.stream, 8, urow, l, l, m, qcol, m);
+        LPCA_LAUNCHED(c);
+      }
+      basis = qcol;
+      basis_gemm_t(c, dx, urow, l, f);  // Q^T X
+    } else {
+      double* g = c.get<double>("re.g", l * l);
+      launch_gram_fast(c.stream, urow, l, m, g, c.get<double>("gram.part", gram_fast_chunks(l, m) * l * l));
+      LPCA_LAUNCHED(c);
+      rinv = c.get<double>("re.rinv", l * l);
+      int* st = c.get<int>("re.st", 1);
+      launch_chol_inverse(c.stream, g, l, rinv, c.get<double>("re.lm", l * l), st);
+      LPCA_LAUNCHED(c);
+      int h = 0;
+      LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      LPCA_CUDA(cudaStreamSynchronize(c.stream));
+      if (h != 0)
+        throw Error(kRankDeficiency, "cholesky: pivot " + S(h - 1) + " is not positive definite", h - 1);
+      basis_gemm_t(c, dx, urow, l, f);                                       // U^T X
+      launch_apply_rinv_t(c.stream, rinv, l, f, n, c.get<double>("re.tmp", l * n));  // L^{-1} U^T X
+      LPCA_LAUNCHED(c);
+    }
+    const double pf2 = dev_sumsq(c, f, l * n);
+    const double frob = std::sqrt(std::max(0.0, xf2 - pf2));
+    // residual operator (I - P) X and its transpose
+    double* t = c.get<double>("re.t", m);
+    double* sv = c.get<double>("re.s", l > 0 ? l : 1);
+    double* s2 = c.get<double>("re.s2", l > 0 ? l : 1);
+    double* stmp = c.get<double>("re.stmp", l > 0 ? l : 1);
+    double* bpart = c.get<double>("re.bpart", basis_t_chunks(m) * (l > 0 ? l : 1));
+    auto project_out = [&](const double* in, double* y) {  // y = in - P in (m-vectors)
+      launch_basis_t(c.stream, basis, m, m, l, in, bpart, sv);
+      LPCA_LAUNCHED(c);
+      const double* coef = sv;
+      if (rinv) {
+        launch_chol_solve(c.stream, rinv, l, sv, stmp, s2);
+        LPCA_LAUNCHED(c);
+        coef = s2;
+      }
+      launch_basis_sub(c.stream, basis, m, m, l, coef, in, y);
+      LPCA_LAUNCHED(c);
+    };
+    DevOperator op;
+    op.rows = m;
+    op.cols = n;
+    op.apply = [&](const double* in, double* y) {
+      x_apply(c, dx, in, t);
+      project_out(t, y);
+    };
+    op.apply_t = [&](const double* in, double* y) {
+      project_out(in, t);
+      x_apply_t(c, dx, t, y);
+    };
+    const double spectral = dev_spectral_norm(c, op, 1e-14 * std::sqrt(xf2));
+    fill_report(out, spectral, frob);
+    if (with_bound && l >= k + 2 && std::max(m, n) <= densify_limit && m > 0 && n > 0) {
+      const std::vector<double> sv_x = dev_singular_values(c, dx);
+      if (static_cast<index_t>(sv_x.size()) > k && k >= 0) {
+        out->has_sigma_k_plus_1 = 1;
+        out->sigma_k_plus_1 = sv_x[static_cast<std::size_t>(k)];
+        out->has_bound = 1;
+        out->bound = bound_value_host(m, n, k, l, out->sigma_k_plus_1);
+      }
+    }
+  });
+}
+
+lpca_status lpca_row_space_reconstruction_error(lpca_ctx* ctx, const lpca_matrix_view* x, const double* v,
+                                                int64_t v_rows, int64_t v_cols, int32_t v_location,
+                                                lpca_recon_report* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (!v && v_rows * v_cols > 0)) throw Error(kInvalidArgument, "null argument");
+    const DevX dx = stage_x_f64(*ctx, x);
+    const index_t m = dx.m, n = dx.n, kd = v_cols;
+    if (n != v_rows)
+      throw Error(kDimension, "row_space_reconstruction_error: X has " + S(n) + " columns but V has " + S(v_rows) +
+                                  " rows");
+    lpca_ctx& c = *ctx;
+    const double* vd = stage_f64(c, v, n * kd, v_location, "rs.v");
+    // check_orthonormal (metrics.cpp:21-31) on V^T V
+    double* g = c.get<double>("rs.g", kd * kd > 0 ? kd * kd : 1);
+    launch_atb(c.stream, vd, n, kd, vd, kd, g);
+    LPCA_LAUNCHED(c);
+    std::vector<double> hg(static_cast<std::size_t>(kd * kd));
+    if (!hg.empty()) LPCA_CUDA(cudaMemcpyAsync(hg.data(), g, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost, c.stream));
+    LPCA_CUDA(cudaStreamSynchronize(c.stream));
+    double worst = 0.0;
+    for (index_t j = 0; j < kd; ++j)
+      for (index_t i = 0; i < kd; ++i)
+        worst = std::max(worst, std::abs(hg[static_cast<std::size_t>(j * kd + i)] - (i == j ? 1.0 : 0.0)));
+    if (worst > 1e-8 * static_cast<double>(std::max<index_t>(1, kd)))
+      throw Error(kInvalidArgument,
+                  "chordal_distance: basis does not have orthonormal columns (max deviation " + std::to_string(worst) + ")");
+    const double xf2 = dev_sumsq_x(c, dx);
+    // ||X V||_F^2
+    double* xv = c.get<double>("rs.xv", m * kd > 0 ? m * kd : 1);
+    if (m > 0 && kd > 0) {
+      if (dx.sparse()) {
+        double* wt = c.get<double>("rs.vrows", n * kd);
+        launch_transpose(c.stream, 8, vd, n, n, kd, wt, kd);
+        launch_spmm_csr(c.stream, m, dx.rp, dx.ci, dx.rv, wt, kd, kd, xv, 8, 1, m);
+      } else {
+        launch_xw_simt<double, double>(c.stream, static_cast<const double*>(dx.p), m, n, dx.ld, vd, kd, n, xv, 1, m, true);
+      }
+      LPCA_LAUNCHED(c);
+    }
+    const double frob = std::sqrt(std::max(0.0, xf2 - dev_sumsq(c, xv, m * kd)));
+    double* w = c.get<double>("rs.w", n);
+    double* sv = c.get<double>("rs.s", kd > 0 ? kd : 1);
+    double* bpart = c.get<double>("rs.bpart", basis_t_chunks(n) * (kd > 0 ? kd : 1));
+    auto project_out = [&](const double* in, double* y) {  // y = in - V V^T in (n-vectors)
+      launch_basis_t(c.stream, vd, n, n, kd, in, bpart, sv);
+      LPCA_LAUNCHED(c);
+      launch_basis_sub(c.stream, vd, n, n, kd, sv, in, y);
+      LPCA_LAUNCHED(c);
+    };
+    DevOperator op;
+    op.rows = m;
+    op.cols = n;
+    op.apply = [&](const double* in, double* y) {
+      project_out(in, w);
+      x_apply(c, dx, w, y);
+    };
+    op.apply_t = [&](const double* in, double* y) {
+      x_apply_t(c, dx, in, w);
+      project_out(w, y);
+    };
+    fill_report(out, dev_spectral_norm(c, op, 1e-14 * std::sqrt(xf2)), frob);
+  });
+}
+
+lpca_status lpca_spectral_norm(lpca_ctx* ctx, const lpca_matrix_view* x, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out) throw Error(kInvalidArgument, "null argument");
+    const DevX dx = stage_x_f64(*ctx, x);
+    DevOperator op;
+    op.rows = dx.m;
+    op.cols = dx.n;
+    op.apply = [&](const double* in, double* y) { x_apply(*ctx, dx, in, y); };
+    op.apply_t = [&](const double* in, double* y) { x_apply_t(*ctx, dx, in, y); };
+    *out = dev_spectral_norm(*ctx, op, 0.0);
+  });
+}
+
+lpca_status lpca_bound_value(int64_t m, int64_t n, int64_t k, int64_t l, double sigma_k_plus_1, double* out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalidArgument, "null argument");
+    *out = bound_value_host(m, n, k, l, sigma_k_plus_1);
   });
 }
 

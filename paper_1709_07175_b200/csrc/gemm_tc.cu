@@ -411,8 +411,8 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
   if (kHalf && kMode == kXW && a.scan && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
-  if (kHalf && kMode == kXTU && a.run_stages > a.stages)
-    throw Error(kInternal, "tc pair: a U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
+  if (kHalf && kMode == kXTU && a.scan && a.run_stages > a.stages)
+    throw Error(kInternal, "tc pair: a scanned U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
   const size_t smem =
       static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 7 * 4 * a.npad + kRscRing * 4 * kBM;  // + xbuf
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -452,8 +452,16 @@ bool tc_pair_mode() { return pair_mode(); }
 int pair_max_n() { return env_int("LPCA_TC_MAXN", 128); }
 
 // Column slices of a padded width: ceil(wpad / max) slices of equal 16-multiples.
-int slice_width(index_t wpad) {
-  const index_t nsl = ceil_div(wpad, static_cast<index_t>(pair_max_n()));
+// Each slice is one more pass over X; a wide slice costs TMEM double-buffering
+// (above 168 columns one run buffer and one A slot remain). Measured per pass
+// element (c3, c4): X W 112-wide 0.88, 160-wide 1.48, 224-wide 1.57 ps; X^T U
+// 160-wide 1.15x a 112-wide. So X W takes one slice up to 224 columns and
+// 128-column slices above; X^T U takes slices of up to 224. LPCA_TC_MAXN forces
+// one maximum for both.
+int slice_width(index_t wpad, bool xtu) {
+  int mx = xtu ? 224 : (wpad <= 224 ? 224 : 128);
+  if (std::getenv("LPCA_TC_MAXN")) mx = pair_max_n();
+  const index_t nsl = ceil_div(wpad, static_cast<index_t>(mx));
   return static_cast<int>(round_up(ceil_div(wpad, nsl), 16));
 }
 
@@ -464,7 +472,7 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
     throw Error(kInternal, "xw_pair: leading dimensions must be 16-byte multiples");
   if (p.half && !p.winv) throw Error(kInternal, "xw_pair: fp16 encoding needs the W scales");
   const int esz = p.half ? 2 : 4;
-  const int sw = slice_width(p.wpad);
+  const int sw = slice_width(p.wpad, false);
   for (index_t c0 = 0; c0 < p.wpad; c0 += sw) {
     const int wc = static_cast<int>(p.wpad - c0 < sw ? p.wpad - c0 : sw);
     PairArgs a{};
@@ -527,7 +535,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
   index_t rows = 0;
   const index_t chunks = utx_pair_splits(p.m, p.n, num_sms, &rows);
   const int esz = p.half ? 2 : 4;
-  const int sw = slice_width(npad);
+  const int sw = slice_width(npad, true);
   for (index_t c0 = 0; c0 < npad; c0 += sw) {
     const int wc = static_cast<int>(npad - c0 < sw ? npad - c0 : sw);
     PairArgs a{};

@@ -337,58 +337,129 @@ __global__ void sign_canon_kernel(double* v, index_t n, double* ut, index_t l) {
     for (index_t i = threadIdx.x; i < l; i += blockDim.x) ut[r * l + i] = -ut[r * l + i];
 }
 
-// Cholesky (left-looking, lazy_projector.cpp:12-37) and the inverse of L,
-// written as w[c * l + j] = L^{-1}(c, j) — i.e. W = R^{-1} = L^{-T} as an
-// x-times-W operand of the sketch GEMM.
-__global__ void __launch_bounds__(1024) chol_inverse_kernel(const double* g, index_t l, double* w,
-                                                            double* lmat, int* status) {
+// Cholesky of G (lazy_projector.cpp:12-37: pivot tolerance 1e-14 * max diag,
+// RankDeficiencyError at the first failing pivot) and the inverse of L,
+// written as w[j * l + c] = L^{-1}(j, c) — i.e. W = R^{-1} = L^{-T} as an
+// x-times-W operand of the sketch GEMM. Blocked right-looking: a one-CTA panel
+// factorisation of 32 columns in shared memory, then the trailing SYRK update
+// over 32 x 32 tiles on many CTAs; the inverse by one warp per column of
+// L^{-1} (forward substitution, axpy form). The reference sums left-looking;
+// the orders differ by roundoff only.
+constexpr int kCholNb = 32;
+
+__global__ void chol_copy_kernel(const double* __restrict__ g, index_t l, double* __restrict__ lm) {
+  const index_t e = static_cast<index_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= l * l) return;
+  const index_t c = e / l, r = e % l;
+  lm[e] = r >= c ? g[e] : 0.0;
+}
+
+// Panel [p0, p0 + nb) x rows [p0, l): factor in shared memory (or in place
+// when the panel exceeds it, in_smem = 0), write back.
+__global__ void __launch_bounds__(256) chol_panel_kernel(const double* __restrict__ g, index_t l, index_t p0,
+                                                         double* __restrict__ lm, int* status, int in_smem) {
+  extern __shared__ double psh[];  // [nb][rows] column-major panel
   __shared__ double red[32];
-  __shared__ int failed;
-  if (threadIdx.x == 0) failed = 0;
+  __shared__ int fail;
+  if (status[0] != 0) return;  // an earlier panel failed
+  const int nb = static_cast<int>(l - p0 < kCholNb ? l - p0 : kCholNb);
+  const index_t rows = l - p0;
+  double* pan = in_smem ? psh : lm + p0 * l + p0;
+  const index_t ldp = in_smem ? rows : l;
   double maxd = 0.0;
   for (index_t j = threadIdx.x; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
   block_max_reduce(maxd, red);
-  const double pivot_tol = 1e-14 * maxd;
-  for (index_t e = threadIdx.x; e < l * l; e += blockDim.x) lmat[e] = 0.0;
-  __syncthreads();
-  for (index_t j = 0; j < l; ++j) {
-    // diagonal
-    if (threadIdx.x == 0) {
-      double d = g[j * l + j];
-      for (index_t r = 0; r < j; ++r) d -= lmat[r * l + j] * lmat[r * l + j];
-      if (d <= pivot_tol) {
-        failed = static_cast<int>(j) + 1;
-      } else {
-        lmat[j * l + j] = sqrt(d);
-      }
+  const double tol = 1e-14 * maxd;
+  if (threadIdx.x == 0) fail = 0;
+  if (in_smem) {
+    for (index_t e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const index_t j = e / rows, r = e % rows;
+      pan[e] = lm[(p0 + j) * l + p0 + r];
     }
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    double* cj = pan + static_cast<index_t>(j) * ldp;
+    const double d = cj[j];
+    if (!(d > tol)) {  // (NaN fails too)
+      if (threadIdx.x == 0) fail = static_cast<int>(p0 + j) + 1;
+      break;
+    }
+    const double dj = sqrt(d), inv = 1.0 / dj;
+    __syncthreads();  // everyone has read cj[j]
+    for (index_t r = j + threadIdx.x; r < rows; r += blockDim.x) cj[r] = r == j ? dj : cj[r] * inv;
     __syncthreads();
-    if (failed) break;
-    const double djj = lmat[j * l + j];
-    for (index_t i = j + 1 + threadIdx.x; i < l; i += blockDim.x) {
-      double v = g[j * l + i];
-      for (index_t r = 0; r < j; ++r) v -= lmat[r * l + i] * lmat[r * l + j];
-      lmat[j * l + i] = v / djj;
+    // rank-1 update of the panel's remaining columns (rows >= column)
+    for (int k = j + 1; k < nb; ++k) {
+      double* ck = pan + static_cast<index_t>(k) * ldp;
+      const double lkj = cj[k];
+      for (index_t r = k + threadIdx.x; r < rows; r += blockDim.x) ck[r] -= cj[r] * lkj;
     }
     __syncthreads();
   }
-  if (failed) {
-    if (threadIdx.x == 0) status[0] = failed;
+  __syncthreads();
+  if (fail) {
+    if (threadIdx.x == 0) status[0] = fail;
     return;
   }
-  // L^{-1}: column c solves L x = e_c by forward substitution; x(j) = L^{-1}(j, c).
-  for (index_t c = threadIdx.x; c < l; c += blockDim.x) {
-    for (index_t j = 0; j < l; ++j) {
-      if (j < c) {
-        w[j * l + c] = 0.0;  // L^{-1}(j, c) = 0 above the diagonal -> w[j*l + c]
-        continue;
-      }
-      double v = j == c ? 1.0 : 0.0;
-      for (index_t r = c; r < j; ++r) v -= lmat[r * l + j] * w[r * l + c];
-      w[j * l + c] = v / lmat[j * l + j];
+  if (in_smem) {
+    for (index_t e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const index_t j = e / rows, r = e % rows;
+      if (r >= j) lm[(p0 + j) * l + p0 + r] = pan[e];
     }
   }
-  if (threadIdx.x == 0) status[0] = 0;
+}
+
+// Trailing update A(i, k) -= sum_{j in panel} L(i, j) L(k, j) for i >= k >= p0 + nb.
+__global__ void __launch_bounds__(256) chol_syrk_kernel(index_t l, index_t p0, double* __restrict__ lm,
+                                                        const int* status) {
+  if (status[0] != 0) return;
+  const index_t t0 = p0 + kCholNb;
+  const index_t i0 = t0 + static_cast<index_t>(blockIdx.x) * 32, k0 = t0 + static_cast<index_t>(blockIdx.y) * 32;
+  if (blockIdx.x < blockIdx.y) return;  // upper tiles
+  __shared__ double li[kCholNb][33];
+  __shared__ double lk[kCholNb][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  for (int j = ty; j < kCholNb; j += 8) {
+    const index_t c = p0 + j;
+    li[j][tx] = i0 + tx < l ? lm[c * l + i0 + tx] : 0.0;
+    lk[j][tx] = k0 + tx < l ? lm[c * l + k0 + tx] : 0.0;
+  }
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    const index_t i = i0 + tx, k = k0 + ty + 8 * q;
+    if (i >= l || k >= l || i < k) continue;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < kCholNb; ++j) acc = fma(li[j][tx], lk[j][ty + 8 * q], acc);
+    lm[k * l + i] -= acc;
+  }
+}
+
+// W = L^{-T}: warp per column c of L^{-1}; the right-hand side (e_c) in shared
+// memory, reciprocal diagonal precomputed.
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ lm, index_t l, double* __restrict__ w,
+                                                       int* status) {
+  extern __shared__ double sh[];
+  if (status[0] != 0) return;
+  double* dinv = sh;                                            // [l]
+  double* b = sh + l + static_cast<index_t>(threadIdx.x / 32) * l;  // this warp's [l]
+  for (index_t j = threadIdx.x; j < l; j += blockDim.x) dinv[j] = 1.0 / lm[j * l + j];
+  __syncthreads();
+  const int lane = threadIdx.x % 32;
+  const index_t c = static_cast<index_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  if (c >= l) return;
+  for (index_t r = lane; r < l; r += 32) b[r] = r == c ? 1.0 : 0.0;
+  __syncwarp();
+  for (index_t j = c; j < l; ++j) {
+    const double x = b[j] * dinv[j];  // L^{-1}(j, c)
+    if (lane == 0) w[j * l + c] = x;
+    const double* colj = lm + j * l;
+    for (index_t r = j + 1 + lane; r < l; r += 32) b[r] -= colj[r] * x;
+    __syncwarp();
+  }
+  for (index_t j = lane; j < c; j += 32) w[j * l + c] = 0.0;
+  if (c == 0 && lane == 0) status[0] = 0;
 }
 
 // tmp(r, j) = sum_{s <= r} L^{-1}(r, s) F(s, j); then F <- tmp.
@@ -500,7 +571,29 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
                          int* status) {
-  chol_inverse_kernel<<<1, 1024, 0, s>>>(g, l, rinv, work, status);
+  if (l <= 0) return;
+  LPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  chol_copy_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(g, l, work);
+  std::size_t psm = static_cast<std::size_t>(l) * kCholNb * sizeof(double);
+  const int in_smem = psm <= 200 * 1024 ? 1 : 0;
+  if (!in_smem) psm = 0;
+  LPCA_CUDA(cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(psm > 48 * 1024 ? psm : 48 * 1024)));
+  for (index_t p0 = 0; p0 < l; p0 += kCholNb) {
+    chol_panel_kernel<<<1, 256, psm, s>>>(g, l, p0, work, status, in_smem);
+    const index_t t = l - p0 - kCholNb;
+    if (t > 0) {
+      const unsigned tiles = static_cast<unsigned>(ceil_div(t, 32));
+      chol_syrk_kernel<<<dim3(tiles, tiles), 256, 0, s>>>(l, p0, work, status);
+    }
+  }
+  int wpb = 8;  // warps per block: dinv + one right-hand side per warp in shared memory
+  while (wpb > 1 && static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
+  const std::size_t ism = static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double);
+  if (ism > 227 * 1024) throw Error(kInternal, "chol_inverse: l too large for the shared-memory solve");
+  LPCA_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ism > 48 * 1024 ? ism : 48 * 1024)));
+  chol_inv_kernel<<<static_cast<unsigned>(ceil_div(l, wpb)), 32 * wpb, ism, s>>>(work, l, rinv, status);
 }
 
 namespace {

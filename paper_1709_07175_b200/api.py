@@ -810,13 +810,23 @@ def apply_map(map_: ReductionMap, x, out=None, layout: str = "col", timings=None
     return y
 
 
-def fit_transform(x, config: ReducerConfig, y_dtype=np.float64, timings=None, ctx=None):
-    """fit then transform of the same X with a single upload; Y row-major host."""
+def fit_transform(x, config: ReducerConfig, y_dtype=np.float64, timings=None, ctx=None, out=None):
+    """fit then transform of the same X in one library call (one upload of a host
+    X; on the device the transform is queued right behind the fit's spectral
+    step). Y is a row-major host array, or `out` (a row-major torch CUDA tensor)."""
     ctx = ctx or default_context()
     vw = _View(x)
     cfg = config._c()
     t = L.Timings()
     h = C.c_void_p()
+    if out is not None:
+        import torch
+        dt = L.LPCA_F32 if out.dtype == torch.float32 else L.LPCA_F64
+        _check(ctx.lib.lpca_fit_transform(ctx.h, C.byref(cfg), C.byref(vw.view), C.byref(h),
+                                          C.c_void_p(out.data_ptr()), dt, L.LPCA_ROW_MAJOR, L.LPCA_DEVICE,
+                                          out.stride(0), C.byref(t)))
+        _fill_timings(timings, t)
+        return ReductionMap(h, ctx), out
     y = np.zeros((vw.view.rows, config.k), dtype=y_dtype)
     dt = L.LPCA_F32 if y.dtype == np.float32 else L.LPCA_F64
     _check(ctx.lib.lpca_fit_transform(ctx.h, C.byref(cfg), C.byref(vw.view), C.byref(h),

@@ -719,7 +719,8 @@ void eigh_dev(lpca_ctx& ctx, double* a, index_t l, double* evals, double* evecs,
 // truncated_svd_via_gram on a device F (l x n). Fills v (n x k), sigma (host),
 // and optionally u~ (device, l x k). Throws the reference's errors.
 void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index_t k, double* v,
-                     std::vector<double>& sigma, double* ut_out) {
+                     std::vector<double>& sigma, double* ut_out,
+                     const std::function<void()>& before_sync = std::function<void()>()) {
   if (l > n)
     throw Error(kDimension, "truncated_svd_via_gram: F must be wide (l <= n), got " + S(l) + "x" + S(n));
   if (k < 1 || k > l)
@@ -749,7 +750,16 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
   LPCA_CUDA(cudaMemcpyAsync(lam.data(), evals, sizeof(double) * l, cudaMemcpyDeviceToHost, ctx.stream));
   LPCA_CUDA(cudaMemcpyAsync(hsw, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   LPCA_CUDA(cudaMemcpyAsync(&hgap, gap, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  cudaEvent_t checked = nullptr;
+  if (before_sync) {  // work enqueued behind the spectral step, before the host checks wait
+    LPCA_CUDA(cudaEventCreateWithFlags(&checked, cudaEventDisableTiming));
+    LPCA_CUDA(cudaEventRecord(checked, ctx.stream));
+    before_sync();
+    LPCA_CUDA(cudaEventSynchronize(checked));
+    LPCA_CUDA(cudaEventDestroy(checked));
+  } else {
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
   hst = hsw[0];
   ctx.last_sweeps = hsw[1];
   if (std::getenv("LPCA_VERBOSE")) std::fprintf(stderr, "lazypca_b200: eigh l=%lld sweeps=%d\n", (long long)l, hsw[1]);
@@ -778,7 +788,13 @@ struct FitResult {
 };
 
 // The fit pipeline on a device-resident X (this rank's rows).
-lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_timings* t) {
+// after_spectral (optional): enqueued on the stream right behind the spectral
+// step, before the host reads the eigenvalues back (the fused fit + transform);
+// it gets the map (V ready on the stream) and the device max|X| of the fit.
+using AfterSpectral = std::function<void(lpca_map&, const uint32_t*)>;
+
+lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_timings* t,
+                  const AfterSpectral* after_spectral = nullptr) {
   const lpca_config c = resolve(cfg_in, x.n);
   if (c.streaming)
     throw Error(kInvalidArgument,
@@ -932,9 +948,18 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     utx_pass(ctx, x, u, l, f, exact, &xs);  // F = U^T X (or Q^T X)
     ctx.pass_slot = -1;
     ev.mark(4);
-    finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
     if (f16) LPCA_CUDA(cudaMemcpyAsync(&map->xmax, xs.dev, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
-    ev.mark(5);
+    bool marked = false;
+    if (after_spectral) {
+      finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr, [&] {
+        ev.mark(5);
+        marked = true;
+        (*after_spectral)(*map, f16 ? xs.dev : nullptr);
+      });
+    } else {
+      finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
+    }
+    if (!marked) ev.mark(5);
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
     if (xovf) {
       int flagged = 0;
@@ -943,7 +968,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
         delete map;
         ctx.force_scan = true;
         try {
-          lpca_map* again = fit_dev(ctx, cfg_in, x, t);
+          lpca_map* again = fit_dev(ctx, cfg_in, x, t, after_spectral);
           ctx.force_scan = false;
           return again;
         } catch (...) {
@@ -970,8 +995,25 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
 }
 
 // Y = X V into a caller buffer (apply_map, reducer.cpp:348-353).
+void transform_finish(lpca_ctx& ctx, lpca_timings* t) {
+  LPCA_CUDA(cudaEventSynchronize(ctx.ev[8]));
+  if (t) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    LPCA_CUDA(cudaEventElapsedTime(&a, ctx.ev[6], ctx.ev[7]));
+    LPCA_CUDA(cudaEventElapsedTime(&b, ctx.ev[16], ctx.ev[17]));
+    LPCA_CUDA(cudaEventElapsedTime(&c, ctx.ev[7], ctx.ev[8]));
+    t->transform += a * 1e-3;
+    t->transform_pass += b * 1e-3;
+    t->d2h += c * 1e-3;
+  }
+}
+
+// xmax_dev: the fit's device max|X| when X is the fitted matrix itself (fused
+// fit + transform: the fp16 scale needs no host value and no range check);
+// finish = false leaves the final wait (and the timings) to transform_finish.
 void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, int y_dtype,
-                   int y_layout, int y_location, index_t ldy, lpca_timings* t, double* d2h) {
+                   int y_layout, int y_location, index_t ldy, lpca_timings* t, double* d2h,
+                   const uint32_t* xmax_dev = nullptr, bool finish = true) {
   if (x.n != map.n)
     throw Error(kDimension, "apply_map: data has " + S(x.n) + " columns but the map expects " + S(map.n));
   if (y_dtype != LPCA_F32 && y_dtype != LPCA_F64) throw Error(kInvalidArgument, "transform: bad y dtype");
@@ -1011,7 +1053,12 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       Panel yo;
       yo.plain = ydev;
       yo.ld = ldy;
-      if (map.xmax > 0.0f && tc_pair_mode() && f16_enabled()) {
+      if (xmax_dev && tc_pair_mode() && f16_enabled()) {
+        XScale xs;  // the same rows the fit scanned: the fitted max is exact
+        xs.use = true;
+        xs.dev = const_cast<uint32_t*>(xmax_dev);
+        xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
+      } else if (map.xmax > 0.0f && tc_pair_mode() && f16_enabled()) {
         // fp16 encoding scaled by the fitted data's max|X|; if the rows read
         // here exceed it (fp16 overflow) or sit far below it (lost bits), the
         // pass is redone in tf32
@@ -1053,12 +1100,7 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
     ctx.pass_slot = -1;
   }
   ev.mark(8);
-  LPCA_CUDA(cudaEventSynchronize(ctx.ev[8]));
-  if (t) {
-    t->transform += ev.secs(6, 7);
-    t->transform_pass += ev.secs(16, 17);
-    t->d2h += ev.secs(7, 8);
-  }
+  if (finish) transform_finish(ctx, t);
 }
 
 // ---- streaming reducers (Algorithms 3 and 4, reducer.cpp:236-335) ------------
@@ -1554,6 +1596,7 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
     const DevX dx = stage_x(*ctx, x, "x", nullptr);
     ev.mark(10);
     lpca_map* map = nullptr;
+    bool fused = false;
     if ((cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP) {
       if (cfg->block_rows < 1) throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
       SliceSource src(dx, cfg->block_rows);
@@ -1562,10 +1605,19 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
       lpca_config c = *cfg;
       c.block_rows = 0;
       c.streaming = 0;
-      map = fit_dev(*ctx, c, dx, timings);
+      // the transform is enqueued behind the spectral step, before the fit's
+      // host checks: no idle gap between the two on the device
+      const AfterSpectral tr = [&](lpca_map& mp, const uint32_t* xmax_dev) {
+        transform_dev(*ctx, mp, dx, y, y_dtype, y_layout, y_location, ldy, nullptr, nullptr, xmax_dev, false);
+        fused = true;
+      };
+      map = fit_dev(*ctx, c, dx, timings, &tr);
     }
     try {
-      transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
+      if (fused)
+        transform_finish(*ctx, timings);
+      else  // RP and the streaming reducers: transform after the fit
+        transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
     } catch (...) {
       delete map;
       throw;

@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
               const __grid_constant__ CUtensorMap tmbl, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array (an integer round
+  // trip would lose the address space and turn every access generic)
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const int S = a.stages, AS = a.aslots;
   constexpr uint32_t x_bytes = kBM * kBK * 4;  // 16 KB X tile
   const uint32_t b_bytes = static_cast<uint32_t>(a.npad) * kBK * 4;
@@ -680,3 +682,14 @@ void launch_utx_tc(cudaStream_t, const float*, index_t, const float*, index_t, i
 }
 
 }  // namespace lpca
+
+#ifdef LPCA_PAIR_PROF
+extern "C" void lpca_debug_pair_prof(unsigned long long* out32, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, lpca::g_pair_prof, sizeof(unsigned long long) * 32);
+  if (reset) {
+    static const unsigned long long zero[32] = {};
+    cudaMemcpyToSymbol(lpca::g_pair_prof, zero, sizeof(zero));
+  }
+}
+#endif

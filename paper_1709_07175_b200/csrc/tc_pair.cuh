@@ -237,13 +237,25 @@ __device__ __forceinline__ void pair_item_coords(const PairArgs& a, int item, in
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+#ifdef LPCA_PAIR_PROF  // role timers (tools/pair_prof.py): cycles summed over CTAs
+__device__ unsigned long long g_pair_prof[2][16];  // [mode][counter]
+#define PP_T0() const long long pp_t0_ = clock64()
+#define PP_ADD(k) \
+  if (lane == 0) pp[k] += clock64() - pp_t0_
+#else
+#define PP_T0()
+#define PP_ADD(k)
+#endif
+
 template <int kMode, bool kHalf>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
                const __grid_constant__ CUtensorMap tmbl, PairArgs a) {
   constexpr int BK = kHalf ? 64 : 32;  // K per stage (one 128 B swizzle row of B)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array (an integer round
+  // trip would lose the address space and turn every access generic)
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   const int S = a.stages, AS = a.aslots;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -298,6 +310,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   float xs = 1.0f;  // s_x (fp16 encoding)
   if (kHalf) xs = pow2_scale_for(a.xmax_in ? __uint_as_float(*a.xmax_in) : a.xmax_val);
 
+#ifdef LPCA_PAIR_PROF
+  long long pp[16] = {};
+  const long long pp_start = clock64();
+#endif
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (lane == 0) {
@@ -309,7 +325,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pair_item_coords<kMode>(a, item, t0, k0, k1);
         const int mine = t0 + static_cast<int>(rank) * kBM;
         for (int k = k0; k < k1; k += BK) {
-          mbar_wait(&empty[stage], phase ^ 1, 1);
+          {
+            PP_T0();
+            mbar_wait(&empty[stage], phase ^ 1, 1);
+            PP_ADD(0);
+          }
           uint8_t* st = smem + stage * stage_bytes;
           mbar_expect_tx(&full_x[stage], x_bytes);
           if (kMode == kXW) {
@@ -337,13 +357,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pair_item_coords<kMode>(a, item, t0, k0, k1);
         for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
           const int b = rc % a.nrb;
-          mbar_wait(&tempty[b], ((rc / a.nrb) & 1) ^ 1, 2);
+          {
+            PP_T0();
+            mbar_wait(&tempty[b], ((rc / a.nrb) & 1) ^ 1, 2);
+            PP_ADD(2);
+          }
           tc_fence_after();
           const uint32_t d = tmem_base + static_cast<uint32_t>(b * a.npad);
           const int q1 = min(k1, q0 + run_k);
           for (int k = q0; k < q1; k += BK) {
-            mbar_wait(&conv[aslot], aphase, 3);
-            mbar_wait(&full_b[stage], phase, 3);
+            {
+              PP_T0();
+              mbar_wait(&conv[aslot], aphase, 3);
+              PP_ADD(3);
+            }
+            {
+              PP_T0();
+              mbar_wait(&full_b[stage], phase, 3);
+              PP_ADD(4);
+            }
             tc_fence_after();
             const uint64_t bh = desc0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
             const uint64_t bl = bh + static_cast<uint64_t>(bh_bytes >> 4);
@@ -435,8 +467,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           xmax = fmaxf(xmax, mx);
         }
         for (int j = 0; j < nst; ++j) {
-          mbar_wait(&full_x[stage], phase, 4);
-          mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+          {
+            PP_T0();
+            mbar_wait(&full_x[stage], phase, 4);
+            if (q == 0) PP_ADD(6);
+          }
+          {
+            PP_T0();
+            mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+            if (q == 0) PP_ADD(7);
+          }
           tc_fence_after();
           const uint8_t* xt = smem + stage * stage_bytes;
           const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
@@ -541,7 +581,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (r + 1 < runs) fetch_scales(r + 1);
         }
-        mbar_wait(&tfull[b], (rc / a.nrb) & 1, 5);
+        {
+          PP_T0();
+          mbar_wait(&tfull[b], (rc / a.nrb) & 1, 5);
+          if (q == 0) PP_ADD(9);
+        }
         tc_fence_after();
         const uint32_t racc = lane_base + static_cast<uint32_t>(b * a.npad);
         const bool first = r == 0, last = r == runs - 1;
@@ -699,6 +743,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   }
+#ifdef LPCA_PAIR_PROF
+  {
+    const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 4 ? 2 : warp == 8 ? 3 : -1;  // q == 0 warps
+    if (role >= 0 && lane == 0 && (warp != 1 || leader)) {
+      for (int k = 0; k < 16; ++k)
+        if (pp[k]) atomicAdd(&g_pair_prof[kMode][k], static_cast<unsigned long long>(pp[k]));
+      atomicAdd(&g_pair_prof[kMode][12 + role], static_cast<unsigned long long>(clock64() - pp_start));
+    }
+  }
+#endif
   __syncthreads();
   cluster_sync();  // the peer is done with every barrier and TMEM column
   if (warp == 1) {

@@ -482,7 +482,9 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
     a.n = static_cast<int>(p.n);
     a.npad = wc;
     a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
-    a.run_stages = env_int("LPCA_TC_RUN", 4);  // K = 256 per fp16 run: half the folds of K = 128
+    // fp16 runs: K = 512 with one global X scale (transform, power steps); the
+    // scanned sketch clamps to the stage ring (K = 256)
+    a.run_stages = env_int("LPCA_TC_RUN", 8);
     a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f) ? (p.ovf ? 2 : 1) : 0;
     a.ovf = p.ovf;
     a.xmax_in = p.xmax_in;

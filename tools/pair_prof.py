@@ -33,6 +33,10 @@ names = ["tma:wait_empty", "-", "mma:wait_tempty", "mma:wait_conv", "mma:wait_fu
 for mode, label in ((0, "X W (sketch + transform)"), (1, "X^T U")):
     v = buf[16 * mode:16 * mode + 16].astype(np.float64)
     print(label)
+    tot = v[14]
+    if tot:
+        print("  conv detail: " + "  ".join(f"{nm} {v[i] / tot * 100:5.1f}%" for nm, i in
+                                          (("load", 1), ("compute+st", 5), ("st_wait", 8), ("arrive", 10))))
     for role, (tot_i, parts) in {"tma": (12, [0]), "mma": (13, [2, 3, 4]), "conv": (14, [6, 7]),
                                  "epi": (15, [9])}.items():
         tot = v[tot_i]

@@ -207,6 +207,38 @@ lpca_status lpca_map_file_write(const char* path, const lpca_map_info* info, con
 lpca_status lpca_map_file_read(const char* path, lpca_map_info* info, double* v_host, int64_t v_capacity,
                                double* sigma_host);
 
+/* ---- matrix files (proj/core/src/matrix_io.cpp, matrix_io.hpp:1-80) ----------
+ * read_sparse_matrix_market / read_dense_matrix_market / read_dense_csv with the
+ * reference's rules (banner checks, 1-based coordinates with duplicates summed
+ * and zeros dropped into the canonical CSC, non-finite values rejected) and its
+ * ParseError messages and line numbers; the write_* functions produce the
+ * reference's bytes (shortest round-trip values). A parsed file is held on the
+ * host: query its shape, copy it out, or view it for lpca_fit/lpca_transform. */
+typedef struct lpca_matrix_file lpca_matrix_file;
+lpca_status lpca_read_sparse_matrix_market(const char* path, lpca_matrix_file** out);
+lpca_status lpca_read_dense_matrix_market(const char* path, lpca_matrix_file** out);
+lpca_status lpca_read_dense_csv(const char* path, lpca_matrix_file** out);
+/* nnz = -1 for a dense file */
+lpca_status lpca_matrix_file_info(const lpca_matrix_file* f, int64_t* rows, int64_t* cols, int64_t* nnz);
+/* sparse: CSC col_ptr (cols+1), row_idx, values (nnz); dense: column-major values (rows*cols) */
+lpca_status lpca_matrix_file_copy(const lpca_matrix_file* f, int64_t* col_ptr, int64_t* row_idx, double* values);
+lpca_status lpca_matrix_file_view(const lpca_matrix_file* f, lpca_matrix_view* out);
+void lpca_matrix_file_free(lpca_matrix_file* f);
+lpca_status lpca_write_sparse_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* col_ptr,
+                                            const int64_t* row_idx, const double* values);
+lpca_status lpca_write_dense_matrix_market(const char* path, int64_t rows, int64_t cols, const double* colmajor);
+lpca_status lpca_write_dense_csv(const char* path, int64_t rows, int64_t cols, const double* colmajor);
+/* Row-block streams from files (MatrixMarketRowBlockStream / CsvRowBlockStream,
+ * matrix_io.cpp:313-443): pass lpca_file_stream_next and the stream as `next` and
+ * `user` to lpca_fit_stream. MatrixMarket blocks are CSC (a counting pass at
+ * open, one scan per block, one block resident); CSV blocks are dense row-major
+ * fp64. A parse error inside next() aborts the fit with that ParseError. */
+typedef struct lpca_file_stream lpca_file_stream;
+lpca_status lpca_open_matrix_market_stream(const char* path, int64_t block_rows, lpca_file_stream** out);
+lpca_status lpca_open_csv_stream(const char* path, int64_t block_rows, lpca_file_stream** out);
+int32_t lpca_file_stream_next(void* stream, lpca_matrix_view* block, int64_t* slice_index);
+void lpca_file_stream_close(lpca_file_stream* s);
+
 /* ---- verification metrics on the device (proj/core/src/metrics.cpp) --------
  * chordal_distance (:123-136): n x k1 and n x k2 column-major orthonormal bases;
  * InvalidArgumentError if either is not orthonormal to 1e-8 * k. */

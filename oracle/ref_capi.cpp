@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -27,6 +28,7 @@
 #include "lazypca/threading.hpp"
 #include "lazypca/tridiag_eigh.hpp"
 #include "lazypca/truncated_svd.hpp"
+#include "lazypca/matrix_io.hpp"
 #include "lazypca/metrics.hpp"
 #include "lazypca/spectral_norm.hpp"
 
@@ -339,6 +341,74 @@ int ref_row_space_reconstruction_error(const void* x, int dtype, std::int64_t m,
 // spectral_norm(SparseMatrix) (proj/core/src/spectral_norm.cpp:70-77).
 int ref_spectral_norm(const void* x, int dtype, std::int64_t m, std::int64_t n, double* out) {
   return guarded([&] { *out = spectral_norm(csc_any(x, dtype, m, n)); });
+}
+
+// matrix_io (proj/core/src/matrix_io.cpp). Readers are two-call: sizes first
+// (arrays null), then the arrays. Sparse: CSC; dense: column-major.
+int ref_read_matrix_file(int kind, const char* path, std::int64_t* rows, std::int64_t* cols, std::int64_t* nnz,
+                         std::int64_t* ptr, std::int64_t* idx, double* val) {
+  return guarded([&] {
+    if (kind == 0) {
+      const SparseMatrix x = read_sparse_matrix_market_file(path);
+      *rows = x.rows();
+      *cols = x.cols();
+      *nnz = x.nnz();
+      if (ptr) std::copy(x.col_ptr().begin(), x.col_ptr().end(), ptr);
+      if (idx) std::copy(x.row_idx().begin(), x.row_idx().end(), idx);
+      if (val) std::copy(x.values().begin(), x.values().end(), val);
+    } else {
+      const DenseMatrix d = kind == 1 ? read_dense_matrix_market_file(path) : read_dense_csv_file(path);
+      *rows = d.rows();
+      *cols = d.cols();
+      *nnz = -1;
+      if (val) copy_out(d, val);
+    }
+  });
+}
+
+int ref_write_matrix_file(int kind, const char* path, std::int64_t rows, std::int64_t cols, const std::int64_t* ptr,
+                          const std::int64_t* idx, const double* val) {
+  return guarded([&] {
+    if (kind == 0) {
+      const std::int64_t nnz = ptr[cols];
+      write_sparse_matrix_market_file(
+          SparseMatrix::from_csc(rows, cols, std::vector<index_t>(ptr, ptr + cols + 1),
+                                 std::vector<index_t>(idx, idx + nnz), std::vector<double>(val, val + nnz)),
+          path);
+    } else if (kind == 1) {
+      write_dense_matrix_market_file(dense_from(val, rows, cols), path);
+    } else {
+      write_dense_csv_file(dense_from(val, rows, cols), path);
+    }
+  });
+}
+
+// Block b of a MatrixMarket / CSV row-block stream as CSC (two-call); *count =
+// the number of blocks the stream produced in total.
+int ref_stream_block(int kind, const char* path, std::int64_t block_rows, std::int64_t b, std::int64_t* count,
+                     std::int64_t* rows, std::int64_t* cols, std::int64_t* nnz, std::int64_t* ptr, std::int64_t* idx,
+                     double* val) {
+  return guarded([&] {
+    std::unique_ptr<RowBlockStream> s;
+    if (kind == 0)
+      s = std::make_unique<MatrixMarketRowBlockStream>(path, block_rows);
+    else
+      s = std::make_unique<CsvRowBlockStream>(path, block_rows);
+    std::int64_t n = 0;
+    while (auto blk = s->next()) {
+      if (n == b) {
+        const SparseMatrix& x = blk->block;
+        *rows = x.rows();
+        *cols = x.cols();
+        *nnz = x.nnz();
+        if (ptr) std::copy(x.col_ptr().begin(), x.col_ptr().end(), ptr);
+        if (idx) std::copy(x.row_idx().begin(), x.row_idx().end(), idx);
+        if (val) std::copy(x.values().begin(), x.values().end(), val);
+      }
+      ++n;
+    }
+    *count = n;
+  });
 }
 
 }  // extern "C"

@@ -221,6 +221,50 @@ def spectral_norm(x: np.ndarray) -> float:
     return out.value
 
 
+def read_matrix_file(kind: int, path: str):
+    """kind 0 sparse MatrixMarket -> (rows, cols, ptr, idx, val); 1 dense MatrixMarket, 2 CSV -> array."""
+    r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
+    lib = load()
+    _chk(lib.ref_read_matrix_file(C.c_int(kind), path.encode(), C.byref(r), C.byref(c), C.byref(z), None, None, None))
+    if kind == 0:
+        ptr = np.zeros(c.value + 1, dtype=np.int64)
+        idx = np.zeros(max(z.value, 1), dtype=np.int64)
+        val = np.zeros(max(z.value, 1))
+        _chk(lib.ref_read_matrix_file(C.c_int(kind), path.encode(), C.byref(r), C.byref(c), C.byref(z), _p(ptr),
+                                      _p(idx), _p(val)))
+        return r.value, c.value, ptr, idx[:z.value], val[:z.value]
+    a = np.zeros((r.value, c.value), order="F")
+    _chk(lib.ref_read_matrix_file(C.c_int(kind), path.encode(), C.byref(r), C.byref(c), C.byref(z), None, None,
+                                  _p(a)))
+    return a
+
+
+def write_matrix_file(kind: int, path: str, rows: int, cols: int, ptr=None, idx=None, val=None) -> None:
+    v = np.asfortranarray(val, dtype=np.float64)  # kept alive across the call
+    _chk(load().ref_write_matrix_file(C.c_int(kind), path.encode(), C.c_int64(rows), C.c_int64(cols),
+                                      _p(ptr), _p(idx), _p(v)))
+
+
+def stream_blocks(kind: int, path: str, block_rows: int):
+    """All blocks of the reference's MatrixMarket (0) / CSV (1) row-block stream as CSC tuples."""
+    lib = load()
+    out = []
+    b = 0
+    while True:
+        cnt, r, c, z = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(-1)
+        _chk(lib.ref_stream_block(C.c_int(kind), path.encode(), C.c_int64(block_rows), C.c_int64(b), C.byref(cnt),
+                                  C.byref(r), C.byref(c), C.byref(z), None, None, None))
+        if b >= cnt.value:
+            return out
+        ptr = np.zeros(c.value + 1, dtype=np.int64)
+        idx = np.zeros(max(z.value, 1), dtype=np.int64)
+        val = np.zeros(max(z.value, 1))
+        _chk(lib.ref_stream_block(C.c_int(kind), path.encode(), C.c_int64(block_rows), C.c_int64(b), C.byref(cnt),
+                                  C.byref(r), C.byref(c), C.byref(z), _p(ptr), _p(idx), _p(val)))
+        out.append((r.value, c.value, ptr, idx[:z.value], val[:z.value]))
+        b += 1
+
+
 def cpu_threads() -> int:
     return len(os.sched_getaffinity(0))
 

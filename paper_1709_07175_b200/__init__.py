@@ -14,7 +14,9 @@ from .api import (  # noqa: F401
     reducer_method_from_string, regenerate, RowBlock, RowBlockStream, SliceRowBlockStream, split_rows,
     load_map_file, read_map_file, save_map_file, write_map_file, chordal_distance, distance_preservation,
     DistancePreservationReport, ReconstructionErrorReport, ResidualRoute, bound_value, reconstruction_error,
-    row_space_reconstruction_error, spectral_norm,
+    row_space_reconstruction_error, spectral_norm, read_sparse_matrix_market, read_dense_matrix_market,
+    read_dense_csv, write_sparse_matrix_market, write_dense_matrix_market, write_dense_csv,
+    MatrixMarketRowBlockStream, CsvRowBlockStream,
     set_thread_count, sketch_f32, spmm, synth_lowrank, thread_count, to_string, tridiag_eigh,
     truncated_svd_via_gram,
 )

@@ -96,6 +96,20 @@ SIGNATURES = {
     "lpca_map_create": (I32, [P, C.POINTER(MapInfo), P, P, PP]),
     "lpca_map_destroy": (I32, [P]),
     "lpca_chordal_distance": (I32, [P, P, I64, I64, P, I64, I64, I32, DP]),
+    "lpca_read_sparse_matrix_market": (I32, [C.c_char_p, PP]),
+    "lpca_read_dense_matrix_market": (I32, [C.c_char_p, PP]),
+    "lpca_read_dense_csv": (I32, [C.c_char_p, PP]),
+    "lpca_matrix_file_info": (I32, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "lpca_matrix_file_copy": (I32, [P, P, P, P]),
+    "lpca_matrix_file_view": (I32, [P, C.POINTER(MatrixView)]),
+    "lpca_matrix_file_free": (None, [P]),
+    "lpca_write_sparse_matrix_market": (I32, [C.c_char_p, I64, I64, P, P, P]),
+    "lpca_write_dense_matrix_market": (I32, [C.c_char_p, I64, I64, P]),
+    "lpca_write_dense_csv": (I32, [C.c_char_p, I64, I64, P]),
+    "lpca_open_matrix_market_stream": (I32, [C.c_char_p, I64, PP]),
+    "lpca_open_csv_stream": (I32, [C.c_char_p, I64, PP]),
+    "lpca_file_stream_next": (I32, [P, C.POINTER(MatrixView), C.POINTER(C.c_int64)]),
+    "lpca_file_stream_close": (None, [P]),
     "lpca_reconstruction_error": (I32, [P, C.POINTER(MatrixView), P, I64, I64, I32, I32, I64, I64, I32, I64,
                                         C.POINTER(ReconReport)]),
     "lpca_row_space_reconstruction_error": (I32, [P, C.POINTER(MatrixView), P, I64, I64, I32,

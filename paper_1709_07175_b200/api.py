@@ -632,6 +632,61 @@ def bound_value(m: int, n: int, k: int, l: int, sigma_k_plus_1: float) -> float:
     return out.value
 
 
+# ---- matrix files (matrix_io.cpp), the reference's formats and bytes ---------------
+def _read_file(fn, path: str):
+    lib = L.load()
+    h = C.c_void_p()
+    _check(fn(str(path).encode(), C.byref(h)))
+    try:
+        rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.lpca_matrix_file_info(h, C.byref(rows), C.byref(cols), C.byref(nnz)))
+        m, n, z = rows.value, cols.value, nnz.value
+        if z >= 0:
+            ptr = np.zeros(n + 1, dtype=np.int64)
+            idx = np.zeros(max(z, 1), dtype=np.int64)
+            val = np.zeros(max(z, 1))
+            _check(lib.lpca_matrix_file_copy(h, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data))
+            return SparseMatrix(m, n, ptr, idx[:z], val[:z])
+        a = np.zeros((m, n), order="F")
+        _check(lib.lpca_matrix_file_copy(h, None, None, a.ctypes.data if a.size else None))
+        return a
+    finally:
+        lib.lpca_matrix_file_free(h)
+
+
+def read_sparse_matrix_market(path: str) -> SparseMatrix:
+    """read_sparse_matrix_market_file (matrix_io.cpp:143-175)."""
+    return _read_file(L.load().lpca_read_sparse_matrix_market, path)
+
+
+def read_dense_matrix_market(path: str) -> np.ndarray:
+    """read_dense_matrix_market_file (matrix_io.cpp:194-230), column-major."""
+    return _read_file(L.load().lpca_read_dense_matrix_market, path)
+
+
+def read_dense_csv(path: str) -> np.ndarray:
+    """read_dense_csv_file (matrix_io.cpp:245-277)."""
+    return _read_file(L.load().lpca_read_dense_csv, path)
+
+
+def write_sparse_matrix_market(x: SparseMatrix, path: str) -> None:
+    lib = L.load()
+    _check(lib.lpca_write_sparse_matrix_market(str(path).encode(), x.rows(), x.cols(), x.col_ptr.ctypes.data,
+                                               x.row_idx.ctypes.data if x.nnz() else None,
+                                               x.values.ctypes.data if x.nnz() else None))
+
+
+def write_dense_matrix_market(a, path: str) -> None:
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    _check(L.load().lpca_write_dense_matrix_market(str(path).encode(), a.shape[0], a.shape[1],
+                                                   a.ctypes.data if a.size else None))
+
+
+def write_dense_csv(a, path: str) -> None:
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    _check(L.load().lpca_write_dense_csv(str(path).encode(), a.shape[0], a.shape[1], a.ctypes.data if a.size else None))
+
+
 # ---- map files (reducer.cpp:355-412), byte-compatible with the reference ----------
 def save_map_file(map_: "ReductionMap", path: str) -> None:
     """save_map_file: one-line JSON header + V as a dense MatrixMarket array."""
@@ -693,6 +748,64 @@ class RowBlockStream:
         raise NotImplementedError
 
 
+
+class _FileRowBlockStream(RowBlockStream):
+    """A native row-block stream over a file; the streaming reducers drive it
+    from C. next() also works from Python (a copy of the block)."""
+
+    def __init__(self, opener, path: str, block_rows: int):
+        self._lib = L.load()
+        self._h = C.c_void_p()
+        _check(opener(str(path).encode(), int(block_rows), C.byref(self._h)))
+
+    def next(self):
+        v = L.MatrixView()
+        sl = C.c_int64()
+        r = self._lib.lpca_file_stream_next(self._h, C.byref(v), C.byref(sl))
+        if r < 0:
+            _check(-r)
+        if r == 0:
+            return None
+        m, n = v.rows, v.cols
+        if v.layout == L.LPCA_CSC:
+            i64 = C.POINTER(C.c_int64)
+            ptr = np.ctypeslib.as_array(C.cast(v.col_ptr, i64), shape=(n + 1,)).copy()
+            z = int(v.nnz)
+            idx = (np.ctypeslib.as_array(C.cast(v.row_idx, i64), shape=(max(z, 1),))[:z].copy() if z
+                   else np.zeros(0, np.int64))
+            val = (np.ctypeslib.as_array(C.cast(v.data, C.POINTER(C.c_double)), shape=(max(z, 1),))[:z].copy()
+                   if z else np.zeros(0))
+            return RowBlock(int(sl.value), SparseMatrix(m, n, ptr, idx, val))
+        a = np.ctypeslib.as_array(C.cast(v.data, C.POINTER(C.c_double)), shape=(m, n)).copy()
+        return RowBlock(int(sl.value), a)
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.lpca_file_stream_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MatrixMarketRowBlockStream(_FileRowBlockStream):
+    """MatrixMarketRowBlockStream (matrix_io.cpp:313-377): CSC row blocks of a
+    coordinate file, one block resident."""
+
+    def __init__(self, path: str, block_rows: int):
+        super().__init__(L.load().lpca_open_matrix_market_stream, path, block_rows)
+
+
+class CsvRowBlockStream(_FileRowBlockStream):
+    """CsvRowBlockStream (matrix_io.cpp:379-443): row blocks of a CSV file (dense)."""
+
+    def __init__(self, path: str, block_rows: int):
+        super().__init__(L.load().lpca_open_csv_stream, path, block_rows)
+
+
 class SliceRowBlockStream(RowBlockStream):
     """Lazy row partition of an in-memory matrix (sparse_matrix.cpp:125-139)."""
 
@@ -728,6 +841,14 @@ def split_rows(x, block_rows: int) -> list:
 
 def _fit_stream(stream: RowBlockStream, config: ReducerConfig, timings, ctx) -> ReductionMap:
     ctx = ctx or default_context()
+    if isinstance(stream, _FileRowBlockStream):  # native: no Python in the block loop
+        cfg = config._c()
+        t = L.Timings()
+        h = C.c_void_p()
+        nxt = C.cast(ctx.lib.lpca_file_stream_next, C.c_void_p)
+        _check(ctx.lib.lpca_fit_stream(ctx.h, C.byref(cfg), nxt, stream._h, C.byref(h), C.byref(t)))
+        _fill_timings(timings, t)
+        return ReductionMap(h, ctx)
     keep = {}
     err = []
 

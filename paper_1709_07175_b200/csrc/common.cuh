@@ -46,6 +46,10 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 // Sets the thread's lpca_last_error* state (defined in lpca.cu).
 void set_last_error(const std::string& msg, std::int64_t index, double gap);
+// An error raised inside a block callback (lpca_file_stream_next), rethrown by
+// the streaming reducer that called it (per thread).
+void set_callback_error(const Error& e);
+bool take_callback_error(Error* out);
 
 inline index_t ceil_div(index_t a, index_t b) { return (a + b - 1) / b; }
 inline index_t round_up(index_t a, index_t b) { return ceil_div(a, b) * b; }

@@ -40,6 +40,17 @@ thread_local double g_err_gap = 0.0;
 }  // namespace
 
 // lpca_last_error* state for the host-only translation units (mapio.cpp).
+namespace {
+thread_local std::unique_ptr<lpca::Error> g_callback_error;
+}
+void lpca::set_callback_error(const Error& e) { g_callback_error = std::make_unique<Error>(e); }
+bool lpca::take_callback_error(Error* out) {
+  if (!g_callback_error) return false;
+  *out = *g_callback_error;
+  g_callback_error.reset();
+  return true;
+}
+
 void lpca::set_last_error(const std::string& msg, std::int64_t index, double gap) {
   g_err_msg = msg;
   g_err_index = index;
@@ -1116,7 +1127,11 @@ struct CallbackSource final : BlockSource {
   CallbackSource(lpca_next_block_fn f, void* u) : fn(f), user(u) {}
   bool next(lpca_matrix_view* v, int64_t* slice) override {
     const int32_t r = fn(user, v, slice);
-    if (r < 0) throw Error(kInvalidArgument, "streaming: the block callback reported error " + S(r));
+    if (r < 0) {
+      Error e(kInvalidArgument, "");
+      if (take_callback_error(&e)) throw e;  // e.g. a ParseError from lpca_file_stream_next
+      throw Error(kInvalidArgument, "streaming: the block callback reported error " + S(r));
+    }
     return r > 0;
   }
 };

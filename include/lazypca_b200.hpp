@@ -382,6 +382,115 @@ class SliceRowBlockStream final : public RowBlockStream {
   index_t block_rows_, slice_count_ = 0, next_slice_ = 0;
 };
 
+// ---- matrix files (matrix_io.hpp), read and written by the library ----------------
+namespace detail {
+inline lpca_matrix_file* open_file(lpca_status (*reader)(const char*, lpca_matrix_file**), const std::string& p) {
+  lpca_matrix_file* f = nullptr;
+  check(reader(p.c_str(), &f));
+  return f;
+}
+}  // namespace detail
+inline SparseMatrix read_sparse_matrix_market_file(const std::string& path) {
+  std::unique_ptr<lpca_matrix_file, void (*)(lpca_matrix_file*)> f(
+      detail::open_file(lpca_read_sparse_matrix_market, path), lpca_matrix_file_free);
+  int64_t r = 0, c = 0, z = 0;
+  detail::check(lpca_matrix_file_info(f.get(), &r, &c, &z));
+  std::vector<index_t> cp(static_cast<std::size_t>(c) + 1), ri(static_cast<std::size_t>(z));
+  std::vector<double> va(static_cast<std::size_t>(z));
+  detail::check(lpca_matrix_file_copy(f.get(), cp.data(), ri.data(), va.data()));
+  return SparseMatrix::from_csc(r, c, std::move(cp), std::move(ri), std::move(va));
+}
+namespace detail {
+inline DenseMatrix read_dense(lpca_status (*reader)(const char*, lpca_matrix_file**), const std::string& path) {
+  std::unique_ptr<lpca_matrix_file, void (*)(lpca_matrix_file*)> f(open_file(reader, path), lpca_matrix_file_free);
+  int64_t r = 0, c = 0, z = 0;
+  check(lpca_matrix_file_info(f.get(), &r, &c, &z));
+  DenseMatrix out(r, c);
+  check(lpca_matrix_file_copy(f.get(), nullptr, nullptr, out.data()));
+  return out;
+}
+}  // namespace detail
+inline DenseMatrix read_dense_matrix_market_file(const std::string& path) {
+  return detail::read_dense(lpca_read_dense_matrix_market, path);
+}
+inline DenseMatrix read_dense_csv_file(const std::string& path) { return detail::read_dense(lpca_read_dense_csv, path); }
+inline void write_sparse_matrix_market_file(const SparseMatrix& x, const std::string& path) {
+  detail::check(lpca_write_sparse_matrix_market(path.c_str(), x.rows(), x.cols(), x.col_ptr().data(),
+                                                x.row_idx().data(), x.values().data()));
+}
+inline void write_dense_matrix_market_file(const DenseMatrix& x, const std::string& path) {
+  detail::check(lpca_write_dense_matrix_market(path.c_str(), x.rows(), x.cols(), x.data()));
+}
+inline void write_dense_csv_file(const DenseMatrix& x, const std::string& path) {
+  detail::check(lpca_write_dense_csv(path.c_str(), x.rows(), x.cols(), x.data()));
+}
+
+// Row blocks straight from a file (matrix_io.hpp:41-80). The streaming reducers
+// drive these natively; next() also works (a copy of the block as CSC).
+class FileRowBlockStream : public RowBlockStream {
+ public:
+  ~FileRowBlockStream() override { lpca_file_stream_close(s_); }
+  FileRowBlockStream(const FileRowBlockStream&) = delete;
+  FileRowBlockStream& operator=(const FileRowBlockStream&) = delete;
+  lpca_file_stream* handle() const { return s_; }
+  std::optional<RowBlock> next() override {
+    lpca_matrix_view v{};
+    int64_t slice = 0;
+    const int32_t r = lpca_file_stream_next(s_, &v, &slice);
+    if (r < 0) detail::check(static_cast<lpca_status>(-r));
+    if (r == 0) return std::nullopt;
+    std::vector<index_t> cp, ri;
+    std::vector<double> va;
+    if (v.layout == LPCA_CSC) {
+      cp.assign(v.col_ptr, v.col_ptr + v.cols + 1);
+      ri.assign(v.row_idx, v.row_idx + v.nnz);
+      const double* d = static_cast<const double*>(v.data);
+      va.assign(d, d + v.nnz);
+    } else {  // dense row-major block (CSV): the reference's sparsified form
+      const double* d = static_cast<const double*>(v.data);
+      cp.assign(static_cast<std::size_t>(v.cols) + 1, 0);
+      for (index_t j = 0; j < v.cols; ++j) {
+        for (index_t i = 0; i < v.rows; ++i)
+          if (d[i * v.ld + j] != 0.0) {
+            ri.push_back(i);
+            va.push_back(d[i * v.ld + j]);
+          }
+        cp[static_cast<std::size_t>(j) + 1] = static_cast<index_t>(ri.size());
+      }
+    }
+    return RowBlock{slice, SparseMatrix::from_csc(v.rows, v.cols, std::move(cp), std::move(ri), std::move(va))};
+  }
+
+ protected:
+  explicit FileRowBlockStream(lpca_file_stream* s) : s_(s) {}
+
+ private:
+  lpca_file_stream* s_;
+};
+class MatrixMarketRowBlockStream final : public FileRowBlockStream {
+ public:
+  MatrixMarketRowBlockStream(const std::string& path, index_t block_rows)
+      : FileRowBlockStream(open(path, block_rows)) {}
+
+ private:
+  static lpca_file_stream* open(const std::string& path, index_t block_rows) {
+    lpca_file_stream* s = nullptr;
+    detail::check(lpca_open_matrix_market_stream(path.c_str(), block_rows, &s));
+    return s;
+  }
+};
+class CsvRowBlockStream final : public FileRowBlockStream {
+ public:
+  CsvRowBlockStream(const std::string& path, index_t block_rows) : FileRowBlockStream(open(path, block_rows)) {}
+
+ private:
+  static lpca_file_stream* open(const std::string& path, index_t block_rows) {
+    lpca_file_stream* s = nullptr;
+    detail::check(lpca_open_csv_stream(path.c_str(), block_rows, &s));
+    return s;
+  }
+};
+
 namespace detail {
 struct StreamPump {  // lpca_next_block_fn over a RowBlockStream; keeps the current block alive
   RowBlockStream* s;
@@ -407,7 +516,9 @@ inline ReductionMap fit_stream(RowBlockStream& blocks, ReducerConfig cfg, Reduce
   StreamPump pump{&blocks, std::nullopt, nullptr};
   lpca_map* out = nullptr;
   lpca_timings tm{};
-  const lpca_status st = lpca_fit_stream(ctx(), &c, &StreamPump::next, &pump, &out, &tm);
+  auto* file = dynamic_cast<FileRowBlockStream*>(&blocks);  // file streams run natively
+  const lpca_status st = file ? lpca_fit_stream(ctx(), &c, &lpca_file_stream_next, file->handle(), &out, &tm)
+                              : lpca_fit_stream(ctx(), &c, &StreamPump::next, &pump, &out, &tm);
   if (pump.err) std::rethrow_exception(pump.err);
   check(st);
   if (t) {

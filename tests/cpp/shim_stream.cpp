@@ -1,7 +1,8 @@
 // The reference-shaped C++ shim end to end: a reference caller's code (dense
 // CSC X, reduce_lazy_spca / reduce_spca_streaming over SliceRowBlockStream,
-// apply_map) relinked against liblazypca_b200. Exit 0 = streaming agrees with
-// in-core to 1e-10 and the transform has the right shape.
+// apply_map, matrix files and a file row-block stream) relinked against
+// liblazypca_b200. Exit 0 = streaming agrees with in-core to 1e-10, the file
+// stream with the in-memory slices bitwise, and the transform has the right shape.
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -51,6 +52,21 @@ int main() {
     const auto back = lazypca::load_map_file("/tmp/lpca_shim_test.map");
     if (back.v.data()[5] != st.v.data()[5] || back.singular_values != st.singular_values || back.method != st.method)
       bad = 1;
+  }
+  // matrix_io: the same X through a MatrixMarket file and the file stream
+  lazypca::write_sparse_matrix_market_file(x, "/tmp/lpca_shim_test.mtx");
+  const auto xr = lazypca::read_sparse_matrix_market_file("/tmp/lpca_shim_test.mtx");
+  if (xr.values() != x.values() || xr.row_idx() != x.row_idx()) bad = 1;
+  {
+    c.method = lazypca::ReducerMethod::lazy_spca;
+    lazypca::SliceRowBlockStream slices(x, 400);
+    lazypca::MatrixMarketRowBlockStream file("/tmp/lpca_shim_test.mtx", 400);
+    const auto a = lazypca::reduce_lazy_spca_streaming(slices, c);
+    const auto b = lazypca::reduce_lazy_spca_streaming(file, c);
+    if (a.singular_values != b.singular_values || a.v.data()[7] != b.v.data()[7]) {
+      std::printf("file stream differs from slices\n");
+      bad = 1;
+    }
   }
   try {
     lazypca::SliceRowBlockStream empty(lazypca::SparseMatrix::from_csc(0, n, std::vector<lazypca::index_t>(n + 1, 0), {}, {}), 10);

@@ -19,6 +19,7 @@
 //                       read from where step 1 left them.
 // The reference's QL sweep (tridiag_eigh.cpp:108-170) is a sequential
 // bulge chase; steps 2-3 replace it with work that is parallel over eigenvalues.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -566,6 +567,185 @@ __global__ void __launch_bounds__(kTriBlkThreads) tridiag_reg_kernel(const doubl
   }
 }
 
+// Multi-CTA variant for l > 128 (one cooperative grid, grid-wide syncs): CTA q
+// of C holds rows q + C a (cyclic, so every CTA keeps work as the corner
+// shrinks) in shared memory. Per step two grid syncs: the owner of row i builds
+// reflector i from its row and publishes u, h (global, double-buffered by step
+// parity) -> every CTA forms p = A u / h for its rows and a u^T p partial ->
+// every CTA sums the partials in the same order, so K and q = p - K u are
+// bitwise equal everywhere and the rank-2 update keeps A exactly symmetric; the
+// owner of row i - 1 then builds the next reflector right after its update.
+constexpr int kCoopThreads = 256;
+
+struct CoopWork {
+  double* u;      // [2][l] reflectors by step parity
+  double* p;      // [2][l]
+  double* kpart;  // [2][C]
+  double* fpart;  // [C] Frobenius / asymmetry partials
+  double* apart;  // [C]
+  double* hsv;    // [2] 1/h by parity; [2] skip flags as doubles at hsv + 2
+};
+
+// kCluster: the C CTAs form one thread-block cluster (C <= 16) and meet at the
+// hardware cluster barrier instead of a grid-wide sync.
+template <bool kCluster>
+__global__ void __launch_bounds__(kCoopThreads) tridiag_coop_kernel(const double* __restrict__ a, int l,
+                                                                    double* __restrict__ refl, double* d, double* e,
+                                                                    double* h, double* norm_out, int* status,
+                                                                    double* gap, CoopWork wk) {
+  namespace cg = cooperative_groups;
+  struct Sync {
+    __device__ void sync() const {
+      if (kCluster) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      } else {
+        cg::this_grid().sync();
+      }
+    }
+  } grid;
+  extern __shared__ double rows_s[];  // [R][l], local row a = global row q + C a
+  __shared__ double red[66];
+  const int C = gridDim.x, q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int R = (l + C - 1) / C;
+  // load (exact symmetry from the upper triangle, tridiag_eigh.cpp:189-191)
+  double fro = 0.0, asym = 0.0;
+  for (int idx = tid; idx < R * l; idx += kCoopThreads) {
+    const int ra = idx / l, c = idx % l, r = q + C * ra;
+    double v = 0.0;
+    if (r < l) {
+      const double vrc = a[static_cast<size_t>(c) * l + r], vcr = a[static_cast<size_t>(r) * l + c];
+      fro += vrc * vrc;
+      asym = fmax(asym, fabs(vrc - vcr));
+      v = r <= c ? vrc : vcr;
+    }
+    rows_s[idx] = v;
+  }
+  fro = block_sum(fro, red);
+  asym = block_max(asym, red);
+  if (tid == 0) {
+    wk.fpart[q] = fro;
+    wk.apart[q] = asym;
+  }
+  grid.sync();
+  {
+    double f = 0.0, am = 0.0;
+    for (int c = 0; c < C; ++c) {
+      f += wk.fpart[c];
+      am = fmax(am, wk.apart[c]);
+    }
+    if (am > 1e-10 * sqrt(f)) {
+      if (q == 0 && tid == 0) {
+        status[0] = 2;
+        gap[0] = am;
+      }
+      return;  // grid-uniform
+    }
+  }
+  // owner of row ri builds reflector ri from its (updated) shared-memory row
+  auto build = [&](int ri) {
+    const int bb = ri & 1;
+    const double* row = rows_s + static_cast<size_t>(ri / C) * l;
+    double* u = wk.u + static_cast<size_t>(bb) * l;
+    if (ri == 1) {
+      if (tid == 0) {
+        e[1] = row[0];
+        h[1] = 0.0;
+        wk.hsv[2 + bb] = 1.0;
+      }
+      return;
+    }
+    double pa = 0.0, ps2 = 0.0;
+    for (int c = tid; c < ri; c += kCoopThreads) {
+      pa += fabs(row[c]);
+      ps2 += row[c] * row[c];
+    }
+    block_sum2(pa, ps2, red);
+    if (pa == 0.0) {
+      if (tid == 0) {
+        e[ri] = 0.0;
+        h[ri] = 0.0;
+        wk.hsv[2 + bb] = 1.0;
+      }
+      return;
+    }
+    const double inv = fast_rcp(pa);
+    const double sigma = ps2 * inv * inv;
+    const double f = row[ri - 1] * inv;
+    const double g = f >= 0.0 ? -sqrt(sigma) : sqrt(sigma);
+    const double hh = sigma - f * g;
+    for (int c = tid; c < ri; c += kCoopThreads) {
+      const double uv = c < ri - 1 ? row[c] * inv : f - g;
+      u[c] = uv;
+      refl[static_cast<size_t>(ri) * l + c] = uv;  // for the back-transformation
+    }
+    if (tid == 0) {
+      e[ri] = pa * g;
+      h[ri] = hh;
+      wk.hsv[bb] = fast_rcp(hh);
+      wk.hsv[2 + bb] = 0.0;
+    }
+  };
+  if (q == (l - 1) % C) build(l - 1);
+  for (int i = l - 1; i >= 1; --i) {
+    const int bb = i & 1;
+    grid.sync();  // reflector i published
+    const bool skip = wk.hsv[2 + bb] != 0.0;
+    const double* u = wk.u + static_cast<size_t>(bb) * l;
+    double* p = wk.p + static_cast<size_t>(bb) * l;
+    const int nra = i > q ? (i - q + C - 1) / C : 0;  // own active rows q + C a < i
+    if (!skip) {
+      const double hinv = wk.hsv[bb];
+      double pu = 0.0;
+      for (int ra = w; ra < nra; ra += kCoopThreads / 32) {  // warp per row
+        const double* row = rows_s + static_cast<size_t>(ra) * l;
+        double acc = 0.0;
+        for (int c = lane; c < i; c += 32) acc = fma(row[c], u[c], acc);
+        acc = warp_sum(acc) * hinv;
+        const int r = q + C * ra;
+        if (lane == 0) p[r] = acc;
+        pu = fma(u[r], acc, pu);  // lane-uniform value: counted once below
+      }
+      if (lane != 0) pu = 0.0;
+      pu = block_sum(pu, red);
+      if (tid == 0) wk.kpart[bb * C + q] = pu;
+    }
+    grid.sync();  // p and the K partials published
+    if (!skip) {
+      double ksum = 0.0;
+      for (int c = 0; c < C; ++c) ksum += wk.kpart[bb * C + c];
+      const double kk = ksum * (0.5 * wk.hsv[bb]);
+      for (int idx = tid; idx < nra * i; idx += kCoopThreads) {
+        const int ra = idx / i, c = idx % i, r = q + C * ra;
+        const double ur = u[r], uc = u[c];
+        const double qr = __dsub_rn(p[r], __dmul_rn(kk, ur)), qc = __dsub_rn(p[c], __dmul_rn(kk, uc));
+        double* x = rows_s + static_cast<size_t>(ra) * l + c;
+        *x = __dsub_rn(*x, __dadd_rn(__dmul_rn(ur, qc), __dmul_rn(qr, uc)));
+      }
+      __syncthreads();
+    }
+    if (i - 1 >= 1 && q == (i - 1) % C) build(i - 1);
+  }
+  for (int ra = tid; ra < R; ra += kCoopThreads) {
+    const int r = q + C * ra;
+    if (r < l) d[r] = rows_s[static_cast<size_t>(ra) * l + r];
+  }
+  if (q == 0 && tid == 0) e[0] = 0.0;
+  grid.sync();
+  if (q == 0) {
+    double tn = 0.0;
+    for (int k = tid; k < l; k += kCoopThreads) {
+      const double ek = k > 0 ? fabs(e[k]) : 0.0, ek1 = k + 1 < l ? fabs(e[k + 1]) : 0.0;
+      tn = fmax(tn, fabs(d[k]) + ek + ek1);
+    }
+    tn = block_max(tn, red);
+    if (tid == 0) {
+      norm_out[0] = tn;
+      status[0] = 0;
+      gap[0] = 0.0;
+    }
+  }
+}
+
 // ---- 2. multisection ---------------------------------------------------------------------
 // Number of eigenvalues of T strictly below x (Sturm sequence of T - x I);
 // ee[i] = e[i]^2, |q| kept >= pivmin (normal), so the reciprocal is finite.
@@ -1003,8 +1183,49 @@ void launch_eigh_tridiag(cudaStream_t s, const double* a, index_t l, double* eva
     LPCA_CUDA(cudaFuncSetAttribute(tridiag_reg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(amat)));
     tridiag_reg_kernel<4><<<1, kTriBlkThreads, amat, s>>>(a, li, refl, d, e, h, tn, status, gap);
   } else {
-    LPCA_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    tridiag_kernel<<<1, kTriThreads, smem, s>>>(a, li, refl, a_smem, d, e, h, tn, status, gap);
+    // one cluster of up to 16 CTAs (hardware barrier) while the rows fit their
+    // shared memory, else a cooperative grid of ~8 rows per CTA
+    const std::size_t row_bytes = static_cast<std::size_t>(l) * sizeof(double);
+    const bool cluster = static_cast<std::size_t>(ceil_div(l, 16)) * row_bytes <= 200 * 1024;
+    int C = cluster ? static_cast<int>(ceil_div(l, ceil_div(l, 16))) : static_cast<int>(ceil_div(l, 8));
+    C = cluster ? C : (C < 8 ? 8 : (C > 148 ? 148 : C));
+    const std::size_t csm = static_cast<std::size_t>(ceil_div(l, C)) * row_bytes;
+    if (csm <= 200 * 1024) {
+      CoopWork wk;
+      wk.u = scratch;  // the refinement's scratch is free during the tridiagonalisation
+      wk.p = wk.u + 2 * l;
+      wk.kpart = wk.p + 2 * l;
+      wk.fpart = wk.kpart + 2 * C;
+      wk.apart = wk.fpart + C;
+      wk.hsv = wk.apart + C;
+      if (cluster) {
+        LPCA_CUDA(cudaFuncSetAttribute(tridiag_coop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(csm)));
+        LPCA_CUDA(cudaFuncSetAttribute(tridiag_coop_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C);
+        cfg.blockDim = dim3(kCoopThreads);
+        cfg.dynamicSmemBytes = csm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        LPCA_CUDA(cudaLaunchKernelEx(&cfg, tridiag_coop_kernel<true>, a, li, refl, d, e, h, tn, status, gap, wk));
+      } else {
+        LPCA_CUDA(cudaFuncSetAttribute(tridiag_coop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(csm)));
+        void* args[] = {&a, const_cast<int*>(&li), &refl, &d, &e, &h, &tn, &status, &gap, &wk};
+        LPCA_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tridiag_coop_kernel<false>), dim3(C),
+                                              dim3(kCoopThreads), args, csm, s));
+      }
+    } else {
+      LPCA_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      tridiag_kernel<<<1, kTriThreads, smem, s>>>(a, li, refl, a_smem, d, e, h, tn, status, gap);
+    }
   }
   const int warps_per_block = 4;
   const unsigned gblocks = static_cast<unsigned>(ceil_div(l, warps_per_block));

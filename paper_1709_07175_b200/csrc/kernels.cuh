@@ -226,6 +226,8 @@ void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rin
                          int* status);
 // g_ii += c * trace(g) (shifted CholeskyQR's first pass).
 void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c);
+// out[0] = flag[0] != 0 (an int flag made summable over ranks).
+void launch_flag_to_f64(cudaStream_t s, const int* flag, double* out);
 // F <- L^{-1} F  ==  (Z R^{-1})^T for Z = F^T; rinv = L^{-T} upper, F l x n col-major.
 void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
                          double* tmp);

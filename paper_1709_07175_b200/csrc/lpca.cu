@@ -878,6 +878,13 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     ctx.pass_slot = 12;
     xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
     ctx.pass_slot = -1;
+    double* xovf_all = nullptr;  // the flag summed over ranks: every rank reruns, or none
+    if (xovf && ctx.world > 1) {
+      xovf_all = ctx.get<double>("xovf.all", 1);
+      launch_flag_to_f64(ctx.stream, xovf, xovf_all);
+      LPCA_LAUNCHED(ctx);
+      ctx.allreduce(xovf_all, 1);
+    }
     xs.use = f16;
     ev.mark(1);
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
@@ -974,7 +981,13 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
     if (xovf) {
       int flagged = 0;
-      LPCA_CUDA(cudaMemcpy(&flagged, xovf, sizeof(int), cudaMemcpyDeviceToHost));
+      if (xovf_all) {
+        double all = 0.0;
+        LPCA_CUDA(cudaMemcpy(&all, xovf_all, sizeof(double), cudaMemcpyDeviceToHost));
+        flagged = all > 0.0;
+      } else {
+        LPCA_CUDA(cudaMemcpy(&flagged, xovf, sizeof(int), cudaMemcpyDeviceToHost));
+      }
       if (flagged) {  // some row's values outgrew its run's first-stage scale: redo with the scan
         delete map;
         ctx.force_scan = true;

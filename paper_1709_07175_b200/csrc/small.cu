@@ -616,6 +616,12 @@ __global__ void add_trace_shift_kernel(double* g, index_t l, double c) {
 }
 }  // namespace
 
+namespace {
+__global__ void flag_to_f64_kernel(const int* flag, double* out) { out[0] = flag[0] != 0 ? 1.0 : 0.0; }
+}  // namespace
+
+void launch_flag_to_f64(cudaStream_t s, const int* flag, double* out) { flag_to_f64_kernel<<<1, 1, 0, s>>>(flag, out); }
+
 void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c) {
   add_trace_shift_kernel<<<1, 1024, 0, s>>>(g, l, c);
 }

@@ -1,6 +1,10 @@
 // Projection generation, synthetic data and layout helpers.
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <unordered_set>
+#include <vector>
+
 #include "kernels.cuh"
 #include "rng.cuh"
 
@@ -9,26 +13,71 @@ namespace lpca {
 namespace {
 
 constexpr int kOmegaThreads = 256;
-constexpr int kOmegaChunk = 4096;  // raw draws staged per round (32 KB of smem)
+constexpr int kOmegaSeg = 128;                   // draws per lane per round
+constexpr int kOmegaChunk = 32 * kOmegaSeg;      // draws per round (32 KB of smem)
+constexpr int kJumps = 33;                       // T^(128 L), L = 0..31, and T^4096
+
+// xoshiro256** is linear over GF(2) in its 256-bit state: advancing J draws is
+// a fixed 256 x 256 bit matrix T^J. Column j of g_jump[k] is T^J e_j (four
+// 64-bit words, s0..s3). With them the 32 lanes of a warp start at draws
+// 128 L of their column's stream and walk 128 draws each, instead of one lane
+// walking all of them: the same raw sequence. Lane L makes one jump, T^(128 L)
+// (its own matrix), and every further round one T^4096.
+__device__ std::uint64_t g_jump[kJumps][256][4];
+
+__device__ __forceinline__ void jump_state(const std::uint64_t (&m)[256][4], Xoshiro& x) {
+  const std::uint64_t in[4] = {x.s0, x.s1, x.s2, x.s3};
+  std::uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+#pragma unroll 4
+  for (int j = 0; j < 256; ++j) {
+    const std::uint64_t bit = (in[j >> 6] >> (j & 63)) & 1ull;
+    const std::uint64_t mask = 0ull - bit;
+    o0 ^= m[j][0] & mask;
+    o1 ^= m[j][1] & mask;
+    o2 ^= m[j][2] & mask;
+    o3 ^= m[j][3] & mask;
+  }
+  x.s0 = o0;
+  x.s1 = o1;
+  x.s2 = o2;
+  x.s3 = o3;
+}
+
+// Raw draws [base, base + 4096) of `col`'s stream into raw[], round `round`
+// (base = 4096 round): lane L of warp 0 jumps to draw base + 128 L.
+__device__ __forceinline__ void omega_raw_round(Xoshiro& lane_state, int round, index_t n, std::uint64_t* raw) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    if (round > 0) jump_state(g_jump[32], lane_state);  // +4096 from this lane's previous round start
+    Xoshiro x = lane_state;
+    const index_t base = static_cast<index_t>(round) * kOmegaChunk + lane * kOmegaSeg;
+    for (int t = 0; t < kOmegaSeg && base + t < n; ++t) raw[lane * kOmegaSeg + t] = x.next();
+  }
+}
+
+__device__ __forceinline__ Xoshiro omega_lane_start(std::uint64_t seed, index_t col) {
+  Xoshiro x = column_stream(seed, static_cast<std::uint64_t>(col));
+  const int lane = threadIdx.x & 31;
+  if (lane > 0) jump_state(g_jump[lane], x);
+  return x;
+}
 
 // One CTA per projection column (gen_gaussian runs one task per column,
-// projection.cpp:71-84). Lane 0 walks the column's xoshiro256** stream — the
-// only sequential part, integer ops only — staging raw 64-bit draws in shared
-// memory; then the whole CTA maps them through normal_icdf and writes the
-// column with coalesced stores.
+// projection.cpp:71-84): warp 0 produces the column's raw 64-bit draws (32
+// lanes at jumped stream positions), then the whole CTA maps them through
+// normal_icdf and writes the column with coalesced stores.
 __global__ void __launch_bounds__(kOmegaThreads) omega_gaussian_kernel(index_t n, std::uint64_t seed,
                                                                        double* out, index_t ld) {
   __shared__ std::uint64_t raw[kOmegaChunk];
   const index_t col = blockIdx.x;
-  Xoshiro rng = column_stream(seed, static_cast<std::uint64_t>(col));
+  Xoshiro st(0);
+  if (threadIdx.x < 32) st = omega_lane_start(seed, col);  // warp 0 only
   double* dst = out + col * ld;
-  for (index_t base = 0; base < n; base += kOmegaChunk) {
+  for (index_t base = 0, round = 0; base < n; base += kOmegaChunk, ++round) {
     const int cnt = static_cast<int>(n - base < kOmegaChunk ? n - base : kOmegaChunk);
-    if (threadIdx.x == 0)
-      for (int i = 0; i < cnt; ++i) raw[i] = rng.next();
+    omega_raw_round(st, static_cast<int>(round), n, raw);
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += kOmegaThreads)
-      dst[base + i] = normal_icdf(u64_to_uniform(raw[i]));
+    for (int i = threadIdx.x; i < cnt; i += kOmegaThreads) dst[base + i] = normal_icdf(u64_to_uniform(raw[i]));
     __syncthreads();
   }
 }
@@ -40,13 +89,13 @@ __global__ void __launch_bounds__(kOmegaThreads) omega_sparse_kernel(index_t n, 
                                                                      index_t ld) {
   __shared__ std::uint64_t raw[kOmegaChunk];
   const index_t col = blockIdx.x;
-  Xoshiro rng = column_stream(seed, static_cast<std::uint64_t>(col));
+  Xoshiro st(0);
+  if (threadIdx.x < 32) st = omega_lane_start(seed, col);  // warp 0 only
   double* dst = out + col * ld;
   const double half = density / 2.0;
-  for (index_t base = 0; base < n; base += kOmegaChunk) {
+  for (index_t base = 0, round = 0; base < n; base += kOmegaChunk, ++round) {
     const int cnt = static_cast<int>(n - base < kOmegaChunk ? n - base : kOmegaChunk);
-    if (threadIdx.x == 0)
-      for (int i = 0; i < cnt; ++i) raw[i] = rng.next();
+    omega_raw_round(st, static_cast<int>(round), n, raw);
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += kOmegaThreads) {
       const double u = u64_to_uniform(raw[i]);
@@ -54,6 +103,46 @@ __global__ void __launch_bounds__(kOmegaThreads) omega_sparse_kernel(index_t n, 
     }
     __syncthreads();
   }
+}
+
+// Host: the jump matrices, computed once and uploaded to each device used.
+void xoshiro_step(std::uint64_t (&s)[4]) {
+  const std::uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = (s[3] << 45) | (s[3] >> 19);
+}
+
+void ensure_jump_tables(cudaStream_t s) {
+  static std::vector<std::uint64_t> host;  // [kJumps][256][4]
+  static std::mutex mu;
+  static std::unordered_set<int> ready;
+  int dev = 0;
+  LPCA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (ready.count(dev)) return;
+  if (host.empty()) {
+    host.assign(static_cast<std::size_t>(kJumps) * 256 * 4, 0);
+    // T^(128 L) column by column, each from the previous L's by 128 more steps
+    for (int j = 0; j < 256; ++j) {
+      std::uint64_t st[4] = {0, 0, 0, 0};
+      st[j >> 6] = 1ull << (j & 63);
+      for (int L = 0; L < 32; ++L) {
+        if (L > 0)
+          for (int t = 0; t < kOmegaSeg; ++t) xoshiro_step(st);
+        for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(L) * 256 + j) * 4 + w] = st[w];
+      }
+      for (int t = 0; t < kOmegaSeg; ++t) xoshiro_step(st);  // 32 * 128 = 4096
+      for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(32) * 256 + j) * 4 + w] = st[w];
+    }
+  }
+  LPCA_CUDA(cudaMemcpyToSymbolAsync(g_jump, host.data(), host.size() * sizeof(std::uint64_t), 0,
+                                    cudaMemcpyHostToDevice, s));
+  LPCA_CUDA(cudaStreamSynchronize(s));  // host buffer is static; the sync keeps the first use simple
+  ready.insert(dev);
 }
 
 // ---- synthetic low-rank data --------------------------------------------------
@@ -234,12 +323,14 @@ int grid_for(index_t work, int threads) {
 void launch_omega_gaussian(cudaStream_t s, index_t n, index_t l, std::uint64_t seed, double* out,
                            index_t ld) {
   if (l <= 0 || n <= 0) return;
+  ensure_jump_tables(s);
   omega_gaussian_kernel<<<static_cast<unsigned>(l), kOmegaThreads, 0, s>>>(n, seed, out, ld);
 }
 
 void launch_omega_very_sparse(cudaStream_t s, index_t n, index_t l, double density,
                               std::uint64_t seed, double* out, index_t ld) {
   if (l <= 0 || n <= 0) return;
+  ensure_jump_tables(s);
   omega_sparse_kernel<<<static_cast<unsigned>(l), kOmegaThreads, 0, s>>>(n, density, seed, out, ld);
 }
 

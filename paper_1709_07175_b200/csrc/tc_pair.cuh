@@ -48,6 +48,7 @@ struct PairArgs {
   int m, n;          // X is m x n
   int npad;          // UMMA N (multiple of 16); each CTA holds npad / 2 rows of B
   int stages, aslots, nrb, run_stages;
+  int half_slots;  // fp16: A ring of half-stage slots (32 columns, K = 32) when only one full slot fits
   uint32_t tmem_cols;
   int items;
   int chunk_rows;    // XTU: rows per chunk (multiple of 128)
@@ -150,6 +151,26 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
   "}"
+
+// Half a stage (K = 32, fp16): 6 MMAs from a 32-column half slot (hi 16, lo 16).
+#define LPCA_PAIR_HALF(KIND)                                                                               \
+  "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"                                \
+  " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"                                                              \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %3, %5, p;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%2], %3, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
+  " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"                   \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
+  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  "}"
+__device__ __forceinline__ void mma_half_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                              uint32_t idesc, uint32_t acc_first) {
+  asm volatile(LPCA_PAIR_HALF("f16")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first),
+               "r"(0u)
+               : "memory");
+}
+#undef LPCA_PAIR_HALF
 
 template <bool kHalf>
 __device__ __forceinline__ void mma_stage_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
@@ -389,6 +410,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint64_t bh = desc0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
             const uint64_t bl = bh + static_cast<uint64_t>(bh_bytes >> 4);
+            if (kHalf && a.half_slots) {
+              // two half slots per stage: the converters fill one while the
+              // MMAs read the other (B rows advance 4 descriptor units per half)
+              for (int hh = 0; hh < 2; ++hh) {
+                if (hh == 1) {
+                  PP_T0();
+                  mbar_wait(&conv[aslot], aphase, 3);
+                  PP_ADD(3);
+                  tc_fence_after();
+                }
+                const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 32);
+                if (elect_one()) {
+                  mma_half_pair(d, at, at + 16, bh + 4 * hh, bl + 4 * hh, idesc, (k != q0 || hh) ? 1u : 0u);
+                  if (hh == 1) mma_commit_pair(&empty[stage]);
+                  mma_commit_pair(&aempty[aslot]);
+                }
+                __syncwarp();
+                ring_advance(aslot, aphase, AS);
+              }
+              ring_advance(stage, phase, S);
+              continue;
+            }
             const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 64);
             if (elect_one()) {
               mma_stage_pair<kHalf>(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u);
@@ -489,7 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           tc_fence_after();
           const uint8_t* xt = smem + stage * stage_bytes;
-          const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * 64);
+          const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * (a.half_slots ? 32 : 64));
           if (kHalf) {
             float v0[32], v1[32];
 #ifdef LPCA_PAIR_PROF
@@ -522,12 +565,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
             float hi[16], lo[16];
-            split_f16_32(v0, hi, lo);
-            tmem_st16(at, hi);
-            tmem_st16(at + 32, lo);
-            split_f16_32(v1, hi, lo);
-            tmem_st16(at + 16, hi);
-            tmem_st16(at + 48, lo);
+            if (a.half_slots) {  // half 0 -> this slot, then half 1 -> the next one
+              split_f16_32(v0, hi, lo);
+              tmem_st16(at, hi);
+              tmem_st16(at + 16, lo);
+              tmem_st_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&conv[aslot]), 0));
+              ring_advance(aslot, aphase, AS);
+              mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+              tc_fence_after();
+              const uint32_t at1 = lane_base + a_col0 + static_cast<uint32_t>(aslot * 32);
+              split_f16_32(v1, hi, lo);
+              tmem_st16(at1, hi);
+              tmem_st16(at1 + 16, lo);
+            } else {
+              split_f16_32(v0, hi, lo);
+              tmem_st16(at, hi);
+              tmem_st16(at + 32, lo);
+              split_f16_32(v1, hi, lo);
+              tmem_st16(at + 16, hi);
+              tmem_st16(at + 48, lo);
+            }
 #ifdef LPCA_PAIR_PROF
             if (q == 0 && lane == 0) pp[5] += clock64() - pp_c0;
 #endif

@@ -1,6 +1,6 @@
 """Role timers of the 2-SM pass kernel: load a library built with -DLPCA_PAIR_PROF
 (LPCA_LIB_PATH), run c2 fit+transform steps, print per-role cycle shares.
-Usage: LPCA_LIB_PATH=abtest/prof.so python tools/pair_prof.py [steps]"""
+Usage: LPCA_LIB_PATH=abtest/prof.so python tools/pair_prof.py [steps] [config] [rows]"""
 import ctypes as C
 import sys
 
@@ -11,15 +11,17 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_1709_07175_b200 as lp  # noqa: E402
 
-cfg = dict(bench.CONFIGS["c2"])
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cfg = dict(bench.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c2"])
+if len(sys.argv) > 3:
+    cfg["m"] = int(sys.argv[3])
 ctx = lp.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 x = torch.empty((cfg["m"], cfg["n"]), dtype=torch.float32, device="cuda")
 lp.synth_lowrank(x, 0, cfg["r"], cfg["rho"], 0.01, bench.SEED_X, ctx=ctx)
 y = torch.empty((cfg["m"], cfg["k"]), dtype=torch.float32, device="cuda")
 conf = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=cfg["k"], l=cfg["l"],
-                        projection=lp.ProjectionSpec(seed=bench.SEED_OMEGA), power_iters=0)
+                        projection=lp.ProjectionSpec(seed=bench.SEED_OMEGA), power_iters=cfg["q"])
 fn = ctx.lib.lpca_debug_pair_prof
 fn.argtypes = [C.c_void_p, C.c_int]
 buf = np.zeros(32, dtype=np.uint64)

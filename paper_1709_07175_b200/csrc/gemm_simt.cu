@@ -9,6 +9,8 @@
 // which reproduces the reference's spmm / gemm_t bit for bit on dense input.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace lpca {
@@ -198,12 +200,151 @@ __global__ void reduce_partials_kernel(const double* __restrict__ part, index_t 
   }
 }
 
+// ---- fp64, free summation order: 128 x 128 CTA tiles, 8 x 8 DFMA register tiles
+// per thread (16 shared loads per 64 DFMA instead of 8 per 16), the next K slab
+// prefetched into registers while the current one is multiplied. Used for the
+// fp64 passes when the reference's exact order is not requested (c5).
+constexpr int kFT = 128, kFK = 16;
+
+// A slab [kFK][kFT] and B slab [kFK][kFT] in shared memory (padded rows).
+struct F64Slabs {
+  double a[kFK][kFT + 1];
+  double b[kFK][kFT + 1];
+};
+
+__device__ __forceinline__ void f64_tile_mma(const F64Slabs& sm, int tx, int ty, double (&acc)[8][8]) {
+#pragma unroll
+  for (int kk = 0; kk < kFK; ++kk) {
+    double av[8], bv[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) av[a] = sm.a[kk][ty + 16 * a];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) bv[b] = sm.b[kk][tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+  }
+}
+
+// out[i*ors + c*ocs] = sum_k X[i, k] W[c, k] (X row-major ldx, W as w[c*ldw + k]).
+template <typename TO>
+__global__ void __launch_bounds__(256, 1) xw_f64_fast_kernel(const double* __restrict__ x, index_t m, index_t n,
+                                                             index_t ldx, const double* __restrict__ w, index_t wc,
+                                                             index_t ldw, TO* __restrict__ out, index_t ors,
+                                                             index_t ocs) {
+  extern __shared__ double f64_smem[];
+  F64Slabs& sm = *reinterpret_cast<F64Slabs*>(f64_smem);
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const index_t i0 = static_cast<index_t>(blockIdx.x) * kFT, c0 = static_cast<index_t>(blockIdx.y) * kFT;
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  double ra[8], rb[8];  // this thread's share of the next slab: rows/cols e / 16, k e % 16
+  auto fetch = [&](index_t k0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + 256 * q, r = e / kFK, kk = e % kFK;
+      const index_t gk = k0 + kk, gi = i0 + r, gc = c0 + r;
+      ra[q] = (gi < m && gk < n) ? x[gi * ldx + gk] : 0.0;
+      rb[q] = (gc < wc && gk < n) ? w[gc * ldw + gk] : 0.0;
+    }
+  };
+  fetch(0);
+  for (index_t k0 = 0; k0 < n; k0 += kFK) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + 256 * q, r = e / kFK, kk = e % kFK;
+      sm.a[kk][r] = ra[q];
+      sm.b[kk][r] = rb[q];
+    }
+    __syncthreads();
+    if (k0 + kFK < n) fetch(k0 + kFK);  // in flight while this slab is multiplied
+    f64_tile_mma(sm, tx, ty, acc);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const index_t gi = i0 + ty + 16 * a;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const index_t gc = c0 + tx + 16 * b;
+      if (gc < wc) out[gi * ors + gc * ocs] = static_cast<TO>(acc[a][b]);
+    }
+  }
+}
+
+// part[c][j*l + r] = sum_{i in chunk c} U[i, r] X[i, j] (U ldu, X ldx row-major).
+__global__ void __launch_bounds__(256, 1) utx_f64_fast_kernel(const double* __restrict__ u, index_t ldu,
+                                                              const double* __restrict__ x, index_t ldx, index_t m,
+                                                              index_t l, index_t n, index_t chunk_rows,
+                                                              double* __restrict__ part) {
+  extern __shared__ double f64_smem[];
+  F64Slabs& sm = *reinterpret_cast<F64Slabs*>(f64_smem);
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const index_t j0 = static_cast<index_t>(blockIdx.x) * kFT, r0 = static_cast<index_t>(blockIdx.y) * kFT;
+  const index_t chunk = blockIdx.z;
+  const index_t row_begin = chunk * chunk_rows, row_end = row_begin + chunk_rows < m ? row_begin + chunk_rows : m;
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  double ra[8], rb[8];  // slab element e: row kk = e / 128, column e % 128
+  auto fetch = [&](index_t i0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + 256 * q, kk = e / kFT, c = e % kFT;
+      const index_t gi = i0 + kk;
+      const bool in = gi < row_end;
+      ra[q] = (in && r0 + c < l) ? u[gi * ldu + r0 + c] : 0.0;
+      rb[q] = (in && j0 + c < n) ? x[gi * ldx + j0 + c] : 0.0;
+    }
+  };
+  fetch(row_begin);
+  for (index_t i0 = row_begin; i0 < row_end; i0 += kFK) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + 256 * q, kk = e / kFT, c = e % kFT;
+      sm.a[kk][c] = ra[q];
+      sm.b[kk][c] = rb[q];
+    }
+    __syncthreads();
+    if (i0 + kFK < row_end) fetch(i0 + kFK);
+    f64_tile_mma(sm, tx, ty, acc);
+    __syncthreads();
+  }
+  double* dst = part + chunk * l * n;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const index_t r = r0 + ty + 16 * a;
+    if (r >= l) continue;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const index_t j = j0 + tx + 16 * b;
+      if (j < n) dst[j * l + r] = acc[a][b];
+    }
+  }
+}
+
 }  // namespace
 
 template <typename T, typename TO>
 void launch_xw_simt(cudaStream_t s, const T* x, index_t m, index_t n, index_t ldx, const T* w,
                     index_t wc, index_t ldw, TO* out, index_t ors, index_t ocs, bool exact) {
   if (m <= 0 || wc <= 0) return;
+  if constexpr (std::is_same<T, double>::value) {
+    if (!exact && wc > 64) {
+      const dim3 g(static_cast<unsigned>(ceil_div(m, kFT)), static_cast<unsigned>(ceil_div(wc, kFT)));
+      const int smem = static_cast<int>(sizeof(F64Slabs));
+      LPCA_CUDA(cudaFuncSetAttribute(xw_f64_fast_kernel<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      xw_f64_fast_kernel<TO><<<g, 256, smem, s>>>(x, m, n, ldx, w, wc, ldw, out, ors, ocs);
+      return;
+    }
+  }
   dim3 grid(static_cast<unsigned>(ceil_div(m, kBM)), static_cast<unsigned>(ceil_div(wc, kBN)));
   if (exact)
     xw_simt_kernel<T, TO, true><<<grid, kThreads, 0, s>>>(x, m, n, ldx, w, wc, ldw, out, ors, ocs);
@@ -215,6 +356,16 @@ template <typename T>
 void launch_utx_simt(cudaStream_t s, const T* u, index_t ldu, const T* x, index_t ldx, index_t m,
                      index_t l, index_t n, index_t chunk_rows, double* part, bool exact) {
   const index_t chunks = ceil_div(m, chunk_rows);
+  if constexpr (std::is_same<T, double>::value) {
+    if (!exact && l > 64 && n > 64) {
+      const dim3 g(static_cast<unsigned>(ceil_div(n, kFT)), static_cast<unsigned>(ceil_div(l, kFT)),
+                   static_cast<unsigned>(chunks));
+      const int smem = static_cast<int>(sizeof(F64Slabs));
+      LPCA_CUDA(cudaFuncSetAttribute(utx_f64_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      utx_f64_fast_kernel<<<g, 256, smem, s>>>(u, ldu, x, ldx, m, l, n, chunk_rows, part);
+      return;
+    }
+  }
   dim3 grid(static_cast<unsigned>(ceil_div(n, kBN)), static_cast<unsigned>(ceil_div(l, kBM)),
             static_cast<unsigned>(chunks));
   if (exact)

@@ -633,7 +633,10 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
     launch_utx_tc_planes(ctx.stream, u.hi, u.lo, u.ldt, static_cast<const float*>(x.p), x.ld, m, l, n, part,
                          ctx.num_sms);
   } else {
-    chunks = pick_chunks(ctx, m, ceil_div(n, 64) * ceil_div(l, 64), exact);
+    // the fp64 fast kernel runs 128 x 128 tiles, one CTA per SM (gemm_simt.cu)
+    const bool fast64 = x.dtype == 8 && !exact && l > 64 && n > 64;
+    chunks = fast64 ? pick_chunks(ctx, m, ceil_div(n, 128) * ceil_div(l, 128) / 2, exact)
+                    : pick_chunks(ctx, m, ceil_div(n, 64) * ceil_div(l, 64), exact);
     const index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
     chunks = ceil_div(m, chunk_rows);
     part = chunks == 1 ? f : ctx.get<double>("f.part", chunks * l * n);

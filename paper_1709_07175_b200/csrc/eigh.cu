@@ -1169,7 +1169,6 @@ void launch_eigh_tridiag(cudaStream_t s, const double* a, index_t l, double* eva
   double* e = d + l;
   double* h = e + l;
   double* tn = h + l;
-  unsigned char* piv = reinterpret_cast<unsigned char*>(tn + 8);
   const std::size_t amat = static_cast<std::size_t>(l * l) * sizeof(double);
   const std::size_t vecs = static_cast<std::size_t>(3 * l) * sizeof(double);
   const int a_smem = amat + vecs <= 200 * 1024 ? 1 : 0;

@@ -28,9 +28,8 @@ conf = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=k, l=l,
 TM = lp.ReducerTimings() if "--timings" in sys.argv else None
 
 
-def step():
-    mp = lp.reduce_lazy_spca(x, conf, timings=TM, ctx=ctx)
-    lp.apply_map(mp, x, out=y, timings=TM, ctx=ctx)
+def step():  # the bench step: one fused fit + transform call
+    lp.fit_transform(x, conf, timings=TM, ctx=ctx, out=y)
 
 
 for _ in range(3):

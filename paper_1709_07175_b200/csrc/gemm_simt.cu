@@ -200,10 +200,10 @@ __global__ void reduce_partials_kernel(const double* __restrict__ part, index_t 
   }
 }
 
-// ---- fp64, free summation order: 128 x 128 CTA tiles, 8 x 8 DFMA register tiles
-// per thread (16 shared loads per 64 DFMA instead of 8 per 16), the next K slab
-// prefetched into registers while the current one is multiplied. Used for the
-// fp64 passes when the reference's exact order is not requested (c5).
+// ---- fp64, free summation order: 128 x 128 CTA tiles on the fp64 tensor cores
+// (DMMA m8n8k4), the next K slab prefetched into registers while the current
+// one is multiplied. Used for the fp64 passes when the reference's exact order
+// is not requested (c5).
 constexpr int kFT = 128, kFK = 16;
 
 // A slab [kFK][kFT] and B slab [kFK][kFT] in shared memory (padded rows).
@@ -212,18 +212,30 @@ struct F64Slabs {
   double b[kFK][kFT + 1];
 };
 
-__device__ __forceinline__ void f64_tile_mma(const F64Slabs& sm, int tx, int ty, double (&acc)[8][8]) {
+// The 128 x 128 tile on the fp64 tensor cores (mma.sync m8n8k4 f64): warp w
+// owns rows 64 (w / 4) .. +64 and columns 32 (w % 4) .. +32 as 8 x 4 tiles of
+// 8 x 8; per K = 4 step a thread loads 8 A and 4 B values for 32 MMAs.
+// Fragments: A[g][t], B[t][g], C[g][2t + {0,1}] with g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void f64_tile_mma(const F64Slabs& sm, int warp, int lane, double (&acc)[8][4][2]) {
+  const int g = lane >> 2, t = lane & 3;
+  const int rbase = 64 * (warp >> 2) + g, cbase = 32 * (warp & 3) + g;
 #pragma unroll
-  for (int kk = 0; kk < kFK; ++kk) {
-    double av[8], bv[8];
+  for (int k = 0; k < kFK; k += 4) {
+    double av[8], bv[4];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) av[a] = sm.a[kk][ty + 16 * a];
+    for (int rb = 0; rb < 8; ++rb) av[rb] = sm.a[k + t][rbase + 8 * rb];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) bv[b] = sm.b[kk][tx + 16 * b];
+    for (int cb = 0; cb < 4; ++cb) bv[cb] = sm.b[k + t][cbase + 8 * cb];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int rb = 0; rb < 8; ++rb)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      for (int cb = 0; cb < 4; ++cb) dmma_8x8x4(acc[rb][cb], av[rb], bv[cb]);
   }
 }
 
@@ -235,13 +247,13 @@ __global__ void __launch_bounds__(256, 1) xw_f64_fast_kernel(const double* __res
                                                              index_t ocs) {
   extern __shared__ double f64_smem[];
   F64Slabs& sm = *reinterpret_cast<F64Slabs*>(f64_smem);
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const index_t i0 = static_cast<index_t>(blockIdx.x) * kFT, c0 = static_cast<index_t>(blockIdx.y) * kFT;
-  double acc[8][8];
+  double acc[8][4][2];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double ra[8], rb[8];  // this thread's share of the next slab: rows/cols e / 16, k e % 16
   auto fetch = [&](index_t k0) {
 #pragma unroll
@@ -262,18 +274,21 @@ __global__ void __launch_bounds__(256, 1) xw_f64_fast_kernel(const double* __res
     }
     __syncthreads();
     if (k0 + kFK < n) fetch(k0 + kFK);  // in flight while this slab is multiplied
-    f64_tile_mma(sm, tx, ty, acc);
+    f64_tile_mma(sm, warp, lane, acc);
     __syncthreads();
   }
+  const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const index_t gi = i0 + ty + 16 * a;
+  for (int rb = 0; rb < 8; ++rb) {
+    const index_t gi = i0 + 64 * (warp >> 2) + 8 * rb + g;
     if (gi >= m) continue;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const index_t gc = c0 + tx + 16 * b;
-      if (gc < wc) out[gi * ors + gc * ocs] = static_cast<TO>(acc[a][b]);
-    }
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const index_t gc = c0 + 32 * (warp & 3) + 8 * cb + 2 * t + h;
+        if (gc < wc) out[gi * ors + gc * ocs] = static_cast<TO>(acc[rb][cb][h]);
+      }
   }
 }
 
@@ -284,15 +299,15 @@ __global__ void __launch_bounds__(256, 1) utx_f64_fast_kernel(const double* __re
                                                               double* __restrict__ part) {
   extern __shared__ double f64_smem[];
   F64Slabs& sm = *reinterpret_cast<F64Slabs*>(f64_smem);
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const index_t j0 = static_cast<index_t>(blockIdx.x) * kFT, r0 = static_cast<index_t>(blockIdx.y) * kFT;
   const index_t chunk = blockIdx.z;
   const index_t row_begin = chunk * chunk_rows, row_end = row_begin + chunk_rows < m ? row_begin + chunk_rows : m;
-  double acc[8][8];
+  double acc[8][4][2];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double ra[8], rb[8];  // slab element e: row kk = e / 128, column e % 128
   auto fetch = [&](index_t i0) {
 #pragma unroll
@@ -314,19 +329,22 @@ __global__ void __launch_bounds__(256, 1) utx_f64_fast_kernel(const double* __re
     }
     __syncthreads();
     if (i0 + kFK < row_end) fetch(i0 + kFK);
-    f64_tile_mma(sm, tx, ty, acc);
+    f64_tile_mma(sm, warp, lane, acc);
     __syncthreads();
   }
   double* dst = part + chunk * l * n;
+  const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const index_t r = r0 + ty + 16 * a;
+  for (int rb = 0; rb < 8; ++rb) {
+    const index_t r = r0 + 64 * (warp >> 2) + 8 * rb + g;
     if (r >= l) continue;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const index_t j = j0 + tx + 16 * b;
-      if (j < n) dst[j * l + r] = acc[a][b];
-    }
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const index_t j = j0 + 32 * (warp & 3) + 8 * cb + 2 * t + h;
+        if (j < n) dst[j * l + r] = acc[rb][cb][h];
+      }
   }
 }
 

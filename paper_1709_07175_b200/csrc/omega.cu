@@ -18,24 +18,29 @@ constexpr int kOmegaChunk = 32 * kOmegaSeg;      // draws per round (32 KB of sm
 constexpr int kJumps = 33;                       // T^(128 L), L = 0..31, and T^4096
 
 // xoshiro256** is linear over GF(2) in its 256-bit state: advancing J draws is
-// a fixed 256 x 256 bit matrix T^J. Column j of g_jump[k] is T^J e_j (four
+// a fixed 256 x 256 bit matrix T^J. Column j of matrix k is T^J e_j (four
 // 64-bit words, s0..s3). With them the 32 lanes of a warp start at draws
 // 128 L of their column's stream and walk 128 draws each, instead of one lane
 // walking all of them: the same raw sequence. Lane L makes one jump, T^(128 L)
 // (its own matrix), and every further round one T^4096.
-__device__ std::uint64_t g_jump[kJumps][256][4];
+// Stored column-interleaved, g_jump[j][k][w]: for a fixed column j the 32
+// lanes' matrices (k = lane) are contiguous, so each step of the product is
+// one coalesced 1 KB read across the warp.
+__device__ std::uint64_t g_jump[256][kJumps][4];
 
-__device__ __forceinline__ void jump_state(const std::uint64_t (&m)[256][4], Xoshiro& x) {
+__device__ __forceinline__ void jump_state(int k, Xoshiro& x) {
   const std::uint64_t in[4] = {x.s0, x.s1, x.s2, x.s3};
   std::uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
 #pragma unroll 4
   for (int j = 0; j < 256; ++j) {
     const std::uint64_t bit = (in[j >> 6] >> (j & 63)) & 1ull;
     const std::uint64_t mask = 0ull - bit;
-    o0 ^= m[j][0] & mask;
-    o1 ^= m[j][1] & mask;
-    o2 ^= m[j][2] & mask;
-    o3 ^= m[j][3] & mask;
+    const ulonglong2 lo = *reinterpret_cast<const ulonglong2*>(&g_jump[j][k][0]);
+    const ulonglong2 hi = *reinterpret_cast<const ulonglong2*>(&g_jump[j][k][2]);
+    o0 ^= lo.x & mask;
+    o1 ^= lo.y & mask;
+    o2 ^= hi.x & mask;
+    o3 ^= hi.y & mask;
   }
   x.s0 = o0;
   x.s1 = o1;
@@ -48,7 +53,7 @@ __device__ __forceinline__ void jump_state(const std::uint64_t (&m)[256][4], Xos
 __device__ __forceinline__ void omega_raw_round(Xoshiro& lane_state, int round, index_t n, std::uint64_t* raw) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
-    if (round > 0) jump_state(g_jump[32], lane_state);  // +4096 from this lane's previous round start
+    if (round > 0) jump_state(32, lane_state);  // +4096 from this lane's previous round start
     Xoshiro x = lane_state;
     const index_t base = static_cast<index_t>(round) * kOmegaChunk + lane * kOmegaSeg;
     for (int t = 0; t < kOmegaSeg && base + t < n; ++t) raw[lane * kOmegaSeg + t] = x.next();
@@ -58,7 +63,7 @@ __device__ __forceinline__ void omega_raw_round(Xoshiro& lane_state, int round, 
 __device__ __forceinline__ Xoshiro omega_lane_start(std::uint64_t seed, index_t col) {
   Xoshiro x = column_stream(seed, static_cast<std::uint64_t>(col));
   const int lane = threadIdx.x & 31;
-  if (lane > 0) jump_state(g_jump[lane], x);
+  if (lane > 0) jump_state(lane, x);
   return x;
 }
 
@@ -133,10 +138,10 @@ void ensure_jump_tables(cudaStream_t s) {
       for (int L = 0; L < 32; ++L) {
         if (L > 0)
           for (int t = 0; t < kOmegaSeg; ++t) xoshiro_step(st);
-        for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(L) * 256 + j) * 4 + w] = st[w];
+        for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(j) * kJumps + L) * 4 + w] = st[w];
       }
       for (int t = 0; t < kOmegaSeg; ++t) xoshiro_step(st);  // 32 * 128 = 4096
-      for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(32) * 256 + j) * 4 + w] = st[w];
+      for (int w = 0; w < 4; ++w) host[(static_cast<std::size_t>(j) * kJumps + 32) * 4 + w] = st[w];
     }
   }
   LPCA_CUDA(cudaMemcpyToSymbolAsync(g_jump, host.data(), host.size() * sizeof(std::uint64_t), 0,

@@ -26,7 +26,7 @@ constexpr int kJumps = 33;                       // T^(128 L), L = 0..31, and T^
 // Stored column-interleaved, g_jump[j][k][w]: for a fixed column j the 32
 // lanes' matrices (k = lane) are contiguous, so each step of the product is
 // one coalesced 1 KB read across the warp.
-__device__ std::uint64_t g_jump[256][kJumps][4];
+__device__ __align__(16) std::uint64_t g_jump[256][kJumps][4];
 
 __device__ __forceinline__ void jump_state(int k, Xoshiro& x) {
   const std::uint64_t in[4] = {x.s0, x.s1, x.s2, x.s3};
@@ -60,10 +60,44 @@ __device__ __forceinline__ void omega_raw_round(Xoshiro& lane_state, int round, 
   }
 }
 
-__device__ __forceinline__ Xoshiro omega_lane_start(std::uint64_t seed, index_t col) {
+// Lane L's start state T^(128 L) s. The 32 lanes' matrices (256 KB, usually
+// evicted from L2 by the X passes between fits) are streamed through shared
+// memory by the whole CTA in 32-column chunks (coalesced 16 B loads), warp 0
+// folding each chunk into its product. Call with all threads; lanes of warp 0
+// get their state, other threads a dummy.
+__device__ Xoshiro omega_lane_start(std::uint64_t seed, index_t col, std::uint64_t* stage) {
+  constexpr int kCols = kOmegaChunk * 8 / (32 * 32);  // columns per chunk that fit the 32 KB stage
   Xoshiro x = column_stream(seed, static_cast<std::uint64_t>(col));
   const int lane = threadIdx.x & 31;
-  if (lane > 0) jump_state(lane, x);
+  const std::uint64_t in[4] = {x.s0, x.s1, x.s2, x.s3};
+  std::uint64_t o[4] = {0, 0, 0, 0};
+  for (int j0 = 0; j0 < 256; j0 += kCols) {
+    // g_jump[j][k][w] for j in [j0, j0 + kCols), k < 32: one contiguous block
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(&g_jump[j0][0][0]);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(stage);
+    for (int e = threadIdx.x; e < kCols * 32 * 2; e += kOmegaThreads) {
+      const int jj = e / 64, rest = e % 64;  // 64 ulonglong2 per column (32 lanes x 2)
+      dst[e] = src[jj * (kJumps * 2) + rest];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll 4
+      for (int jj = 0; jj < kCols; ++jj) {
+        const int j = j0 + jj;
+        const std::uint64_t mask = 0ull - ((in[j >> 6] >> (j & 63)) & 1ull);
+        const std::uint64_t* m = stage + (jj * 32 + lane) * 4;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) o[w] ^= m[w] & mask;
+      }
+    }
+    __syncthreads();
+  }
+  if (lane > 0) {
+    x.s0 = o[0];
+    x.s1 = o[1];
+    x.s2 = o[2];
+    x.s3 = o[3];
+  }
   return x;
 }
 
@@ -75,8 +109,7 @@ __global__ void __launch_bounds__(kOmegaThreads) omega_gaussian_kernel(index_t n
                                                                        double* out, index_t ld) {
   __shared__ std::uint64_t raw[kOmegaChunk];
   const index_t col = blockIdx.x;
-  Xoshiro st(0);
-  if (threadIdx.x < 32) st = omega_lane_start(seed, col);  // warp 0 only
+  Xoshiro st = omega_lane_start(seed, col, raw);  // raw doubles as the jump-matrix stage
   double* dst = out + col * ld;
   for (index_t base = 0, round = 0; base < n; base += kOmegaChunk, ++round) {
     const int cnt = static_cast<int>(n - base < kOmegaChunk ? n - base : kOmegaChunk);
@@ -94,8 +127,7 @@ __global__ void __launch_bounds__(kOmegaThreads) omega_sparse_kernel(index_t n, 
                                                                      index_t ld) {
   __shared__ std::uint64_t raw[kOmegaChunk];
   const index_t col = blockIdx.x;
-  Xoshiro st(0);
-  if (threadIdx.x < 32) st = omega_lane_start(seed, col);  // warp 0 only
+  Xoshiro st = omega_lane_start(seed, col, raw);  // raw doubles as the jump-matrix stage
   double* dst = out + col * ld;
   const double half = density / 2.0;
   for (index_t base = 0, round = 0; base < n; base += kOmegaChunk, ++round) {

@@ -417,7 +417,7 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
-  if (kHalf && kMode == kXW && a.scan && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
+  if (kHalf && kMode == kXW && a.scan == 1 && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
   if (kHalf && kMode == kXTU && a.scan && a.run_stages > a.stages)
     throw Error(kInternal, "tc pair: a scanned U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
   const size_t smem =

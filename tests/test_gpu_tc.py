@@ -80,8 +80,9 @@ def test_tc_power_and_spca(ctx, ref):
 def test_sketch_first_stage_scales_fall_back_to_the_scan(ctx):
     """The sketch takes each run's A-row scale from the run's first stage; rows
     whose later stage outgrows it (or sits far below it) make the fit rerun with
-    the full per-run scan. X here has, in every 128-column run, a zero first
-    half and small values in the second half, and a few huge entries late."""
+    the full per-run scan. X here has, in every 128-column block, a zero first
+    half and small values in the second half (so every run's first stage is
+    zero, whatever the run length), and a few huge entries late."""
     import torch
     rng = np.random.default_rng(8)
     m, n = 8192, 1024

@@ -46,6 +46,7 @@ def projection(cfg, lp):
     return lp.ProjectionSpec(kind=kind, density=cfg.get("density", 1.0), seed=SEED_OMEGA)
 SEED_X, SEED_OMEGA = 1000, 7
 METRIC = "Lazy SPCA fit+transform samples/sec"
+FP64_TFLOPS = 37.0  # B200 datasheet dense fp64 (tensor) rate; the fp64 configs' roofline peak
 
 
 def _peaks():
@@ -241,21 +242,33 @@ def run_ours(args, cfg):
     tr_s = tm.transform_pass / args.steps
     x_bytes = m * n * esz
     npad = (l + 15) // 16 * 16
-    if esz == 4:  # fp16 hi/lo planes: W^T in, U^T out (+ its 128-row block scales)
-        sk_bytes = x_bytes + 4 * npad * n + 4 * npad * m + 4 * npad * ((m + 127) // 128)
+    if esz == 4:  # fp16 hi/lo planes: W^T in, U^T out (+ its 256-row block scales)
+        sk_bytes = x_bytes + 4 * npad * n + 4 * npad * m + 4 * npad * ((m + 255) // 256)
     else:
         sk_bytes = x_bytes + n * l * 8 + m * l * 8
     hbm, peak_kind = _peaks()
     achieved = sk_bytes / sketch_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": _traffic(args.config), "kernel": "sketch U = X Omega (tc2_kernel<XW, fp16>)",
-            "peak_source": peak_kind, "algorithmic_bytes": sk_bytes, "kernel_ms": sketch_s * 1e3,
+            "peak_source": peak_kind, "algorithmic_bytes": sk_bytes, "kernel_ms": sketch_s * 1e3}
+    if esz == 8:
+        # fp64 X runs the DMMA kernel (xw_f64_fast_kernel), bound by the fp64
+        # tensor-core rate, not HBM: 2 m n l flops per pass. No measured fp64
+        # peak exists in MEASURED_PEAKS.json; the datasheet figure stands in.
+        tf = 2.0 * m * n * l / sketch_s / 1e12
+        roof.update({"bound": "tensor", "achieved": tf, "peak": FP64_TFLOPS, "unit": "TFLOP/s",
+                     "frac": tf / FP64_TFLOPS, "traffic": None,
+                     "kernel": ("sketch U = X Omega (xw_f64_fast_kernel, DMMA m8n8k4)" if l > 64 and n > 64
+                                else "sketch U = X Omega (xw_simt_kernel, DFMA)"),
+                     "peak_source": "B200 datasheet fp64 tensor 37 TFLOP/s (not measured)",
+                     "hbm_GBps": achieved, "algorithmic_flops": 2.0 * m * n * l})
+    roof.update({
             "phases_ms": {"sketch": tm.sketch / args.steps * 1e3, "power": tm.power / args.steps * 1e3,
                           "f_form": tm.f_form / args.steps * 1e3, "svd": tm.svd / args.steps * 1e3,
                           "transform": tm.transform / args.steps * 1e3},
             "pass_ms": {"sketch": sketch_s * 1e3, "f": f_s * 1e3, "transform": tr_s * 1e3},
             "f_pass_GBps": (x_bytes + 4 * npad * m) / f_s / 1e9 if f_s > 0 else None,
-            "transform_pass_GBps": (x_bytes + m * k * esz) / tr_s / 1e9 if tr_s > 0 else None}
+            "transform_pass_GBps": (x_bytes + m * k * esz) / tr_s / 1e9 if tr_s > 0 else None})
 
     e2e = None
     if not args.no_e2e:
@@ -271,7 +284,7 @@ def run_ours(args, cfg):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (BASELINE low-rank generator, seeded, generated on device)",
             "config": {"workload": cfg["name"], "rows_per_gpu": m, "global_rows": world * m,
-                       "method": "lazy_spca", "gemm_path": args.gemm or "tcgen05",
+                       "method": "lazy_spca", "gemm_path": (args.gemm or "tcgen05") if cfg["dtype"] != "f64" else "dmma (fp64 X)",
                        "parallelism": f"dp{world} (row shards, NCCL allreduce of F)",
                        "l2": "inputs larger than L2 (X is %.1f GB per GPU)" % (x_bytes / 1e9)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -1,20 +1,31 @@
 """Lazy SPCA fit+transform throughput on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c3|c1] [--gemm tcgen05|simt] [--no-e2e] [--no-cpu]
+                  [--config c3|c2|c1|c4|c5] [--gemm tcgen05|simt] [--no-e2e] [--no-cpu]
 
-A step is one Lazy SPCA fit (Omega regeneration, sketch U = X Omega, F = U^T X,
-the l x l step) plus the transform Y = X V over one rank's resident rows.
-N > 1: launched by torch.distributed.run, one process per GPU; each rank holds
-its own row shard (weak scaling) and the F exchange is one NCCL allreduce
-inside the library. Rank 0 prints one JSON line.
+The bench line is BASELINE configs[2] ("c3", the north-star workload: X fp32
+4.6M x 4096, l = 220, q = 1) unless --config says otherwise.
+
+A step is one Lazy SPCA fit (Omega regeneration, sketch U = X Omega, the power
+step Z = X^T U, Z <- orth(Z), U = X Z, F = U^T X, the l x l step) plus the
+transform Y = X V over this rank's resident rows, through one
+lpca_fit_transform call.
+
+Multi-GPU: --gpus N > 1 re-launches this script under torch.distributed.run
+(one process per GPU) unless it already runs under it. The global row count is
+fixed and row-sharded (strong scaling: rank r holds rows
+[r * ceil(m / N), ...)); each rank generates its own shard on its GPU, and the
+F and Z exchanges are NCCL allreduces inside the library. Rank 0 prints one
+JSON line; time is the max over ranks of the device-event time.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -23,7 +34,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-# BASELINE.json configs; the bench line is configs[1] ("c2") unless --config.
+# BASELINE.json configs. m is the GLOBAL row count (sharded over ranks).
 CONFIGS = {
     "c1": dict(m=10_000, n=1_000, r=50, rho=0.9, k=10, l=20, q=0, dtype="f64",
                name="configs[0]: X fp64 10,000x1,000, r=50, rho=0.9, k=10, l=20, q=0"),
@@ -35,26 +46,62 @@ CONFIGS = {
                kind="very_sparse", density=1.0 / 128,
                name="configs[3]: X fp32 2,000,000x16,384, r=400, rho=0.98, very sparse Omega "
                     "(density 1/sqrt(n)), k=256, l=300, q=2"),
-    "c5": dict(m=1_000_000, n=2_048, r=500, rho=0.99, k=256, l=512, q=1, dtype="f64",
-               name="configs[4] per GPU: X fp64 1,000,000x2,048 (8e6 rows over 8 GPUs), r=500, "
-                    "rho=0.99, k=256, l=512, q=1"),
+    "c5": dict(m=8_000_000, n=2_048, r=500, rho=0.99, k=256, l=512, q=1, dtype="f64",
+               name="configs[4]: X fp64 8,000,000x2,048, r=500, rho=0.99, k=256, l=512, q=1"),
 }
+DEFAULT_CONFIG = "c3"
+# bounded CPU samples (rows) for the reference's CPU path: ~10-30 s of work for
+# cpu_baseline, a few seconds per step for --impl reference
+CPU_ROWS = {"c1": 10_000, "c2": 40_000, "c3": 16_384, "c4": 4_096, "c5": 8_192}
+REF_ROWS = {"c1": 10_000, "c2": 16_384, "c3": 6_144, "c4": 2_048, "c5": 4_096}
+
+SEED_X, SEED_OMEGA = 1000, 7
+METRIC = "Lazy SPCA fit+transform samples/sec"
 
 
 def projection(cfg, lp):
     kind = lp.ProjectionKind.very_sparse if cfg.get("kind") == "very_sparse" else lp.ProjectionKind.gaussian
     return lp.ProjectionSpec(kind=kind, density=cfg.get("density", 1.0), seed=SEED_OMEGA)
-SEED_X, SEED_OMEGA = 1000, 7
-METRIC = "Lazy SPCA fit+transform samples/sec"
-FP64_TFLOPS = 37.0  # B200 datasheet dense fp64 (tensor) rate; the fp64 configs' roofline peak
 
 
-def _peaks():
+def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
+    """(first row, row count) of rank's contiguous shard of m rows (strong scaling)."""
+    per = -(-m // world)
+    lo = min(m, rank * per)
+    return lo, min(m, lo + per) - lo
+
+
+def peaks() -> dict:
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written: HBM copy GB/s,
+    dense bf16 TF/s burst and sustained), plus profiles/peaks_r02.json
+    (tools/peaks.cu on a B200 of this pool: tcgen05 f16 / tf32, DMMA, DFMA)."""
+    out = {"hbm_gbs": 6550.0, "bf16_tflops_sustained": 1408.4, "source": "fallback (B200_PROFILING.md)"}
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        out.update(hbm_gbs=float(d["hbm_gbs"]),
+                   bf16_tflops_sustained=float(d.get("bf16_tflops_sustained", d.get("bf16_tflops"))),
+                   source="MEASURED_PEAKS.json")
+    q = ROOT / "profiles" / "peaks_r02.json"
+    if q.exists():
+        d = json.loads(q.read_text())
+        out["dmma_f64_tflops"] = float(d["dmma_f64_tflops"])
+        out["dfma_f64_tflops"] = float(d["dfma_f64_tflops"])
+        out["f16_tcgen05_tflops_microbench"] = float(d["f16_tcgen05_tflops"])
+        out["peaks_file"] = "profiles/peaks_r02.json"
+    else:
+        out["dmma_f64_tflops"] = 37.0  # datasheet stand-in until tools/peaks.py has run
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -115,41 +162,79 @@ def _dist():
     return rank, world, local
 
 
+def relaunch_if_needed(args) -> int | None:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N processes and return its exit code. Under torchrun, --gpus must match
+    WORLD_SIZE."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the comm_nranks lines stay visible in the log
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def stub_worker(args, cfg):
+    """Launcher check without a GPU (tests/test_bench_cpu.py): every rank joins a
+    gloo group and reports its shard; rank 0 prints the gathered list."""
+    import torch.distributed as dist
+    rank, world, _ = _dist()
+    dist.init_process_group("gloo")
+    m = args.rows or cfg["m"]
+    row0, rows = shard_rows(m, world, rank)
+    got = [None] * world
+    dist.all_gather_object(got, {"rank": rank, "world": world, "row0": row0, "rows": rows})
+    if rank == 0:
+        print(json.dumps({"stub": True, "n_gpus": args.gpus, "global_rows": m, "shards": got}), flush=True)
+    dist.destroy_process_group()
+
+
+# ---- the reference's CPU path ---------------------------------------------------
 def cpu_reference(cfg: dict, sample_rows: int, threads: int, steps: int = 1, warmup: int = 0):
     """The reference's own CPU implementation (oracle/_ref: proj/core compiled
-    unmodified) on a bounded row sample of the same workload. Returns
-    (samples/s, kind, cores, sample description)."""
+    from /root/reference unmodified, with its default -march=native on hosts of
+    the build's ISA) on a bounded row sample of the same workload. q = 0 runs
+    reduce(lazy_spca) + apply_map; q >= 1 (no reference reducer: SPEC.md:371)
+    composes the reference's kernels build_sketch / gemm_t / householder_qr /
+    spmm / truncated_svd_via_gram (oracle/ref_capi.cpp). Returns
+    (samples/s, kind, cores, description, seconds per step)."""
     import numpy as np
     from oracle import lazypca_oracle as O
     from oracle import refbind as R
+    R.use_native(True)
     dt = np.float32 if cfg["dtype"] == "f32" else np.float64
-    x = O.synth_lowrank(0, sample_rows, cfg["n"], cfg["r"], cfg["rho"], 0.01, SEED_X, dtype=dt,
-                        exact_log=False)
+    x = O.synth_lowrank(0, sample_rows, cfg["n"], cfg["r"], cfg["rho"], 0.01, SEED_X, dtype=dt, exact_log=False)
     R.set_threads(threads)
-    if cfg["q"] > 0:
-        kind = "port"  # q >= 1 has no reference implementation (SPEC.md:371)
-        times = []
-        for i in range(warmup + steps):
-            t0 = time.perf_counter()
-            v, s, _ = O.reduce_lazy_spca(x.astype(np.float64), cfg["k"], cfg["l"], SEED_OMEGA,
-                                         kind=cfg.get("kind", "gaussian"), density=cfg.get("density", 1.0),
-                                         power_iters=cfg["q"])
-            O.apply_map(x, v)
-            if i >= warmup:
-                times.append(time.perf_counter() - t0)
-    else:
-        kind = "reference"
-        times = []
-        for i in range(warmup + steps):
-            _, _, _, secs = R.fit_transform(2, x, cfg["k"], cfg["l"], SEED_OMEGA,
-                                            kind=1 if cfg.get("kind") == "very_sparse" else 0,
+    kind = 1 if cfg.get("kind") == "very_sparse" else 0
+    times = []
+    for i in range(warmup + steps):
+        if cfg["q"] > 0:
+            _, _, _, secs = R.lazy_power_fit_transform(x, cfg["k"], cfg["l"], SEED_OMEGA, cfg["q"], kind=kind,
+                                                       density=cfg.get("density", 1.0))
+        else:
+            _, _, _, secs = R.fit_transform(2, x, cfg["k"], cfg["l"], SEED_OMEGA, kind=kind,
                                             density=cfg.get("density", 1.0), want_y=True)
-            if i >= warmup:
-                times.append(secs)
+        if i >= warmup:
+            times.append(secs)
     per = sum(times) / len(times)
-    desc = (f"{sample_rows} rows x {cfg['n']} of the same generator, dense stored as the reference's "
-            f"CSC; reduce(lazy_spca)+apply_map, {threads} threads, {len(times)} timed reps")
-    return sample_rows / per, kind, threads, desc, per
+    how = ("reduce(lazy_spca) + apply_map" if cfg["q"] == 0 else
+           f"Lazy SPCA with q={cfg['q']} composed from the reference's build_sketch / gemm_t / householder_qr / "
+           "spmm / truncated_svd_via_gram + spmm(X, V)")
+    desc = (f"{sample_rows} rows x {cfg['n']} of the same generator (dense stored as the reference's CSC, "
+            f"conversion untimed); {how}; {threads} threads on {cpu_model()}; reference built "
+            f"{R.build_flags()}; {len(times)} timed reps")
+    return sample_rows / per, "reference", threads, desc, per
 
 
 def run_reference(args, cfg):
@@ -157,22 +242,83 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    rows = int(args.ref_rows)
-    value, kind, cores, desc, per = cpu_reference(cfg, rows, threads, steps=args.steps,
-                                                  warmup=args.warmup)
+    rows = int(args.ref_rows or REF_ROWS[args.config])
+    value, kind, cores, desc, per = cpu_reference(cfg, rows, threads, steps=args.steps, warmup=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (BASELINE low-rank generator, seeded)",
         "config": {"workload": cfg["name"], "sample_rows": rows, "method": "lazy_spca"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
-                         "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind, "sample": desc},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---- roofline ---------------------------------------------------------------------
+def pass_roof(rows, n, w, esz, t, pk, extra_bytes=0):
+    """One X pass: algorithmic bytes (X once + operand/output planes) over HBM,
+    algorithmic flops 2 rows n w at the dtype's peak (fp32 data: three fp16
+    products per fp32-faithful one, so bf16_sustained / 3; fp64: DMMA)."""
+    byts = rows * n * esz + extra_bytes
+    flops = 2.0 * rows * n * w
+    p_flops = (pk["bf16_tflops_sustained"] / 3.0 if esz == 4 else pk["dmma_f64_tflops"]) * 1e12
+    t_hbm = byts / (pk["hbm_gbs"] * 1e9)
+    t_mma = flops / p_flops
+    return {"ms": t * 1e3, "bytes": byts, "flops": flops, "t_hbm_ms": t_hbm * 1e3, "t_mma_ms": t_mma * 1e3,
+            "bound": "hbm" if t_hbm >= t_mma else "tensor",
+            "frac": (max(t_hbm, t_mma) / t) if t > 0 else None}
+
+
+def roofline(cfg, rows, esz, tm, steps, pk, config):
+    n, k, l, q = cfg["n"], cfg["k"], cfg["l"], cfg["q"]
+    npad = (l + 15) // 16 * 16
+    up = 4 * npad * rows if esz == 4 else rows * l * 8          # U^T fp16 hi/lo planes (or U fp64)
+    passes = {
+        "sketch": pass_roof(rows, n, l, esz, tm.sketch_pass / steps, pk, up + 4 * npad * n),
+        "f": pass_roof(rows, n, l, esz, tm.f_pass / steps, pk, up),
+        "transform": pass_roof(rows, n, k, esz, tm.transform_pass / steps, pk, rows * k * esz),
+    }
+    if q > 0:
+        pp = pass_roof(rows, n, l, esz, tm.power_pass / steps / (2 * q), pk, up)
+        passes["power (per pass, 2 per step)"] = pp
+    tot_t = sum(p["ms"] * (2 * q if "power" in nm else 1) for nm, p in passes.items()) / 1e3
+    tot_roof = sum(max(p["t_hbm_ms"], p["t_mma_ms"]) * (2 * q if "power" in nm else 1)
+                   for nm, p in passes.items()) / 1e3
+    sk = passes["sketch"]
+    bound = sk["bound"]
+    if bound == "tensor":
+        achieved, peak, unit = sk["flops"] / (sk["ms"] * 1e-3) / 1e12, sk["flops"] / (sk["t_mma_ms"] * 1e-3) / 1e12, "TFLOP/s"
+    else:
+        achieved, peak, unit = sk["bytes"] / (sk["ms"] * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+    kern = ("tc2_kernel<XW, fp16> (2-SM tcgen05, 3-term fp16 split)" if esz == 4
+            else "xw_f64_fast_kernel (DMMA m8n8k4)")
+    return {
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+        "traffic": _traffic(config),
+        "kernel": f"sketch U = X Omega, {kern}",
+        "peak_note": ("fp32 data: fp32-equivalent TFLOP/s (2 m n l) against bf16_tflops_sustained / 3 "
+                      "(every fp32 product is three fp16 products)" if esz == 4 else
+                      "fp64 data: TFLOP/s against the measured DMMA rate") + f"; peaks from {pk['source']}",
+        "x_passes_frac": tot_roof / tot_t if tot_t > 0 else None,
+        "x_passes_ms": tot_t * 1e3,
+        "passes": passes,
+        "peaks": pk,
+    }
+
+
+def _traffic(config):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(config)
+        except Exception:
+            return None
+    return None
+
+
+# ---- our arm --------------------------------------------------------------------
 def run_ours(args, cfg):
     import torch
     import paper_1709_07175_b200 as lp
@@ -193,20 +339,20 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 
-    m, n, k, l = cfg["m"], cfg["n"], cfg["k"], cfg["l"]
+    m_global = args.rows or cfg["m"]
+    row0, m = shard_rows(m_global, world, rank)
+    n, k, l = cfg["n"], cfg["k"], cfg["l"]
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
     esz = 4 if cfg["dtype"] == "f32" else 8
     x = torch.empty((m, n), dtype=tdt, device="cuda")
-    lp.synth_lowrank(x, rank * m, cfg["r"], cfg["rho"], 0.01, SEED_X, ctx=ctx)
+    lp.synth_lowrank(x, row0, cfg["r"], cfg["rho"], 0.01, SEED_X, ctx=ctx)
     y = torch.empty((m, k), dtype=tdt, device="cuda")
     conf = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=k, l=l,
                             projection=projection(cfg, lp), power_iters=cfg["q"])
     torch.cuda.synchronize()
 
     def step(tm=None):
-        # fit + transform of the resident X in one library call (lpca_fit_transform:
-        # the same kernels as reduce_lazy_spca + apply_map, the transform queued
-        # behind the fit's spectral step instead of after its host checks)
+        # fit + transform of the resident shard in one library call
         mp, _ = lp.fit_transform(x, conf, timings=tm, ctx=ctx, out=y)
         return mp
 
@@ -233,60 +379,35 @@ def run_ours(args, cfg):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * m / (ms * 1e-3)
-
-    # dominant kernel: the sketch pass U = X Omega, timed alone by the library's
-    # device events around its launch on this stream (lpca_timings.sketch_pass)
-    sketch_s = tm.sketch_pass / args.steps
-    f_s = tm.f_pass / args.steps
-    tr_s = tm.transform_pass / args.steps
-    x_bytes = m * n * esz
-    npad = (l + 15) // 16 * 16
-    if esz == 4:  # fp16 hi/lo planes: W^T in, U^T out (+ its 256-row block scales)
-        sk_bytes = x_bytes + 4 * npad * n + 4 * npad * m + 4 * npad * ((m + 255) // 256)
-    else:
-        sk_bytes = x_bytes + n * l * 8 + m * l * 8
-    hbm, peak_kind = _peaks()
-    achieved = sk_bytes / sketch_s / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": _traffic(args.config), "kernel": "sketch U = X Omega (tc2_kernel<XW, fp16>)",
-            "peak_source": peak_kind, "algorithmic_bytes": sk_bytes, "kernel_ms": sketch_s * 1e3}
-    if esz == 8:
-        # fp64 X runs the DMMA kernel (xw_f64_fast_kernel), bound by the fp64
-        # tensor-core rate, not HBM: 2 m n l flops per pass. No measured fp64
-        # peak exists in MEASURED_PEAKS.json; the datasheet figure stands in.
-        tf = 2.0 * m * n * l / sketch_s / 1e12
-        roof.update({"bound": "tensor", "achieved": tf, "peak": FP64_TFLOPS, "unit": "TFLOP/s",
-                     "frac": tf / FP64_TFLOPS, "traffic": None,
-                     "kernel": ("sketch U = X Omega (xw_f64_fast_kernel, DMMA m8n8k4)" if l > 64 and n > 64
-                                else "sketch U = X Omega (xw_simt_kernel, DFMA)"),
-                     "peak_source": "B200 datasheet fp64 tensor 37 TFLOP/s (not measured)",
-                     "hbm_GBps": achieved, "algorithmic_flops": 2.0 * m * n * l})
-    roof.update({
-            "phases_ms": {"sketch": tm.sketch / args.steps * 1e3, "power": tm.power / args.steps * 1e3,
-                          "f_form": tm.f_form / args.steps * 1e3, "svd": tm.svd / args.steps * 1e3,
-                          "transform": tm.transform / args.steps * 1e3},
-            "pass_ms": {"sketch": sketch_s * 1e3, "f": f_s * 1e3, "transform": tr_s * 1e3},
-            "f_pass_GBps": (x_bytes + 4 * npad * m) / f_s / 1e9 if f_s > 0 else None,
-            "transform_pass_GBps": (x_bytes + m * k * esz) / tr_s / 1e9 if tr_s > 0 else None})
+    value = m_global / (ms * 1e-3)
+    pk = peaks()
+    roof = roofline(cfg, m, esz, tm, args.steps, pk, args.config)
+    roof["phases_ms"] = {"sketch": tm.sketch / args.steps * 1e3, "power": tm.power / args.steps * 1e3,
+                         "f_form": tm.f_form / args.steps * 1e3, "svd": tm.svd / args.steps * 1e3,
+                         "transform": tm.transform / args.steps * 1e3}
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(args, cfg, ctx, x, conf, world, dist, lp, torch)
+        e2e = _e2e(args, cfg, ctx, x, conf, m_global, dist, lp, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, kind, cores, desc, _ = cpu_reference(cfg, int(args.cpu_rows), len(os.sched_getaffinity(0)))
+        v, kind, cores, desc, _ = cpu_reference(cfg, int(args.cpu_rows or CPU_ROWS[args.config]),
+                                                len(os.sched_getaffinity(0)))
         cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind, "sample": desc}
     if rank == 0:
+        dname = {"f32": "f32 (3-term fp16 split on tcgen05, fp32 accumulate, fp64 l x l step)",
+                 "f64": "f64 (DMMA)"}[cfg["dtype"]]
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": cfg["dtype"], "data": "synthetic (BASELINE low-rank generator, seeded, generated on device)",
-            "config": {"workload": cfg["name"], "rows_per_gpu": m, "global_rows": world * m,
-                       "method": "lazy_spca", "gemm_path": (args.gemm or "tcgen05") if cfg["dtype"] != "f64" else "dmma (fp64 X)",
-                       "parallelism": f"dp{world} (row shards, NCCL allreduce of F)",
-                       "l2": "inputs larger than L2 (X is %.1f GB per GPU)" % (x_bytes / 1e9)},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": cfg["dtype"], "dtype_detail": dname,
+            "data": "synthetic (BASELINE low-rank generator, seeded, each shard generated on its GPU)",
+            "config": {"workload": cfg["name"], "global_rows": m_global, "rows_per_gpu": m,
+                       "method": "lazy_spca",
+                       "gemm_path": (args.gemm or "tcgen05") if cfg["dtype"] != "f64" else "dmma (fp64 X)",
+                       "parallelism": f"dp{world} (row shards, NCCL allreduce of Z and F)",
+                       "l2": "inputs larger than L2 (X is %.1f GB per GPU)" % (m * n * esz / 1e9)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -297,25 +418,19 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def _traffic(config):
-    p = ROOT / "profiles" / "traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get(config)
-        except Exception:
-            return None
-    return None
-
-
-def _e2e(args, cfg, ctx, x, conf, world, dist, lp, torch):
+def _e2e(args, cfg, ctx, x, conf, m_global, dist, lp, torch):
     """Same metric through the public C ABI with host buffers: every step copies
-    X from pinned host memory to the device and Y back (lpca_fit_transform)."""
+    this rank's X from pinned host memory to the device and Y back
+    (lpca_fit_transform with LPCA_HOST views)."""
     import ctypes as C
     from paper_1709_07175_b200 import _lib as L
-    m, n, k = cfg["m"], cfg["n"], cfg["k"]
-    xh = torch.empty((m, n), dtype=x.dtype, pin_memory=True)
+    m, n, k = x.shape[0], cfg["n"], cfg["k"]
+    try:
+        xh = torch.empty((m, n), dtype=x.dtype, pin_memory=True)
+        yh = torch.empty((m, k), dtype=x.dtype, pin_memory=True)
+    except RuntimeError as e:
+        return {"unavailable": f"pinned host buffers of {m * n * x.element_size() / 1e9:.1f} GB: {e}"[:200]}
     xh.copy_(x)
-    yh = torch.empty((m, k), dtype=x.dtype, pin_memory=True)
     vw = lp.api._View(xh)  # host row-major view
     cfgc = conf._c()
     dt = L.LPCA_F32 if x.dtype == torch.float32 else L.LPCA_F64
@@ -329,8 +444,7 @@ def _e2e(args, cfg, ctx, x, conf, world, dist, lp, torch):
                                                  L.LPCA_HOST, 0, C.byref(t)))
         ctx.lib.lpca_map_destroy(h)
 
-    for _ in range(max(1, args.warmup)):
-        one()
+    one()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -344,27 +458,34 @@ def _e2e(args, cfg, ctx, x, conf, world, dist, lp, torch):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
     esz = x.element_size()
-    return {"value": world * m / sec, "unit": "samples/s", "h2d_bytes_per_step": m * n * esz,
+    return {"value": m_global / sec, "unit": "samples/s", "h2d_bytes_per_step": m * n * esz,
             "d2h_bytes_per_step": m * k * esz, "ms_per_step": sec * 1e3, "steps": steps,
-            "path": "lpca_fit_transform (C ABI), pinned host X in, host Y out"}
+            "path": "lpca_fit_transform (C ABI), pinned host X in, host Y out (per rank)"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--rows", type=int, default=0, help="override the global row count (experiments only)")
     ap.add_argument("--gemm", default=None, choices=["tcgen05", "simt"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-rows", type=int, default=40_000)
-    ap.add_argument("--ref-rows", type=int, default=16_384)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-rows", type=int, default=0)
+    ap.add_argument("--ref-rows", type=int, default=0)
+    ap.add_argument("--stub-worker", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.stub_worker:
+        stub_worker(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_ours(args, cfg)

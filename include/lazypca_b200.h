@@ -100,6 +100,7 @@ typedef struct {
   double sketch, qr, f_form, svd, total;
   double power, transform, h2d, d2h;
   double sketch_pass, f_pass, transform_pass;
+  double power_pass; /* the power steps' X-pass kernels (Z = X^T U and U = X Z), first 8 steps */
 } lpca_timings;
 
 typedef struct lpca_ctx lpca_ctx;

@@ -207,6 +207,41 @@ int ref_fit_transform(int method, const void* x, int dtype, std::int64_t m, std:
   });
 }
 
+// Lazy SPCA with q power steps composed from the reference's own kernels
+// (the reference has no power iterations; this is the builder's
+// scheme of SURVEY 8(a) a16 restated on the reference's code):
+//   U = build_sketch(X, Omega)                         (reducer.cpp:163-169)
+//   q times: Z = gemm_t(U, X)^T, Q = householder_qr(Z).q, U = spmm(X, Q)
+//   F = gemm_t(U, X); truncated_svd_via_gram(F, k)     (reducer.cpp:216-234)
+//   Y = spmm(X, V)                                     (apply_map, reducer.cpp:348-353)
+// Timed like ref_fit_transform (CSC conversion outside the timed region).
+// For q = 0 the result equals reduce_lazy_spca + apply_map.
+int ref_lazy_power_fit_transform(const void* x, int dtype, std::int64_t m, std::int64_t n, std::int64_t k,
+                                 std::int64_t l, std::uint64_t seed, int kind, double density, int q,
+                                 double* y_out, double* v_out, double* sigma_out, double* seconds) {
+  return guarded([&] {
+    const SparseMatrix xs = csc_any(x, dtype, m, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    const ReducerConfig cfg = make_cfg(2, k, l, seed, kind, density, 0).resolved(n);
+    const ProjectionMatrix omega = regenerate(cfg.projection);
+    DenseMatrix u = build_sketch(xs, omega).u;
+    for (int it = 0; it < q; ++it) {
+      const DenseMatrix zt = gemm_t(u, xs);  // l x n
+      DenseMatrix z(n, l);
+      for (index_t j = 0; j < l; ++j)
+        for (index_t i = 0; i < n; ++i) z(i, j) = zt(j, i);
+      u = spmm(xs, householder_qr(z).q);
+    }
+    const TruncatedSVD svd = truncated_svd_via_gram(gemm_t(u, xs), k);
+    const DenseMatrix y = spmm(xs, svd.v);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (y_out) copy_out(y, y_out);
+    if (v_out) copy_out(svd.v, v_out);
+    if (sigma_out)
+      for (std::int64_t i = 0; i < k; ++i) sigma_out[i] = svd.singular_values[static_cast<std::size_t>(i)];
+  });
+}
+
 // save_map_file / load_map_file (proj/core/src/reducer.cpp:355-412). method:
 // 0 rp, 1 spca, 2 lazy_spca; sigma may be null (no singular values).
 int ref_save_map_file(int method, std::int64_t k, std::int64_t l, std::int64_t n, std::uint64_t seed,

@@ -16,6 +16,9 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "_ref" / "liblazypca_ref.so"
+# the reference's own default build (-march=native) for the timed CPU baseline
+LIB_NATIVE = HERE / "_ref" / "liblazypca_ref_native.so"
+_NATIVE_ISA = ("avx512f", "avx512bw", "avx512vl", "avx512_fp16", "amx_tile")
 REF_SRC = Path("/root/reference/proj/core")
 
 _lib = None
@@ -40,12 +43,38 @@ def available() -> bool:
     return LIB.exists()
 
 
+_use_native = False
+
+
+def native_supported() -> bool:
+    """True when the -march=sapphirerapids build exists and this CPU has that ISA."""
+    try:
+        flags = Path("/proc/cpuinfo").read_text().split()
+    except OSError:
+        return False
+    return LIB_NATIVE.exists() and all(f in flags for f in _NATIVE_ISA)
+
+
+def use_native(on: bool = True) -> bool:
+    """Selects the native build (before the first call). Returns whether it is used."""
+    global _use_native
+    if _lib is not None:
+        raise RuntimeError("refbind: select the build before the first call")
+    _use_native = bool(on) and native_supported()
+    return _use_native
+
+
+def build_flags() -> str:
+    return "-O3 -march=sapphirerapids (reference default -march=native)" if _use_native else "-O3 -march=x86-64-v2"
+
+
 def load():
     global _lib
     if _lib is None:
-        if not LIB.exists():
-            raise RuntimeError(f"{LIB} missing; build it with `make -C oracle` where /root/reference exists")
-        lib = C.CDLL(str(LIB))
+        path = LIB_NATIVE if _use_native else LIB
+        if not path.exists():
+            raise RuntimeError(f"{path} missing; build it with `make -C oracle` where /root/reference exists")
+        lib = C.CDLL(str(path))
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_last_error_index.restype = C.c_int64
         _lib = lib
@@ -115,6 +144,23 @@ def fit_transform(method: int, x: np.ndarray, k: int, l: int, seed: int, kind: i
     _chk(load().ref_fit_transform(C.c_int(method), _p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n),
                                   C.c_int64(k), C.c_int64(l), C.c_uint64(seed), C.c_int(kind),
                                   C.c_double(density), _p(y), _p(v), _p(sig), C.byref(secs)))
+    return y, v, sig, secs.value
+
+
+def lazy_power_fit_transform(x: np.ndarray, k: int, l: int, seed: int, q: int, kind: int = 0,
+                             density: float = 1.0, want_y: bool = True):
+    """Lazy SPCA with q power steps composed from the reference's kernels
+    (build_sketch, gemm_t, householder_qr, spmm, truncated_svd_via_gram) + the
+    transform; returns (Y, V, sigma, seconds). See ref_capi.cpp."""
+    x, dt = _x(x)
+    m, n = x.shape
+    y = np.zeros((m, k), order="F") if want_y else None
+    v = np.zeros((n, k), order="F")
+    sig = np.zeros(k)
+    secs = C.c_double()
+    _chk(load().ref_lazy_power_fit_transform(_p(x), C.c_int(dt), C.c_int64(m), C.c_int64(n), C.c_int64(k),
+                                             C.c_int64(l), C.c_uint64(seed), C.c_int(kind), C.c_double(density),
+                                             C.c_int(q), _p(y), _p(v), _p(sig), C.byref(secs)))
     return y, v, sig, secs.value
 
 

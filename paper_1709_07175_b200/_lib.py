@@ -39,7 +39,7 @@ class Config(C.Structure):
 class Timings(C.Structure):
     _fields_ = [(f, C.c_double) for f in
                 ("sketch", "qr", "f_form", "svd", "total", "power", "transform", "h2d", "d2h",
-                 "sketch_pass", "f_pass", "transform_pass")]
+                 "sketch_pass", "f_pass", "transform_pass", "power_pass")]
 
 
 # int32_t (*lpca_next_block_fn)(void* user, lpca_matrix_view* block, int64_t* slice_index)

@@ -238,6 +238,7 @@ class ReducerTimings:
     sketch_pass: float = 0.0     # the X-pass kernels alone (extension)
     f_pass: float = 0.0
     transform_pass: float = 0.0
+    power_pass: float = 0.0      # both X passes of every power step (first 8 steps)
 
 
 def _fill_timings(t: Optional[ReducerTimings], c: L.Timings) -> None:
@@ -905,6 +906,23 @@ def reduce(x, config: ReducerConfig, timings: ReducerTimings | None = None, ctx=
     return _fit(x, config, timings, ctx)
 
 
+def _check_out(out, m: int, k: int, ctx) -> int:
+    """Validates a caller's Y buffer (row-major m x k torch CUDA tensor on the
+    context's device, fp32/fp64) and returns its leading dimension."""
+    import torch
+    if not isinstance(out, torch.Tensor):
+        raise InvalidArgumentError("out must be a torch tensor")
+    if out.dtype not in (torch.float32, torch.float64):
+        raise InvalidArgumentError(f"out must be float32 or float64, got {out.dtype}")
+    if not out.is_cuda or out.device.index != ctx.device:
+        raise InvalidArgumentError(f"out must live on cuda:{ctx.device}, got {out.device}")
+    if out.dim() != 2 or tuple(out.shape) != (m, k):
+        raise DimensionError(f"out has shape {tuple(out.shape)}, expected ({m}, {k})")
+    if m > 0 and k > 0 and (out.stride(1) != 1 or out.stride(0) < k):
+        raise InvalidArgumentError("out must be row-major (stride(1) == 1, stride(0) >= k)")
+    return max(out.stride(0), k)
+
+
 def apply_map(map_: ReductionMap, x, out=None, layout: str = "col", timings=None, ctx=None):
     """Y = X V (reducer.cpp:348-353). Returns a column-major fp64 numpy array like
     the reference, unless `out` (a torch CUDA tensor, row-major) is given."""
@@ -914,9 +932,10 @@ def apply_map(map_: ReductionMap, x, out=None, layout: str = "col", timings=None
     m = vw.view.rows
     if out is not None:
         import torch
+        ldy = _check_out(out, m, map_.k, ctx)
         dt = L.LPCA_F32 if out.dtype == torch.float32 else L.LPCA_F64
         _check(ctx.lib.lpca_transform(ctx.h, map_.handle(), C.byref(vw.view), C.c_void_p(out.data_ptr()),
-                                      dt, L.LPCA_ROW_MAJOR, L.LPCA_DEVICE, out.stride(0), C.byref(t)))
+                                      dt, L.LPCA_ROW_MAJOR, L.LPCA_DEVICE, ldy, C.byref(t)))
         _fill_timings(timings, t)
         return out
     if layout == "col":
@@ -942,10 +961,11 @@ def fit_transform(x, config: ReducerConfig, y_dtype=np.float64, timings=None, ct
     h = C.c_void_p()
     if out is not None:
         import torch
+        ldy = _check_out(out, vw.view.rows, config.k, ctx)
         dt = L.LPCA_F32 if out.dtype == torch.float32 else L.LPCA_F64
         _check(ctx.lib.lpca_fit_transform(ctx.h, C.byref(cfg), C.byref(vw.view), C.byref(h),
                                           C.c_void_p(out.data_ptr()), dt, L.LPCA_ROW_MAJOR, L.LPCA_DEVICE,
-                                          out.stride(0), C.byref(t)))
+                                          ldy, C.byref(t)))
         _fill_timings(timings, t)
         return ReductionMap(h, ctx), out
     y = np.zeros((vw.view.rows, config.k), dtype=y_dtype)

@@ -15,8 +15,13 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "liblazypca_b200.so"
+# LPCA_BUILD_TAG / LPCA_EXTRA_NVCC_FLAGS: a side build for experiments (e.g. the
+# role timers, -DLPCA_PAIR_PROF) into _build_<tag>/ and liblazypca_b200_<tag>.so,
+# loaded through LPCA_LIB_PATH; the product build ignores both.
+_TAG = os.environ.get("LPCA_BUILD_TAG", "")
+BUILD = PKG / ("_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = PKG / ("liblazypca_b200" + (f"_{_TAG}" if _TAG else "") + ".so")
+EXTRA = os.environ.get("LPCA_EXTRA_NVCC_FLAGS", "").split() if _TAG else []
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -62,7 +67,7 @@ def _compile(src: str, verbose: bool) -> None:
         cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-I", str(CSRC),
                "-I", "/usr/local/cuda/include", "-I", _json_include(), "-c", str(CSRC / src), "-o", str(obj)]
     else:
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(CSRC / src), "-o", str(obj)]
     if verbose and src not in HOST_SOURCES:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

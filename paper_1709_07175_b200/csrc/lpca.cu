@@ -129,7 +129,9 @@ struct lpca_ctx {
   int last_sweeps = 0;
   int eigensolver = 0;  // 0: tridiagonal route (tridiag_eigh), 1: parallel Jacobi (jacobi_eigh)
   std::unordered_map<std::string, std::pair<void*, std::size_t>> ws;
-  cudaEvent_t ev[18] = {};
+  // phase events [0, 18); power-step pass events [18, 18 + 4 * kPowerEvSteps)
+  static constexpr int kPowerEvSteps = 8;
+  cudaEvent_t ev[18 + 4 * kPowerEvSteps] = {};
   std::unordered_set<lpca_map*> live_maps;  // maps whose V was allocated on this context's stream
   int pass_slot = -1;  // >= 0: the next X pass records ev[pass_slot] / ev[pass_slot + 1] around its kernel
   bool force_scan = false;  // fit_dev retry: per-run scales by the full scan
@@ -282,6 +284,11 @@ void check_view(const lpca_matrix_view* x) {
     throw Error(kInvalidArgument, "matrix view: unknown layout");
   } else if (!x->data && x->rows * x->cols > 0) {
     throw Error(kInvalidArgument, "matrix view: null data");
+  } else if (x->ld != 0 && x->rows * x->cols > 0) {
+    const index_t inner = x->layout == LPCA_ROW_MAJOR ? x->cols : x->rows;
+    if (x->ld < inner)
+      throw Error(kInvalidArgument, "matrix view: ld = " + S(x->ld) + " is smaller than the " +
+                                        (x->layout == LPCA_ROW_MAJOR ? "row" : "column") + " length " + S(inner));
   }
 }
 
@@ -890,16 +897,62 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     }
     xs.use = f16;
     ev.mark(1);
+    // Whether a later sketch stage outgrew its run's first-stage scale (summed
+    // over ranks, so every rank takes the same branch). Read only after the
+    // stream has drained past the flag's producer.
+    auto sketch_flagged = [&]() -> bool {
+      if (!xovf) return false;
+      LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+      if (xovf_all) {
+        double all = 0.0;
+        LPCA_CUDA(cudaMemcpy(&all, xovf_all, sizeof(double), cudaMemcpyDeviceToHost));
+        return all > 0.0;
+      }
+      int flagged = 0;
+      LPCA_CUDA(cudaMemcpy(&flagged, xovf, sizeof(int), cudaMemcpyDeviceToHost));
+      return flagged != 0;
+    };
+    // An overflowed stage leaves inf/NaN in U, so the host checks below (power
+    // step pivots, rank floor) may throw before the flag is read: an error
+    // raised while the flag is set reruns the fit with the full scan instead.
+    auto rerun_scanned = [&]() -> lpca_map* {
+      delete map;
+      map = nullptr;
+      ctx.force_scan = true;
+      try {
+        lpca_map* again = fit_dev(ctx, cfg_in, x, t, after_spectral);
+        ctx.force_scan = false;
+        return again;
+      } catch (...) {
+        ctx.force_scan = false;
+        throw;
+      }
+    };
+    try {
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
     double* f = ctx.get<double>("f", l * n);
     if (c.power_iters > 0) {
       double* z = ctx.get<double>("z.w", l * n);
       for (int it = 0; it < c.power_iters; ++it) {
+        const bool timed = it < lpca_ctx::kPowerEvSteps;
+        const int pe = 18 + 4 * it;
+        if (timed) {  // both passes' kernels bracketed (lpca_timings.power_pass)
+          ev.mark(pe);
+          ev.mark(pe + 1);
+          ctx.pass_slot = pe;
+        }
         utx_pass(ctx, x, u, l, f, exact, &xs);               // F = U^T X  (= Z^T)
-        orth_rows(ctx, f, l, n);                             // Z <- orth(Z), CholeskyQR2
+        ctx.pass_slot = -1;
+        orth_rows(ctx, f, l, n);                             // Z <- orth(Z), shifted CholeskyQR3
         launch_transpose(ctx.stream, 8, f, l, l, n, z, n);  // W = Z as n x l column-major
         LPCA_LAUNCHED(ctx);
+        if (timed) {
+          ev.mark(pe + 2);
+          ev.mark(pe + 3);
+          ctx.pass_slot = pe + 2;
+        }
         xw_pass(ctx, x, z, l, n, u, exact, f16 ? &xs : nullptr);  // U = X Z
+        ctx.pass_slot = -1;
       }
     }
     ev.mark(2);
@@ -982,28 +1035,11 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     }
     if (!marked) ev.mark(5);
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
-    if (xovf) {
-      int flagged = 0;
-      if (xovf_all) {
-        double all = 0.0;
-        LPCA_CUDA(cudaMemcpy(&all, xovf_all, sizeof(double), cudaMemcpyDeviceToHost));
-        flagged = all > 0.0;
-      } else {
-        LPCA_CUDA(cudaMemcpy(&flagged, xovf, sizeof(int), cudaMemcpyDeviceToHost));
-      }
-      if (flagged) {  // some row's values outgrew its run's first-stage scale: redo with the scan
-        delete map;
-        ctx.force_scan = true;
-        try {
-          lpca_map* again = fit_dev(ctx, cfg_in, x, t, after_spectral);
-          ctx.force_scan = false;
-          return again;
-        } catch (...) {
-          ctx.force_scan = false;
-          throw;
-        }
-      }
+    } catch (const Error&) {
+      if (sketch_flagged()) return rerun_scanned();
+      throw;
     }
+    if (sketch_flagged()) return rerun_scanned();  // finite but imprecise: redo with the scan
     if (t) {
       t->sketch += ev.secs(0, 1);
       t->power += ev.secs(1, 2);
@@ -1013,6 +1049,8 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       t->total += ev.secs(0, 5);
       t->sketch_pass += ev.secs(12, 13);
       t->f_pass += ev.secs(14, 15);
+      for (int it = 0; it < c.power_iters && it < lpca_ctx::kPowerEvSteps; ++it)
+        t->power_pass += ev.secs(18 + 4 * it, 19 + 4 * it) + ev.secs(20 + 4 * it, 21 + 4 * it);
     }
     return map;
   } catch (...) {
@@ -1049,6 +1087,9 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
   const index_t m = x.m, k = map.k;
   const bool row = y_layout == LPCA_ROW_MAJOR;
   if (ldy <= 0) ldy = row ? k : m;
+  if (ldy < (row ? k : m))
+    throw Error(kInvalidArgument, "transform: ldy = " + S(ldy) + " is smaller than the output's " +
+                                      (row ? "row length k = " + S(k) : "column length m = " + S(m)));
   PhaseEvents ev(ctx);
   ev.mark(6);
   ev.mark(16);

@@ -94,3 +94,23 @@ def test_sketch_first_stage_scales_fall_back_to_the_scan(ctx):
     m32 = lp.reduce_lazy_spca(torch.from_numpy(x).cuda(), cfg, ctx=ctx)
     v64, s64, _ = O.reduce_lazy_spca(x.astype(np.float64), 16, 32, 3)
     assert np.max(np.abs(m32.singular_values - s64) / s64) < 1e-4
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_sketch_overflow_in_a_later_stage_reruns_before_host_checks(ctx, q):
+    """rows with small nonzero noise in each run's first stage
+    and O(1) values later overflow fp16 at the first-stage scale (inf in U, NaN
+    in F). The power step's pivots and the rank floor would throw before the
+    overflow flag was read; the fit must rerun with the scan instead."""
+    import torch
+    rng = np.random.default_rng(11)
+    m, n = 8192, 2048
+    x = rng.standard_normal((m, n)).astype(np.float32) * 0.5
+    for c0 in range(0, n, 512):
+        x[:, c0:c0 + 64] = rng.standard_normal((m, 64)).astype(np.float32) * 1e-3
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=16, l=32, projection=lp.ProjectionSpec(seed=3),
+                           power_iters=q)
+    got = lp.reduce_lazy_spca(torch.from_numpy(x).cuda(), cfg, ctx=ctx)
+    v64, s64, _ = O.reduce_lazy_spca(x.astype(np.float64), 16, 32, 3, power_iters=q)
+    assert np.all(np.isfinite(got.singular_values))
+    assert np.max(np.abs(got.singular_values - s64) / s64) < 1e-4

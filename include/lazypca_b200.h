@@ -119,6 +119,17 @@ lpca_status lpca_ctx_create(int32_t device, lpca_ctx** out);
 lpca_status lpca_nccl_unique_id(void* out_128_bytes);
 lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
                                  const void* nccl_id_128, lpca_ctx** out);
+/* Row-sharded data parallelism over a caller's collective instead of NCCL (e.g.
+ * an MPI or gloo allreduce, or several ranks sharing one device in tests): the
+ * library calls fn(user, data, count, stream) for every exchange, where data is
+ * `count` fp64 values in device memory of this context's device; fn must leave
+ * their sum over all ranks in place, ordered after the work already enqueued on
+ * `stream` (a cudaStream_t) and before anything enqueued after it returns (a
+ * synchronous implementation may synchronise the stream first). Non-zero return
+ * = failure (LPCA_ERR_NCCL). Every rank issues the same sequence of calls. */
+typedef int32_t (*lpca_allreduce_fn)(void* user, double* data, int64_t count, void* cuda_stream);
+lpca_status lpca_ctx_create_hooked(int32_t device, int32_t rank, int32_t world, lpca_allreduce_fn fn, void* user,
+                                   lpca_ctx** out);
 lpca_status lpca_ctx_destroy(lpca_ctx* ctx);
 /* Launch everything on this cudaStream_t (default: the context's own stream). */
 lpca_status lpca_ctx_set_stream(lpca_ctx* ctx, void* cuda_stream);

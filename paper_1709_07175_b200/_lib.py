@@ -42,6 +42,9 @@ class Timings(C.Structure):
                  "sketch_pass", "f_pass", "transform_pass", "power_pass")]
 
 
+# int32_t (*lpca_allreduce_fn)(void* user, double* data, int64_t count, void* cuda_stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
 # int32_t (*lpca_next_block_fn)(void* user, lpca_matrix_view* block, int64_t* slice_index)
 NEXT_BLOCK_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(MatrixView), C.POINTER(C.c_int64))
 
@@ -76,6 +79,7 @@ SIGNATURES = {
     "lpca_ctx_create": (I32, [I32, PP]),
     "lpca_nccl_unique_id": (I32, [P]),
     "lpca_ctx_create_dist": (I32, [I32, I32, I32, P, PP]),
+    "lpca_ctx_create_hooked": (I32, [I32, I32, I32, P, P, PP]),
     "lpca_ctx_destroy": (I32, [P]),
     "lpca_ctx_set_stream": (I32, [P, P]),
     "lpca_ctx_synchronize": (I32, [P]),

@@ -369,6 +369,31 @@ class Context:
         self.h = h
         self.device, self.rank, self.world = device, rank, world
 
+    @classmethod
+    def hooked(cls, device: int, rank: int, world: int, allreduce) -> "Context":
+        """A rank whose exchanges go through `allreduce(data_ptr, count, stream_ptr)`
+        (in-place fp64 sum over ranks of `count` values at device address
+        data_ptr, ordered on the CUDA stream stream_ptr) instead of NCCL
+        (lpca_ctx_create_hooked). Exceptions in the callback fail the call."""
+        self = cls.__new__(cls)
+        self.lib = L.load()
+
+        def tramp(_user, data, count, stream):
+            try:
+                allreduce(int(data or 0), int(count), int(stream or 0))
+                return 0
+            except Exception:  # reported as LPCA_ERR_NCCL by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._hook = L.ALLREDUCE_FN(tramp)  # kept alive with the context
+        h = C.c_void_p()
+        _check(self.lib.lpca_ctx_create_hooked(device, rank, world, self._hook, None, C.byref(h)))
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+        return self
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

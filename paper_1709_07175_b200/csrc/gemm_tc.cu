@@ -410,9 +410,12 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   if (!plan_tmem(a.npad, a.nrb, a.aslots, a.tmem_cols)) throw Error(kInternal, "tc pair: TMEM plan failed");
   // wide fp16 slices (one full A slot left): two half-stage slots in its place,
   // so conversion and MMA overlap (LPCA_TC_HALFSLOTS=0 keeps the single slot)
-  const int hs_mode = env_int("LPCA_TC_HALFSLOTS", 1);  // 0 never, 1 when one full slot is left, 2 always
-  a.half_slots = kHalf && ((a.aslots == 1 && hs_mode >= 1) || hs_mode == 2) ? 1 : 0;
-  if (a.half_slots) a.aslots *= 2;
+  // wide slices keep one full slot's worth of A columns: cut it into quarter
+  // slots (K = 16), so a freed quarter is refilled while the MMAs read the other
+  // three (LPCA_TC_SLOTDIV = 1 / 2 / 4 forces full / half / quarter slots)
+  const int div = env_int("LPCA_TC_SLOTDIV", a.aslots == 1 ? 4 : 1);
+  a.half_slots = kHalf && (div == 2 || div == 4) ? div : 0;
+  if (a.half_slots) a.aslots *= a.half_slots;
   const uint32_t bk = kHalf ? 64 : 32;
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);

@@ -223,7 +223,15 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 // status[0] = pivot index + 1 on failure (pivot tol 1e-14 * max diag,
 // lazy_projector.cpp:12-37).
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
-                         int* status);
+                         int* status, double tol_rel = 1e-14);
+// C = op(A) op(B) + beta C, l x l column-major (op = transpose when ta / tb; b null = identity).
+void launch_small_gemm(cudaStream_t s, int ta, int tb, index_t l, const double* a, const double* b, double* c,
+                       double beta);
+// rdiag = 1 / diag(W) (first) or rdiag *= 1 / diag(W): diag of a product of R factors.
+void launch_rdiag_update(cudaStream_t s, const double* w, index_t l, double* rdiag, int first);
+void launch_trace(cudaStream_t s, const double* g, index_t l, double* out);
+// W = R^{-1} for an upper-triangular R, in launch_chol_inverse's layout (work: l x l).
+void launch_upper_inverse(cudaStream_t s, const double* r, index_t l, double* w, double* work, int* status);
 // g_ii += c * trace(g) (shifted CholeskyQR's first pass).
 void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c);
 // out[0] = flag[0] != 0 (an int flag made summable over ranks).

@@ -122,6 +122,8 @@ struct lpca_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   ncclComm_t comm = nullptr;
+  lpca_allreduce_fn hook = nullptr;  // caller's collective in place of NCCL
+  void* hook_user = nullptr;
   int num_sms = 148;
   int gemm_path = 0;  // 0 = tcgen05 split-TF32 for fp32 data, 1 = SIMT
   int exact = 0;      // fp64 reference summation order (tests)
@@ -137,6 +139,25 @@ struct lpca_ctx {
   bool force_scan = false;  // fit_dev retry: per-run scales by the full scan
 
   void note_launch(int n = 1) { launches += n; }
+
+  // Pinned host block for the small device->host reads of one call (status
+  // words, eigenvalues, R diagonals): cudaMemcpyAsync into pageable memory
+  // would block the host at the copy, before the work queued behind it.
+  char* pin = nullptr;
+  std::size_t pin_used = 0;
+  static constexpr std::size_t kPinBytes = 1 << 20;
+  void pin_reset() { pin_used = 0; }
+  template <typename T>
+  T* stage_read(const T* dev, index_t count) {
+    const std::size_t bytes = sizeof(T) * static_cast<std::size_t>(count > 0 ? count : 1);
+    if (!pin) LPCA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pin), kPinBytes));
+    const std::size_t off = (pin_used + 15) & ~std::size_t(15);
+    if (off + bytes > kPinBytes) throw Error(lpca::kInternal, "pinned readback block exhausted");
+    pin_used = off + bytes;
+    T* h = reinterpret_cast<T*>(pin + off);
+    if (count > 0) LPCA_CUDA(cudaMemcpyAsync(h, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, stream));
+    return h;
+  }
 
   void* buf(const std::string& name, std::size_t bytes) {
     auto it = ws.find(name);
@@ -159,8 +180,27 @@ struct lpca_ctx {
   }
   void allreduce(double* p, index_t count) {
     if (world <= 1) return;
+    if (hook) {
+      if (hook(hook_user, p, count, stream) != 0) throw Error(lpca::kNccl, "allreduce hook failed");
+      return;
+    }
     nccl_check(nccl().all_reduce(p, p, static_cast<std::size_t>(count), ncclDouble, ncclSum, comm, stream),
                "ncclAllReduce");
+  }
+  // Every rank's `k` host values: rank r's go to slots [r k, r k + k) of a zeroed
+  // world x k vector summed over ranks (an allgather through the sum
+  // collective). Synchronises the stream; world == 1 returns the input.
+  std::vector<double> gather_host(const std::vector<double>& mine) {
+    if (world <= 1) return mine;
+    const std::size_t k = mine.size(), total = k * static_cast<std::size_t>(world);
+    std::vector<double> all(total, 0.0);
+    std::copy(mine.begin(), mine.end(), all.begin() + static_cast<std::ptrdiff_t>(k * rank));
+    double* d = static_cast<double*>(buf("agree", total * sizeof(double)));
+    LPCA_CUDA(cudaMemcpyAsync(d, all.data(), total * sizeof(double), cudaMemcpyHostToDevice, stream));
+    allreduce(d, static_cast<index_t>(total));
+    LPCA_CUDA(cudaMemcpyAsync(all.data(), d, total * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    LPCA_CUDA(cudaStreamSynchronize(stream));
+    return all;
   }
 };
 
@@ -240,6 +280,7 @@ double projection_scale(const lpca_config& c) {
 void check_ctx(lpca_ctx* ctx) {
   if (!ctx) throw Error(kInvalidArgument, "null context");
   LPCA_CUDA(cudaSetDevice(ctx->device));
+  ctx->pin_reset();  // every entry point starts with an empty readback block
 }
 
 // ---- device-resident X ------------------------------------------------------
@@ -670,12 +711,143 @@ void utx_pass(lpca_ctx& ctx, const DevX& x, const Panel& u, index_t l, double* f
 // (q >= 2 makes Z's columns that close: plain CholeskyQR2 fails there, as the
 // survey's naive-power probe did), then two plain CholeskyQR passes
 // restore orthogonality. Each pass: F <- L^{-1} F with L L^T = F F^T.
-void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
+// The power step's Cholesky statuses (pivot + 1 of a failed pass, else 0).
+void check_orth_status(const int* h3) {
+  for (int p = 0; p < 3; ++p)
+    if (h3[p] != 0)
+      throw Error(kRankDeficiency, "power iteration: cholesky pivot " + S(h3[p] - 1) + " is not positive definite",
+                  h3[p] - 1);
+}
+
+// Shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020)
+// of the tall matrix A = [top; body]: top an optional l x l fp64 block (the
+// streaming reducer's running R, on this rank), body `rows` x l row-major
+// (dtype, ld) on this rank, rows of all ranks stacked when over_ranks (the
+// Gram matrices are summed). The first Cholesky factors G + s I with
+// s = 11 (M l + l (l + 1)) u ||A||_F^2 (M = global rows), which succeeds up
+// to cond(A) ~ 1/u; two plain passes restore orthogonality. Q overwrites top
+// and body. Left on the device for one deferred host check (qr_check): the
+// diagonal of R = R3 R2 R1 (the remaining column norms the reference's
+// Householder QR tests, qr.cpp:37-58), ||A||_F^2 and each pass's Cholesky
+// failure (pivot + 1). With r_out, R itself (upper, column-major l x l).
+struct QrDev {
+  double* rdiag = nullptr;
+  double* fro2 = nullptr;
+  int* st = nullptr;
+};
+
+QrDev cholqr3(lpca_ctx& ctx, double* top, void* body, int dtype, index_t rows, index_t ld, index_t l,
+              double global_rows, bool over_ranks, bool exact, double* r_out, const std::string& tag) {
+  QrDev q;
+  q.rdiag = ctx.get<double>(tag + ".rdiag", l);
+  q.fro2 = ctx.get<double>(tag + ".fro2", 1);
+  q.st = ctx.get<int>(tag + ".st", 3);
+  double* g = ctx.get<double>(tag + ".g", l * l);
+  double* w = ctx.get<double>(tag + ".w", l * l);
+  double* lm = ctx.get<double>(tag + ".lm", l * l);
+  double* tmp = ctx.get<double>(tag + ".tmp", l * l);
+  const double shift = 11.0 * (global_rows * static_cast<double>(l) + static_cast<double>(l) * (l + 1)) * 0x1p-53;
+  for (int p = 0; p < 3; ++p) {
+    // G = A^T A (this rank's rows, then summed over ranks)
+    if (rows > 0) {
+      index_t chunks = pick_chunks(ctx, rows, ceil_div(l, 64) * ceil_div(l, 64), exact);
+      const index_t chunk_rows = round_up(ceil_div(rows, chunks), 128);
+      chunks = ceil_div(rows, chunk_rows);
+      double* gpart = chunks == 1 ? g : ctx.get<double>(tag + ".gpart", chunks * l * l);
+      if (dtype == 4)
+        launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(body), ld, rows, l, chunk_rows, gpart);
+      else
+        launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(body), ld, rows, l, chunk_rows, gpart);
+      LPCA_LAUNCHED(ctx);
+      if (chunks > 1) {
+        launch_reduce_partials(ctx.stream, gpart, chunks, l * l, g);
+        LPCA_LAUNCHED(ctx);
+      }
+    } else {
+      launch_zero(ctx.stream, g, sizeof(double) * l * l);
+    }
+    if (top) {
+      launch_small_gemm(ctx.stream, 1, 0, l, top, top, g, 1.0);
+      LPCA_LAUNCHED(ctx);
+    }
+    if (over_ranks) ctx.allreduce(g, l * l);
+    if (p == 0) {
+      launch_trace(ctx.stream, g, l, q.fro2);
+      launch_add_trace_shift(ctx.stream, g, l, shift);
+      ctx.note_launch(2);
+    }
+    launch_chol_inverse(ctx.stream, g, l, w, lm, q.st + p, 0.0);
+    launch_rdiag_update(ctx.stream, w, l, q.rdiag, p == 0);
+    ctx.note_launch(2);
+    if (r_out) {  // R <- R_p R with R_p = L_p^T
+      launch_small_gemm(ctx.stream, 1, 0, l, lm, p == 0 ? nullptr : r_out, tmp, 0.0);
+      LPCA_CUDA(cudaMemcpyAsync(r_out, tmp, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, ctx.stream));
+      LPCA_LAUNCHED(ctx);
+    }
+    // Q <- Q W_p
+    if (rows > 0) {
+      void* qb = ctx.buf(tag + ".q", dsize(dtype) * rows * ld);
+      if (dtype == 8) {
+        launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(body), rows, l, ld, w, l, l,
+                                       static_cast<double*>(qb), ld, 1, exact);
+      } else {
+        float* w32 = ctx.get<float>(tag + ".w32", l * l);
+        launch_convert_f64_to_f32(ctx.stream, w, l, w32, l, l, l, 1.0);
+        LPCA_LAUNCHED(ctx);
+        launch_zero(ctx.stream, qb, sizeof(float) * rows * ld);
+        launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(body), rows, l, ld, w32, l, l,
+                                     static_cast<float*>(qb), ld, 1, false);
+      }
+      LPCA_LAUNCHED(ctx);
+      LPCA_CUDA(cudaMemcpyAsync(body, qb, dsize(dtype) * rows * ld, cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    if (top) {
+      launch_small_gemm(ctx.stream, 0, 0, l, top, w, tmp, 0.0);
+      LPCA_CUDA(cudaMemcpyAsync(top, tmp, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, ctx.stream));
+      LPCA_LAUNCHED(ctx);
+    }
+  }
+  return q;
+}
+
+// Host copies of a QrDev, valid after the stream has been synchronised.
+struct QrHost {
+  const double* rdiag = nullptr;
+  const double* fro2 = nullptr;
+  const int* st = nullptr;
+  index_t l = 0;
+};
+QrHost qr_stage(lpca_ctx& ctx, const QrDev& d, index_t l) {
+  return QrHost{ctx.stage_read(d.rdiag, l), ctx.stage_read(d.fro2, 1), ctx.stage_read(d.st, 3), l};
+}
+
+// householder_qr's rank test (qr.cpp:37-58): the first column whose remaining
+// norm |R_jj| is at most 1e-12 ||A||_F (or whose Cholesky pivot failed) is
+// numerically dependent. Returns -1 or the column; *norm gets |R_jj|.
+index_t qr_first_dependent(const QrHost& h, double* norm) {
+  const double tol = 1e-12 * std::sqrt(h.fro2[0] > 0.0 ? h.fro2[0] : 0.0);
+  for (int p = 0; p < 3; ++p)
+    if (h.st[p] != 0) {  // a pass's pivot was not positive: that column has no remaining norm
+      *norm = 0.0;
+      return h.st[p] - 1;
+    }
+  for (index_t j = 0; j < h.l; ++j) {
+    const double r = std::fabs(h.rdiag[j]);
+    if (!(r > tol)) {
+      *norm = r;
+      return j;
+    }
+  }
+  return -1;
+}
+
+void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n, int* st3 = nullptr) {
   double* g = ctx.get<double>("orth.g", l * l);
   double* w = ctx.get<double>("orth.w", l * l);
   double* lm = ctx.get<double>("orth.l", l * l);
   double* tmp = ctx.get<double>("orth.tmp", l * n);
-  int* st = ctx.get<int>("orth.status", 1);
+  const bool deferred = st3 != nullptr;
+  if (!deferred) st3 = ctx.get<int>("orth.status", 3);
   double* gpart = ctx.get<double>("gram.part", gram_fast_chunks(l, n) * l * l);
   const double shift = 11.0 * (static_cast<double>(n) * l + static_cast<double>(l) * (l + 1)) * 0x1p-53;
   for (int pass = 0; pass < 3; ++pass) {
@@ -685,16 +857,16 @@ void orth_rows(lpca_ctx& ctx, double* f, index_t l, index_t n) {
       launch_add_trace_shift(ctx.stream, g, l, shift);
       LPCA_LAUNCHED(ctx);
     }
-    launch_chol_inverse(ctx.stream, g, l, w, lm, st);
+    launch_chol_inverse(ctx.stream, g, l, w, lm, st3 + pass);
     LPCA_LAUNCHED(ctx);
-    int h = 0;
-    LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
-    if (h != 0)
-      throw Error(kRankDeficiency, "power iteration: cholesky pivot " + S(h - 1) +
-                                       " is not positive definite", h - 1);
     launch_apply_rinv_t(ctx.stream, w, l, f, n, tmp);
     LPCA_LAUNCHED(ctx);
+  }
+  if (!deferred) {
+    const int* h = ctx.stage_read(st3, 3);
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+    check_orth_status(h);
+    ctx.pin_reset();
   }
 }
 
@@ -741,7 +913,8 @@ void eigh_dev(lpca_ctx& ctx, double* a, index_t l, double* evals, double* evecs,
 // and optionally u~ (device, l x k). Throws the reference's errors.
 void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index_t k, double* v,
                      std::vector<double>& sigma, double* ut_out,
-                     const std::function<void()>& before_sync = std::function<void()>()) {
+                     const std::function<void()>& before_sync = std::function<void()>(),
+                     const std::function<void()>& pre_check = std::function<void()>()) {
   if (l > n)
     throw Error(kDimension, "truncated_svd_via_gram: F must be wide (l <= n), got " + S(l) + "x" + S(n));
   if (k < 1 || k > l)
@@ -765,12 +938,11 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
   if (ut_out) {
     LPCA_CUDA(cudaMemcpyAsync(ut_out, evecs, sizeof(double) * l * k, cudaMemcpyDeviceToDevice, ctx.stream));
   }
-  std::vector<double> lam(static_cast<std::size_t>(l));
-  int hst = 0, hsw[2] = {0, 0};
-  double hgap = 0.0;
-  LPCA_CUDA(cudaMemcpyAsync(lam.data(), evals, sizeof(double) * l, cudaMemcpyDeviceToHost, ctx.stream));
-  LPCA_CUDA(cudaMemcpyAsync(hsw, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  LPCA_CUDA(cudaMemcpyAsync(&hgap, gap, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  // pinned staging: the copies are queued, the host does not wait here
+  const double* lam = ctx.stage_read(evals, l);
+  const int* hsw = ctx.stage_read(st, 2);
+  const double* hgapp = ctx.stage_read(gap, 1);
+  int hst = 0;
   cudaEvent_t checked = nullptr;
   if (before_sync) {  // work enqueued behind the spectral step, before the host checks wait
     LPCA_CUDA(cudaEventCreateWithFlags(&checked, cudaEventDisableTiming));
@@ -781,8 +953,10 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
   } else {
     LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
   }
+  if (pre_check) pre_check();  // earlier phases' deferred checks (power steps, SPCA's QR) come first
   hst = hsw[0];
   ctx.last_sweeps = hsw[1];
+  const double hgap = hgapp[0];
   if (std::getenv("LPCA_VERBOSE")) std::fprintf(stderr, "lazypca_b200: eigh l=%lld sweeps=%d\n", (long long)l, hsw[1]);
   if (hst == 2)
     throw Error(kInvalidArgument, "eigh: input is not symmetric (max |a_ij - a_ji| = " +
@@ -791,7 +965,7 @@ void finish_spectral(lpca_ctx& ctx, const double* f, index_t l, index_t n, index
     throw Error(kConvergence, "eigh: Jacobi off-diagonal " + std::to_string(hgap) +
                                   " still above tolerance after 50 sweeps", -1, hgap);
   // rank floor (truncated_svd.cpp:28-39)
-  const double lambda_max = lam.front();
+  const double lambda_max = lam[0];
   const double floor = 1e-12 * (lambda_max > 0.0 ? lambda_max : 0.0);
   index_t safe = 0;
   while (safe < l && lam[static_cast<std::size_t>(safe)] > floor && lam[static_cast<std::size_t>(safe)] > 0.0)
@@ -816,6 +990,21 @@ using AfterSpectral = std::function<void(lpca_map&, const uint32_t*)>;
 
 lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_timings* t,
                   const AfterSpectral* after_spectral = nullptr) {
+  // Ranks first agree on the shape (one small collective), so a rank-specific
+  // input error is raised on every rank instead of leaving the others waiting
+  // in a collective; the global row count sets the QR shifts.
+  double m_global = static_cast<double>(x.m);
+  if (ctx.world > 1) {
+    const std::vector<double> all = ctx.gather_host({static_cast<double>(x.n), static_cast<double>(x.m)});
+    m_global = 0.0;
+    for (int r = 0; r < ctx.world; ++r) {
+      if (all[2 * r] != static_cast<double>(x.n))
+        throw Error(kDimension, "ranks disagree on the column count: rank " + std::to_string(r) + " has " +
+                                    S(static_cast<index_t>(all[2 * r])) + ", rank " + std::to_string(ctx.rank) +
+                                    " has " + S(x.n));
+      m_global += all[2 * r + 1];
+    }
+  }
   const lpca_config c = resolve(cfg_in, x.n);
   if (c.streaming)
     throw Error(kInvalidArgument,
@@ -889,10 +1078,14 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
     ctx.pass_slot = -1;
     double* xovf_all = nullptr;  // the flag summed over ranks: every rank reruns, or none
-    if (xovf && ctx.world > 1) {
+    if (ctx.world > 1 && !ctx.force_scan) {  // issued by every rank, with or without an fp16 sketch
       xovf_all = ctx.get<double>("xovf.all", 1);
-      launch_flag_to_f64(ctx.stream, xovf, xovf_all);
-      LPCA_LAUNCHED(ctx);
+      if (xovf) {
+        launch_flag_to_f64(ctx.stream, xovf, xovf_all);
+        LPCA_LAUNCHED(ctx);
+      } else {
+        launch_zero(ctx.stream, xovf_all, sizeof(double));
+      }
       ctx.allreduce(xovf_all, 1);
     }
     xs.use = f16;
@@ -901,7 +1094,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     // over ranks, so every rank takes the same branch). Read only after the
     // stream has drained past the flag's producer.
     auto sketch_flagged = [&]() -> bool {
-      if (!xovf) return false;
+      if (!xovf && !xovf_all) return false;
       LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
       if (xovf_all) {
         double all = 0.0;
@@ -931,6 +1124,10 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     try {
     // power iterations (builder extension; SPEC.md:371 lists them as a non-goal)
     double* f = ctx.get<double>("f", l * n);
+    // deferred checks: status words stay on the device until the one readback
+    // in front of the spectral step's host checks (no host sync per phase)
+    int* pst = c.power_iters > 0 ? ctx.get<int>("power.st", 3 * c.power_iters) : nullptr;
+    QrDev spca_qr;
     if (c.power_iters > 0) {
       double* z = ctx.get<double>("z.w", l * n);
       for (int it = 0; it < c.power_iters; ++it) {
@@ -943,7 +1140,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
         }
         utx_pass(ctx, x, u, l, f, exact, &xs);               // F = U^T X  (= Z^T)
         ctx.pass_slot = -1;
-        orth_rows(ctx, f, l, n);                             // Z <- orth(Z), shifted CholeskyQR3
+        orth_rows(ctx, f, l, n, pst + 3 * it);              // Z <- orth(Z), shifted CholeskyQR3
         launch_transpose(ctx.stream, 8, f, l, l, n, z, n);  // W = Z as n x l column-major
         LPCA_LAUNCHED(ctx);
         if (timed) {
@@ -957,58 +1154,10 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     }
     ev.mark(2);
     if (c.method == LPCA_SPCA) {
-      // CholeskyQR2 of U (the reference uses Householder QR, qr.cpp:104-132;
-      // Q is the same up to roundoff once R's diagonal is made positive).
-      double* gpart = nullptr;
-      double* gu = ctx.get<double>("spca.g", l * l);
-      double* w = ctx.get<double>("spca.w", l * l);
-      double* lm = ctx.get<double>("spca.l", l * l);
-      int* st = ctx.get<int>("spca.status", 1);
-      for (int pass = 0; pass < 2; ++pass) {
-        if (m > 0) {
-          index_t chunks = pick_chunks(ctx, m, ceil_div(l, 64) * ceil_div(l, 64), exact);
-          index_t chunk_rows = round_up(ceil_div(m, chunks), 128);
-          chunks = ceil_div(m, chunk_rows);
-          gpart = chunks == 1 ? gu : ctx.get<double>("spca.gpart", chunks * l * l);
-          if (x.dtype == 4)
-            launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld, m, l, chunk_rows, gpart);
-          else
-            launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u.plain), u.ld, m, l, chunk_rows, gpart);
-          LPCA_LAUNCHED(ctx);
-          if (chunks > 1) {
-            launch_reduce_partials(ctx.stream, gpart, chunks, l * l, gu);
-            LPCA_LAUNCHED(ctx);
-          }
-        } else {
-          launch_zero(ctx.stream, gu, sizeof(double) * l * l);
-        }
-        ctx.allreduce(gu, l * l);
-        launch_chol_inverse(ctx.stream, gu, l, w, lm, st);
-        LPCA_LAUNCHED(ctx);
-        int h = 0;
-        LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
-        if (h != 0)
-          throw Error(kRankDeficiency, "qr: column " + S(h - 1) +
-                                           " is numerically dependent on earlier columns", h - 1);
-        if (m > 0) {
-          // Q = U R^{-1}: the sketch GEMM with X := U (m x l) and W := R^{-1}
-          void* q = ctx.buf("q", dsize(x.dtype) * m * u.ld);
-          if (x.dtype == 8) {
-            launch_xw_simt<double, double>(ctx.stream, static_cast<const double*>(u.plain), m, l, u.ld, w,
-                                           l, l, static_cast<double*>(q), u.ld, 1, exact);
-          } else {
-            float* w32 = ctx.get<float>("spca.w32", l * l);
-            launch_convert_f64_to_f32(ctx.stream, w, l, w32, l, l, l, 1.0);
-            LPCA_LAUNCHED(ctx);
-            launch_zero(ctx.stream, q, sizeof(float) * m * u.ld);
-            launch_xw_simt<float, float>(ctx.stream, static_cast<const float*>(u.plain), m, l, u.ld, w32,
-                                         l, l, static_cast<float*>(q), u.ld, 1, false);
-          }
-          LPCA_LAUNCHED(ctx);
-          LPCA_CUDA(cudaMemcpyAsync(u.plain, q, dsize(x.dtype) * m * u.ld, cudaMemcpyDeviceToDevice, ctx.stream));
-        }
-      }
+      // Q of U by shifted CholeskyQR3 (the reference: householder_qr,
+      // qr.cpp:104-132; the same Q once R's diagonal is positive, the same rank
+      // test on R's diagonal, checked with the spectral step's readback)
+      spca_qr = cholqr3(ctx, nullptr, u.plain, x.dtype, m, u.ld, l, m_global, true, exact, nullptr, "spca");
       if (u.hi && m > 0) {  // Q's tf32 planes for the tensor-core F = Q^T X
         launch_split_tf32_transpose(ctx.stream, static_cast<const float*>(u.plain), m, l, u.ld, u.hi, u.lo,
                                     u.ldt);
@@ -1022,16 +1171,31 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     utx_pass(ctx, x, u, l, f, exact, &xs);  // F = U^T X (or Q^T X)
     ctx.pass_slot = -1;
     ev.mark(4);
-    if (f16) LPCA_CUDA(cudaMemcpyAsync(&map->xmax, xs.dev, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
+    const float* xmax_h = f16 ? ctx.stage_read(reinterpret_cast<const float*>(xs.dev), 1) : nullptr;
+    const int* pst_h = pst ? ctx.stage_read(pst, 3 * c.power_iters) : nullptr;
+    QrHost qr_h;
+    if (spca_qr.rdiag) qr_h = qr_stage(ctx, spca_qr, l);
+    auto pre_check = [&] {  // in the reference's order: power steps, then the QR
+      if (xmax_h) map->xmax = xmax_h[0];
+      for (int it = 0; pst_h && it < c.power_iters; ++it) check_orth_status(pst_h + 3 * it);
+      if (qr_h.rdiag) {
+        double norm = 0.0;
+        const index_t j = qr_first_dependent(qr_h, &norm);
+        if (j >= 0)
+          throw Error(kRankDeficiency, "qr: column " + S(j) + " is numerically dependent on earlier columns" +
+                                           " (remaining norm " + std::to_string(norm) + ")",
+                      j);
+      }
+    };
     bool marked = false;
     if (after_spectral) {
       finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr, [&] {
         ev.mark(5);
         marked = true;
         (*after_spectral)(*map, f16 ? xs.dev : nullptr);
-      });
+      }, pre_check);
     } else {
-      finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr);
+      finish_spectral(ctx, f, l, n, k, map->v, map->sigma, nullptr, std::function<void()>(), pre_check);
     }
     if (!marked) ev.mark(5);
     LPCA_CUDA(cudaEventSynchronize(ctx.ev[5]));
@@ -1272,24 +1436,61 @@ struct BlockStager {
   }
 };
 
-// Streaming Lazy SPCA (Algorithm 4) and SPCA (Algorithm 3): one pass over the
-// blocks accumulating F = sum_s U_s^T X_s (gemm_t_add) and, for SPCA, the Gram
-// U^T U = sum_s U_s^T U_s whose Cholesky factor R stands in for the reference's
-// stacked Householder R (qr.cpp:134-142; equal up to roundoff at full rank);
-// then F <- R^{-T} F (solve_rt_in_place) and the spectral step. Ranks reduce
-// their own blocks and sum F (and U^T U) with one allreduce each at the end.
+// Streaming Lazy SPCA (Algorithm 4) and SPCA (Algorithm 3), reducer.cpp:236-335:
+// one pass over the blocks accumulating F = sum_s U_s^T X_s (gemm_t_add). SPCA
+// also carries the running R of the stacked sketch, R_s = qr_r([R_{s-1}; U_s])
+// (qr.cpp:134-142, reducer.cpp:276-292), here by shifted CholeskyQR3 of the
+// stacked matrix with the reference's per-slice rank test ("slice s: qr: ...",
+// index s); at the end F <- R^{-T} F (solve_rt_in_place, reducer.cpp:55-73,
+// with its 1e-12 ||R||_F diagonal test). Ranks reduce their own blocks; a rank's
+// errors are held until every rank reaches the first collective and agree on
+// them there (so no rank is left waiting), the ranks' R factors are stacked
+// (an allgather through the sum collective) and reduced once more, and F is
+// summed with one allreduce. A rank with an empty stream contributes nothing.
 lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& src, lpca_timings* t) {
   BlockStager stager(ctx);
   lpca_matrix_view v{};
   int64_t slice = -1;
-  if (!src.next(&v, &slice)) throw Error(kInvalidArgument, "streaming: the block stream is empty");
-  if (slice != 0) throw Error(kInvalidArgument, "streaming: first slice index must be 0, got " + S(slice));
-  check_view(&v);
-  lpca_config c = resolve(cfg_in, v.cols);
+  const bool dist = ctx.world > 1;
+  // Errors before the first collective: raised at once on a single rank, held
+  // and agreed on with world > 1.
+  std::unique_ptr<Error> held;
+  auto hold = [&](const Error& e) {
+    if (!dist) throw e;
+    if (!held) held = std::make_unique<Error>(e);
+  };
+  bool have = false;
+  try {
+    have = src.next(&v, &slice);
+    if (have) {
+      if (slice != 0) throw Error(kInvalidArgument, "streaming: first slice index must be 0, got " + S(slice));
+      check_view(&v);
+    } else if (!dist) {
+      throw Error(kInvalidArgument, "streaming: the block stream is empty");
+    }
+  } catch (const Error& e) {
+    hold(e);
+    have = false;
+  }
+  index_t n = have ? v.cols : 0;
+  if (dist) {  // agree on the width (ranks with an empty stream take it from the others)
+    const std::vector<double> all = ctx.gather_host({have ? 1.0 : 0.0, static_cast<double>(n)});
+    index_t nn = -1;
+    for (int r = 0; r < ctx.world; ++r) {
+      if (all[2 * r] == 0.0) continue;
+      const index_t nr = static_cast<index_t>(all[2 * r + 1]);
+      if (nn >= 0 && nr != nn)
+        throw Error(kDimension, "streaming: ranks disagree on the column count (" + S(nn) + " vs " + S(nr) + ")");
+      nn = nr;
+    }
+    if (nn < 0) throw Error(kInvalidArgument, "streaming: the block stream is empty on every rank");
+    n = nn;
+  }
+  lpca_config c = resolve(cfg_in, n);
   if (c.power_iters > 0)
     throw Error(kInvalidArgument,
                 "streaming: power iterations read the data more than once; use the in-core reducers");
-  const index_t n = c.proj_n, l = c.l, k = c.k;
+  const index_t l = c.l, k = c.k;
   PhaseEvents ev(ctx);
   ev.mark(0);
   auto map = std::make_unique<lpca_map>();
@@ -1318,106 +1519,138 @@ lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& 
   const bool spca = c.method == LPCA_SPCA;
   double* f = ctx.get<double>("stream.f", l * n);
   double* fb = ctx.get<double>("stream.fb", l * n);
-  double* g = spca ? ctx.get<double>("stream.g", l * l) : nullptr;
-  double* gb = spca ? ctx.get<double>("stream.gb", l * l) : nullptr;
+  double* rrun = spca ? ctx.get<double>("stream.r", l * l) : nullptr;   // running R (upper, column-major)
+  double* rtop = spca ? ctx.get<double>("stream.rtop", l * l) : nullptr;  // R_{s-1} as the stacked top block
   launch_zero(ctx.stream, f, sizeof(double) * l * n);
-  if (spca) launch_zero(ctx.stream, g, sizeof(double) * l * l);
+  if (spca) launch_zero(ctx.stream, rrun, sizeof(double) * l * l);
   uint32_t* xmax = ctx.get<uint32_t>("xmax", 1);
   double sk = 0, ff = 0, qr = 0, h2d = 0;
   index_t expected = 0;
   bool first = true;
-  for (;;) {
-    if (!first) {
-      stager.before_next();
-      if (!src.next(&v, &slice)) break;
-      // pull(): slice order and width (reducer.cpp:101-113)
-      if (slice != expected)
-        throw Error(kInvalidArgument, "streaming: expected slice " + S(expected) + ", got " + S(slice));
-      check_view(&v);
-      if (v.cols != n)
-        throw Error(kDimension, "streaming: block has " + S(v.cols) + " columns but the projection expects " + S(n));
+  try {
+    while (have) {
+      if (!first) {
+        stager.before_next();
+        if (!src.next(&v, &slice)) break;
+        // pull(): slice order and width (reducer.cpp:101-113)
+        if (slice != expected)
+          throw Error(kInvalidArgument, "streaming: expected slice " + S(expected) + ", got " + S(slice));
+        check_view(&v);
+        if (v.cols != n)
+          throw Error(kDimension,
+                      "streaming: block has " + S(v.cols) + " columns but the projection expects " + S(n));
+      }
+      if (spca && first && v.rows < l)
+        throw Error(kDimension, "streaming spca: first block has " + S(v.rows) +
+                                    " rows; the orthonormal route needs at least l = " + S(l));
+      ++expected;
+      const DevX x = stager.stage(&v, &h2d);
+      if (x.m > 0) {
+        const bool exact = ctx.exact != 0 && x.dtype == 8;
+        const bool tc = use_tc(ctx, x, l);
+        const bool f16 = tc && tc_pair_mode() && f16_enabled() && !spca;
+        XScale xs;
+        xs.dev = xmax;
+        Panel u;
+        u.ld = round_up(l, 16);
+        if (!tc || spca) u.plain = ctx.buf("stream.u", dsize(x.dtype) * x.m * u.ld);
+        if (f16) {
+          launch_zero(ctx.stream, xmax, sizeof(uint32_t));
+          u.ldt16 = round_up(x.m, 8);
+          u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
+          u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
+          u.uinv = ctx.get<float>("u.inv", ceil_div(x.m, kUScaleRows) * u.ld);
+        } else if (tc) {
+          u.ldt = planes_ld(x.m);
+          u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
+          u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
+        }
+        ev.mark(1);
+        XScale sketch;
+        sketch.use = true;
+        sketch.check = xmax;
+        xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);  // U_s = X_s Omega
+        xs.use = f16;
+        ev.mark(2);
+        if (x.sparse()) {  // gemm_t_add continues the running sums: bitwise the reference's streaming
+          launch_gemm_t_csc(ctx.stream, n, x.cp, x.ri, x.cv, static_cast<const double*>(u.plain), u.ld, l, f, true);
+          LPCA_LAUNCHED(ctx);
+        } else {
+          utx_pass(ctx, x, u, l, fb, exact, &xs, false);  // F += U_s^T X_s
+          launch_add_f64(ctx.stream, fb, f, l * n);
+          LPCA_LAUNCHED(ctx);
+        }
+        ev.mark(3);
+        if (spca) {  // R_s = qr_r([R_{s-1}; U_s]) (U_s is consumed)
+          LPCA_CUDA(cudaMemcpyAsync(rtop, rrun, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, ctx.stream));
+          const QrDev qd = cholqr3(ctx, first ? nullptr : rtop, u.plain, x.dtype, x.m, u.ld, l,
+                                   static_cast<double>(x.m + (first ? 0 : l)), false, exact, rrun, "stream.qr");
+          const QrHost qh = qr_stage(ctx, qd, l);
+          ev.mark(4);
+          LPCA_CUDA(cudaEventSynchronize(ctx.ev[4]));
+          double norm = 0.0;
+          const index_t j = qr_first_dependent(qh, &norm);
+          if (j >= 0)
+            throw Error(kRankDeficiency, "slice " + S(slice) + ": qr: column " + S(j) +
+                                             " is numerically dependent on earlier columns (remaining norm " +
+                                             std::to_string(norm) + ")",
+                        slice);
+          ctx.pin_reset();
+        } else {
+          ev.mark(4);
+          LPCA_CUDA(cudaEventSynchronize(ctx.ev[4]));
+        }
+        sk += ev.secs(1, 2);
+        ff += ev.secs(2, 3);
+        qr += ev.secs(3, 4);
+      }
+      stager.release();
+      first = false;
     }
-    if (spca && first && v.rows < l)
-      throw Error(kDimension, "streaming spca: first block has " + S(v.rows) +
-                                  " rows; the orthonormal route needs at least l = " + S(l));
-    ++expected;
-    const DevX x = stager.stage(&v, &h2d);
-    if (x.m > 0) {
-      const bool exact = ctx.exact != 0 && x.dtype == 8;
-      const bool tc = use_tc(ctx, x, l);
-      const bool f16 = tc && tc_pair_mode() && f16_enabled() && !spca;
-      XScale xs;
-      xs.dev = xmax;
-      Panel u;
-      u.ld = round_up(l, 16);
-      if (!tc || spca) u.plain = ctx.buf("stream.u", dsize(x.dtype) * x.m * u.ld);
-      if (f16) {
-        launch_zero(ctx.stream, xmax, sizeof(uint32_t));
-        u.ldt16 = round_up(x.m, 8);
-        u.h16hi = ctx.get<__half>("u.h16hi", u.ld * u.ldt16);
-        u.h16lo = ctx.get<__half>("u.h16lo", u.ld * u.ldt16);
-        u.uinv = ctx.get<float>("u.inv", ceil_div(x.m, kUScaleRows) * u.ld);
-      } else if (tc) {
-        u.ldt = planes_ld(x.m);
-        u.hi = ctx.get<float>("u.hi", u.ld * u.ldt);
-        u.lo = ctx.get<float>("u.lo", u.ld * u.ldt);
-      }
-      ev.mark(1);
-      XScale sketch;
-      sketch.use = true;
-      sketch.check = xmax;
-      xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);  // U_s = X_s Omega
-      xs.use = f16;
-      ev.mark(2);
-      if (x.sparse()) {  // gemm_t_add continues the running sums: bitwise the reference's streaming
-        launch_gemm_t_csc(ctx.stream, n, x.cp, x.ri, x.cv, static_cast<const double*>(u.plain), u.ld, l, f, true);
-        LPCA_LAUNCHED(ctx);
-      } else {
-        utx_pass(ctx, x, u, l, fb, exact, &xs, false);  // F += U_s^T X_s
-        launch_add_f64(ctx.stream, fb, f, l * n);
-        LPCA_LAUNCHED(ctx);
-      }
-      ev.mark(3);
-      if (spca) {  // U^T U += U_s^T U_s
-        index_t chunks = pick_chunks(ctx, x.m, ceil_div(l, 64) * ceil_div(l, 64), exact);
-        const index_t chunk_rows = round_up(ceil_div(x.m, chunks), 128);
-        chunks = ceil_div(x.m, chunk_rows);
-        double* gpart = ctx.get<double>("stream.gpart", chunks * l * l);
-        if (x.dtype == 4)
-          launch_syrk_partials<float>(ctx.stream, static_cast<const float*>(u.plain), u.ld, x.m, l, chunk_rows, gpart);
-        else
-          launch_syrk_partials<double>(ctx.stream, static_cast<const double*>(u.plain), u.ld, x.m, l, chunk_rows,
-                                       gpart);
-        LPCA_LAUNCHED(ctx);
-        launch_reduce_partials(ctx.stream, gpart, chunks, l * l, gb);
-        LPCA_LAUNCHED(ctx);
-        launch_add_f64(ctx.stream, gb, g, l * l);
-        LPCA_LAUNCHED(ctx);
-      }
-      ev.mark(4);
-      LPCA_CUDA(cudaEventSynchronize(ctx.ev[4]));
-      sk += ev.secs(1, 2);
-      ff += ev.secs(2, 3);
-      qr += ev.secs(3, 4);
+  } catch (const Error& e) {
+    hold(e);
+  }
+  if (dist) {  // every rank arrives here: agree on the held errors (lowest rank's first)
+    const std::vector<double> all = ctx.gather_host(
+        {held ? static_cast<double>(held->code) : 0.0, held ? static_cast<double>(held->index) : -1.0});
+    for (int r = 0; r < ctx.world; ++r) {
+      if (all[2 * r] == 0.0) continue;
+      if (held && r == ctx.rank) throw *held;
+      throw Error(static_cast<int>(all[2 * r]), "streaming: rank " + std::to_string(r) + " failed (see its error)",
+                  static_cast<std::int64_t>(all[2 * r + 1]));
     }
-    stager.release();
-    first = false;
   }
   ev.mark(1);
   ctx.allreduce(f, l * n);
   if (spca) {
-    ctx.allreduce(g, l * l);
+    double* r = rrun;
+    if (dist) {  // stack every rank's R and reduce the stack once more
+      const index_t wl = static_cast<index_t>(ctx.world) * l;
+      double* stack = ctx.get<double>("stream.rstack", wl * l);  // row-major (world l) x l
+      double* rt = ctx.get<double>("stream.rt", l * l);
+      launch_zero(ctx.stream, stack, sizeof(double) * wl * l);
+      launch_transpose(ctx.stream, 8, rrun, l, l, l, rt, l);  // column-major R -> row-major
+      LPCA_LAUNCHED(ctx);
+      LPCA_CUDA(cudaMemcpyAsync(stack + static_cast<index_t>(ctx.rank) * l * l, rt, sizeof(double) * l * l,
+                                cudaMemcpyDeviceToDevice, ctx.stream));
+      ctx.allreduce(stack, wl * l);
+      r = ctx.get<double>("stream.rall", l * l);
+      cholqr3(ctx, nullptr, stack, 8, wl, l, l, static_cast<double>(wl), false, false, r, "stream.qr2");
+    }
+    // solve_rt_in_place's test (reducer.cpp:55-73): |R_ii| <= 1e-12 ||R||_F
+    const double* rh = ctx.stage_read(r, l * l);
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+    double fro = 0.0;
+    for (index_t e = 0; e < l * l; ++e) fro += rh[e] * rh[e];
+    const double tol = 1e-12 * std::sqrt(fro);
+    for (index_t i = 0; i < l; ++i)
+      if (!(std::fabs(rh[i * l + i]) > tol))
+        throw Error(kRankDeficiency, "triangular solve: R diagonal entry " + S(i) + " is numerically zero", i);
     double* w = ctx.get<double>("spca.w", l * l);
     double* lm = ctx.get<double>("spca.l", l * l);
     int* st = ctx.get<int>("spca.status", 1);
-    launch_chol_inverse(ctx.stream, g, l, w, lm, st);
+    launch_upper_inverse(ctx.stream, r, l, w, lm, st);
     LPCA_LAUNCHED(ctx);
-    int h = 0;
-    LPCA_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
-    if (h != 0)  // solve_rt_in_place's check (reducer.cpp:55-73)
-      throw Error(kRankDeficiency,
-                  "triangular solve: R diagonal entry " + S(h - 1) + " is numerically zero", h - 1);
     launch_apply_rinv_t(ctx.stream, w, l, f, n, ctx.get<double>("orth.tmp", l * n));  // F <- R^{-T} F
     LPCA_LAUNCHED(ctx);
   }
@@ -1430,7 +1663,6 @@ lpca_map* fit_stream_dev(lpca_ctx& ctx, const lpca_config& cfg_in, BlockSource& 
     t->f_form += ff;
     t->qr += qr + ev.secs(1, 2);
     t->svd += ev.secs(2, 3);
-    t->h2d += 0.0;
     t->total += ev.secs(0, 3);
   }
   (void)h2d;
@@ -1466,32 +1698,56 @@ lpca_status lpca_nccl_unique_id(void* out_128_bytes) {
   });
 }
 
+namespace {
+lpca_ctx* make_ctx(int32_t device, int32_t rank, int32_t world) {
+  if (world < 1 || rank < 0 || rank >= world) throw Error(kInvalidArgument, "bad rank/world");
+  int count = 0;
+  LPCA_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    throw Error(kCuda, "device " + std::to_string(device) + " not present (" + std::to_string(count) + " visible)");
+  cudaDeviceProp prop;
+  LPCA_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    throw Error(kCuda, "lazypca_b200 needs an sm_100 (B200) device; found sm_" + std::to_string(prop.major) +
+                           std::to_string(prop.minor));
+  LPCA_CUDA(cudaSetDevice(device));
+  auto ctx = new lpca_ctx();
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->num_sms = num_sms_of(device);
+  const char* path = std::getenv("LPCA_GEMM_PATH");
+  if (path && std::string(path) == "simt") ctx->gemm_path = 1;
+  const cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    LPCA_CUDA(e);
+  }
+  ctx->stream = ctx->own_stream;
+  return ctx;
+}
+}  // namespace
+
+lpca_status lpca_ctx_create_hooked(int32_t device, int32_t rank, int32_t world, lpca_allreduce_fn fn, void* user,
+                                   lpca_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalidArgument, "null output");
+    *out = nullptr;
+    if (world > 1 && !fn) throw Error(kInvalidArgument, "world > 1 needs an allreduce function");
+    lpca_ctx* ctx = make_ctx(device, rank, world);
+    ctx->hook = fn;
+    ctx->hook_user = user;
+    *out = ctx;
+  });
+}
+
 lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
                                  const void* nccl_id_128, lpca_ctx** out) {
   return guarded([&] {
     if (!out) throw Error(kInvalidArgument, "null output");
     *out = nullptr;
-    if (world < 1 || rank < 0 || rank >= world) throw Error(kInvalidArgument, "bad rank/world");
-    int count = 0;
-    LPCA_CUDA(cudaGetDeviceCount(&count));
-    if (device < 0 || device >= count)
-      throw Error(kCuda, "device " + std::to_string(device) + " not present (" + std::to_string(count) + " visible)");
-    cudaDeviceProp prop;
-    LPCA_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10)
-      throw Error(kCuda, "lazypca_b200 needs an sm_100 (B200) device; found sm_" +
-                             std::to_string(prop.major) + std::to_string(prop.minor));
-    LPCA_CUDA(cudaSetDevice(device));
-    auto ctx = new lpca_ctx();
-    ctx->device = device;
-    ctx->rank = rank;
-    ctx->world = world;
-    ctx->num_sms = num_sms_of(device);
-    const char* path = std::getenv("LPCA_GEMM_PATH");
-    if (path && std::string(path) == "simt") ctx->gemm_path = 1;
+    lpca_ctx* ctx = make_ctx(device, rank, world);
     try {
-      LPCA_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
-      ctx->stream = ctx->own_stream;
       if (world > 1) {
         if (!nccl_id_128) throw Error(kInvalidArgument, "world > 1 needs an NCCL unique id");
         ncclUniqueId id;
@@ -1499,7 +1755,7 @@ lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
         nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
       }
     } catch (...) {
-      delete ctx;
+      lpca_ctx_destroy(ctx);
       throw;
     }
     *out = ctx;
@@ -1519,6 +1775,7 @@ lpca_status lpca_ctx_destroy(lpca_ctx* ctx) {
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
     if (ctx->comm) nccl().comm_destroy(ctx->comm);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });

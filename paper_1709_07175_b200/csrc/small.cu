@@ -357,7 +357,8 @@ __global__ void chol_copy_kernel(const double* __restrict__ g, index_t l, double
 // Panel [p0, p0 + nb) x rows [p0, l): factor in shared memory (or in place
 // when the panel exceeds it, in_smem = 0), write back.
 __global__ void __launch_bounds__(256) chol_panel_kernel(const double* __restrict__ g, index_t l, index_t p0,
-                                                         double* __restrict__ lm, int* status, int in_smem) {
+                                                         double* __restrict__ lm, int* status, int in_smem,
+                                                         double tol_rel) {
   extern __shared__ double psh[];  // [nb][rows] column-major panel
   __shared__ double red[32];
   __shared__ int fail;
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(const double* __restric
   double maxd = 0.0;
   for (index_t j = threadIdx.x; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
   block_max_reduce(maxd, red);
-  const double tol = 1e-14 * maxd;
+  const double tol = tol_rel * maxd;
   if (threadIdx.x == 0) fail = 0;
   if (in_smem) {
     for (index_t e = threadIdx.x; e < rows * nb; e += blockDim.x) {
@@ -570,7 +571,7 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 }
 
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
-                         int* status) {
+                         int* status, double tol_rel) {
   if (l <= 0) return;
   LPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
   chol_copy_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(g, l, work);
@@ -580,7 +581,7 @@ void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rin
   LPCA_CUDA(cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(psm > 48 * 1024 ? psm : 48 * 1024)));
   for (index_t p0 = 0; p0 < l; p0 += kCholNb) {
-    chol_panel_kernel<<<1, 256, psm, s>>>(g, l, p0, work, status, in_smem);
+    chol_panel_kernel<<<1, 256, psm, s>>>(g, l, p0, work, status, in_smem, tol_rel);
     const index_t t = l - p0 - kCholNb;
     if (t > 0) {
       const unsigned tiles = static_cast<unsigned>(ceil_div(t, 32));
@@ -632,6 +633,83 @@ void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* 
   apply_linv_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(rinv, l, f, n, tmp);
   LPCA_CUDA(cudaMemcpyAsync(f, tmp, static_cast<std::size_t>(total) * sizeof(double),
                             cudaMemcpyDeviceToDevice, s));
+}
+
+// ---- pieces of shifted CholeskyQR3 (lpca.cu cholqr3) ---------------------------
+namespace {
+// C = op(A) op(B) + beta C for l x l column-major matrices (op = transpose when
+// the flag is set); one thread per output, fixed k order.
+__global__ void small_gemm_kernel(int ta, int tb, index_t l, const double* __restrict__ a,
+                                  const double* __restrict__ b, double* __restrict__ c, double beta) {
+  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (e >= l * l) return;
+  const index_t j = e / l, i = e % l;
+  double acc = 0.0;
+  for (index_t k = 0; k < l; ++k) {
+    const double av = ta ? a[i * l + k] : a[k * l + i];
+    const double bv = !b ? (k == j ? 1.0 : 0.0) : tb ? b[k * l + j] : b[j * l + k];  // null B = identity
+    acc = fma(av, bv, acc);
+  }
+  c[e] = beta != 0.0 ? fma(beta, c[e], acc) : acc;
+}
+
+// rdiag = diag(R_p) (first pass) or rdiag *= diag(R_p), with diag(R_p) = 1 / W_jj
+// for W = R_p^{-1} as launch_chol_inverse writes it.
+__global__ void rdiag_update_kernel(const double* __restrict__ w, index_t l, double* __restrict__ rdiag, int first) {
+  const index_t j = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (j >= l) return;
+  const double d = 1.0 / w[j * l + j];
+  rdiag[j] = first ? d : rdiag[j] * d;
+}
+
+__global__ void trace_kernel(const double* __restrict__ g, index_t l, double* out) {
+  __shared__ double red[32];
+  double t = 0.0;
+  for (index_t j = threadIdx.x; j < l; j += blockDim.x) t += g[j * l + j];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) out[0] = t;
+  }
+}
+
+// lm (lower, column-major) = R^T for an upper-triangular R; zeros above.
+__global__ void upper_to_lower_kernel(const double* __restrict__ r, index_t l, double* __restrict__ lm) {
+  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
+  if (e >= l * l) return;
+  const index_t c = e / l, i = e % l;
+  lm[e] = i >= c ? r[i * l + c] : 0.0;
+}
+}  // namespace
+
+void launch_small_gemm(cudaStream_t s, int ta, int tb, index_t l, const double* a, const double* b, double* c,
+                       double beta) {
+  if (l <= 0) return;
+  small_gemm_kernel<<<static_cast<unsigned>(ceil_div(l * l, 128)), 128, 0, s>>>(ta, tb, l, a, b, c, beta);
+}
+
+void launch_rdiag_update(cudaStream_t s, const double* w, index_t l, double* rdiag, int first) {
+  if (l <= 0) return;
+  rdiag_update_kernel<<<static_cast<unsigned>(ceil_div(l, 128)), 128, 0, s>>>(w, l, rdiag, first);
+}
+
+void launch_trace(cudaStream_t s, const double* g, index_t l, double* out) { trace_kernel<<<1, 1024, 0, s>>>(g, l, out); }
+
+// W = R^{-1} (launch_chol_inverse's layout) of an upper-triangular R.
+void launch_upper_inverse(cudaStream_t s, const double* r, index_t l, double* w, double* work, int* status) {
+  if (l <= 0) return;
+  LPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  upper_to_lower_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(r, l, work);
+  int wpb = 8;
+  while (wpb > 1 && static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
+  const std::size_t ism = static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double);
+  if (ism > 227 * 1024) throw Error(kInternal, "upper_inverse: l too large for the shared-memory solve");
+  LPCA_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ism > 48 * 1024 ? ism : 48 * 1024)));
+  chol_inv_kernel<<<static_cast<unsigned>(ceil_div(l, wpb)), 32 * wpb, ism, s>>>(work, l, w, status);
 }
 
 }  // namespace lpca

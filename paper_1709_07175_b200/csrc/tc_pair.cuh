@@ -48,7 +48,8 @@ struct PairArgs {
   int m, n;          // X is m x n
   int npad;          // UMMA N (multiple of 16); each CTA holds npad / 2 rows of B
   int stages, aslots, nrb, run_stages;
-  int half_slots;  // fp16: A ring of half-stage slots (32 columns, K = 32) when only one full slot fits
+  int half_slots;  // fp16 A ring granularity: 0 = full-stage slots (64 columns, K = 64), 2 = half-stage
+                   // slots (32 columns, K = 32), 4 = quarter-stage slots (16 columns, K = 16)
   uint32_t tmem_cols;
   int items;
   int chunk_rows;    // XTU: rows per chunk (multiple of 128)
@@ -172,6 +173,19 @@ __device__ __forceinline__ void mma_half_pair(uint32_t d, uint32_t a_hi, uint32_
 }
 #undef LPCA_PAIR_HALF
 
+// A quarter stage (K = 16, fp16): 3 MMAs from a 16-column quarter slot (hi 8, lo 8).
+__device__ __forceinline__ void mma_quarter_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                                 uint32_t idesc, uint32_t acc_first) {
+  asm volatile(
+      "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %3, %5, p;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], [%2], %3, %5, t;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %4, %5, t;\n"
+      "}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first), "r"(0u)
+      : "memory");
+}
+
 template <bool kHalf>
 __device__ __forceinline__ void mma_stage_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
                                                uint32_t idesc, uint32_t acc_first) {
@@ -243,6 +257,17 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 __device__ __forceinline__ void split_f16_32(const float (&v)[32], float (&hi)[16], float (&lo)[16]) {
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
+    const __half2 h = __floats2half2_rn(v[2 * c], v[2 * c + 1]);
+    const float2 hf = __half22float2(h);
+    hi[c] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h));
+    lo[c] = __uint_as_float(pack_h2(v[2 * c] - hf.x, v[2 * c + 1] - hf.y));
+  }
+}
+
+// Splits 16 consecutive-K values (already scaled) into 8 packed hi and 8 packed lo columns.
+__device__ __forceinline__ void split_f16_16(const float* v, float (&hi)[8], float (&lo)[8]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
     const __half2 h = __floats2half2_rn(v[2 * c], v[2 * c + 1]);
     const float2 hf = __half22float2(h);
     hi[c] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h));
@@ -410,6 +435,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint64_t bh = desc0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
             const uint64_t bl = bh + static_cast<uint64_t>(bh_bytes >> 4);
+            if (kHalf && a.half_slots == 4) {
+              // four quarter slots per stage (K = 16 each): a freed quarter is
+              // refilled while the MMAs read the other three (B rows advance 2
+              // descriptor units = 32 B per quarter)
+              for (int hh = 0; hh < 4; ++hh) {
+                if (hh > 0) {
+                  PP_T0();
+                  mbar_wait(&conv[aslot], aphase, 3);
+                  PP_ADD(3);
+                  tc_fence_after();
+                }
+                const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 16);
+                if (elect_one()) {
+                  mma_quarter_pair(d, at, at + 8, bh + 2 * hh, bl + 2 * hh, idesc, (k != q0 || hh) ? 1u : 0u);
+                  if (hh == 3) mma_commit_pair(&empty[stage]);
+                  mma_commit_pair(&aempty[aslot]);
+                }
+                __syncwarp();
+                ring_advance(aslot, aphase, AS);
+              }
+              ring_advance(stage, phase, S);
+              continue;
+            }
             if (kHalf && a.half_slots) {
               // two half slots per stage: the converters fill one while the
               // MMAs read the other (B rows advance 4 descriptor units per half)
@@ -532,7 +580,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           tc_fence_after();
           const uint8_t* xt = smem + stage * stage_bytes;
-          const uint32_t at = lane_base + a_col0 + static_cast<uint32_t>(aslot * (a.half_slots ? 32 : 64));
+          const uint32_t at =
+              lane_base + a_col0 + static_cast<uint32_t>(aslot * (a.half_slots == 4 ? 16 : a.half_slots ? 32 : 64));
           if (kHalf) {
             float v0[32], v1[32];
 #ifdef LPCA_PAIR_PROF
@@ -565,7 +614,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
             float hi[16], lo[16];
-            if (a.half_slots) {  // half 0 -> this slot, then half 1 -> the next one
+            if (a.half_slots == 4) {  // quarters 0..3 -> four consecutive slots (the first one is held)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                float h8[8], l8[8];
+                split_f16_16((qq < 2 ? v0 : v1) + 16 * (qq & 1), h8, l8);
+                if (qq > 0) {
+                  ring_advance(aslot, aphase, AS);
+                  mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+                  tc_fence_after();
+                }
+                const uint32_t aq = lane_base + a_col0 + static_cast<uint32_t>(aslot * 16);
+                tmem_st8(aq, h8);
+                tmem_st8(aq + 8, l8);
+                if (qq < 3) {
+                  tmem_st_wait();
+                  tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&conv[aslot]), 0));
+                }
+              }
+            } else if (a.half_slots) {  // half 0 -> this slot, then half 1 -> the next one
               split_f16_32(v0, hi, lo);
               tmem_st16(at, hi);
               tmem_st16(at + 16, lo);

@@ -137,6 +137,9 @@ struct lpca_ctx {
   std::unordered_set<lpca_map*> live_maps;  // maps whose V was allocated on this context's stream
   int pass_slot = -1;  // >= 0: the next X pass records ev[pass_slot] / ev[pass_slot + 1] around its kernel
   bool force_scan = false;  // fit_dev retry: per-run scales by the full scan
+  // the last transform's fp16 range flag (pinned host copy) and its scanned redo
+  const int* tr_flag = nullptr;
+  std::function<void()> tr_redo;
 
   void note_launch(int n = 1) { launches += n; }
 
@@ -1226,6 +1229,14 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
 // Y = X V into a caller buffer (apply_map, reducer.cpp:348-353).
 void transform_finish(lpca_ctx& ctx, lpca_timings* t) {
   LPCA_CUDA(cudaEventSynchronize(ctx.ev[8]));
+  const int* flag = ctx.tr_flag;
+  auto redo = std::move(ctx.tr_redo);
+  ctx.tr_flag = nullptr;
+  ctx.tr_redo = nullptr;
+  if (flag && *flag && redo) {  // a run's first-stage scale did not cover the run
+    redo();
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
   if (t) {
     float a = 0.f, b = 0.f, c = 0.f;
     LPCA_CUDA(cudaEventElapsedTime(&a, ctx.ev[6], ctx.ev[7]));
@@ -1285,25 +1296,28 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       Panel yo;
       yo.plain = ydev;
       yo.ld = ldy;
-      if (xmax_dev && tc_pair_mode() && f16_enabled()) {
-        XScale xs;  // the same rows the fit scanned: the fitted max is exact
-        xs.use = true;
-        xs.dev = const_cast<uint32_t*>(xmax_dev);
-        xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
-      } else if (map.xmax > 0.0f && tc_pair_mode() && f16_enabled()) {
-        // fp16 encoding scaled by the fitted data's max|X|; if the rows read
-        // here exceed it (fp16 overflow) or sit far below it (lost bits), the
-        // pass is redone in tf32
+      if (tc_pair_mode() && f16_enabled()) {
+        // fp16 encoding with a power-of-two scale per (row, 512-deep run) taken
+        // from the run's first stage (16x headroom): every row of Y keeps its
+        // own relative precision whatever the rows' dynamic range. A later
+        // stage outside the scale's range sets the flag; transform_finish then
+        // redoes the pass with every run scanned first.
         XScale xs;
         xs.use = true;
-        xs.host = map.xmax;
-        xs.check = ctx.get<uint32_t>("xmax.chk", 1);
-        launch_zero(ctx.stream, xs.check, sizeof(uint32_t));
+        xs.ovf = ctx.get<int>("t.ovf", 1);
+        launch_zero(ctx.stream, xs.ovf, sizeof(int));
         xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
-        float seen = 0.0f;
-        LPCA_CUDA(cudaMemcpyAsync(&seen, xs.check, sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
-        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
-        if (!(seen <= map.xmax && seen >= map.xmax * 0x1p-8f)) xw_pass(ctx, x, map.v, k, map.n, yo, false);
+        ctx.tr_flag = ctx.stage_read(xs.ovf, 1);
+        const double* v = map.v;
+        const index_t kk = k, nn = map.n;
+        const bool to_host = y_location == LPCA_HOST;
+        const std::size_t yb = ybytes;
+        ctx.tr_redo = [&ctx, x, v, kk, nn, yo, to_host, y, ydev, yb]() {
+          XScale scan;
+          scan.use = true;
+          xw_pass(ctx, x, v, kk, nn, yo, false, &scan);
+          if (to_host) LPCA_CUDA(cudaMemcpyAsync(y, ydev, yb, cudaMemcpyDeviceToHost, ctx.stream));
+        };
       } else {
         xw_pass(ctx, x, map.v, k, map.n, yo, false);
       }

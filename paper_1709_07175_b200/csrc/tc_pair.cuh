@@ -753,9 +753,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool first = r == 0, last = r == runs - 1;
         // this run's A-row unscale (XW: X row; XTU: X column `row`): power of two
         const float rowf = kHalf ? (a.scan ? rsc[(rc % kRscRing) * kBM + q * 32 + lane] : xinv) : 1.0f;
-        if (!last || to_planes16) {
-          // fold the run into L: 32 columns per TMEM round trip (both loads
-          // issued before one wait; the fold is latency-bound otherwise)
+        {
+          // fold the run into L (the last run too: the run buffer is released
+          // before the item's output is written from L, so the MMAs of the next
+          // item overlap it): 32 columns per TMEM round trip (both loads issued
+          // before one wait; the fold is latency-bound otherwise)
           int c0 = 0;
           for (; c0 + 32 <= a.npad; c0 += 32) {
             uint32_t rv[32], rs[32];
@@ -797,21 +799,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
-          continue;
         }
+      }
+      if (!to_planes16) {
+        // the item's output from L: X W rows (row-major fp32, 16 B stores when
+        // aligned) or tf32 hi/lo planes of its transpose; X^T U: fp64 partials
+        tc_fence_after();
         for (int c0 = 0; c0 < a.npad; c0 += 16) {
           float v[16];
-          tmem_ld16(racc + c0, v);
-          if (kHalf) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] *= kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
-          }
-          if (!first) {
-            float s[16];
-            tmem_ld16(lacc + c0, s);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = __fadd_rn(v[e], s[e]);
-          }
+          tmem_ld16(lacc + c0, v);
           if (kMode == kXW) {
             if (kHalf) {
 #pragma unroll
@@ -827,10 +823,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
               }
               if (a.out) {
-                float* po = a.out + static_cast<size_t>(row) * a.ldo;
+                float* po = a.out + static_cast<size_t>(row) * a.ldo + c0;
+                if (c0 + 16 <= a.wstore && (a.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) {
 #pragma unroll
-                for (int e = 0; e < 16; ++e)
-                  if (c0 + e < a.wstore) po[c0 + e] = v[e];
+                  for (int e = 0; e < 16; e += 4)
+                    *reinterpret_cast<float4*>(po + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 16; ++e)
+                    if (c0 + e < a.wstore) po[e] = v[e];
+                }
               }
             }
           } else if (row < a.n) {
@@ -842,10 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
-      }
-      if (to_planes16) {
+      } else {
         // OUT^T as fp16 hi/lo planes scaled per (column, 256-row block = this
         // pair's item): pass 1 reduces each warp's column maxima of the raw
         // accumulator; pass 1.5 combines the four warps, swaps the CTA's

@@ -28,7 +28,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu", "eigh.cu", "sparse.cu", "metrics.cu",
            "spectral.cu"]
-HOST_SOURCES = ["mapio.cpp", "matrixio.cpp"]  # host-only C++ (g++)
+HOST_SOURCES = ["textio.cpp"]  # host-only C++ (g++)
 CXX = os.environ.get("CXX", "g++")
 
 

@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 SOURCES = ["lpca.cu", "omega.cu", "gemm_simt.cu", "gemm_tc.cu", "small.cu", "eigh.cu", "sparse.cu", "metrics.cu",
-           "spectral.cu"]
+           "spectral.cu", "sparse_omega.cu"]
 HOST_SOURCES = ["textio.cpp"]  # host-only C++ (g++)
 CXX = os.environ.get("CXX", "g++")
 

@@ -224,6 +224,18 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 // lazy_projector.cpp:12-37).
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
                          int* status, double tol_rel = 1e-14);
+// Very sparse Omega sketch (csrc/sparse_omega.cu): per-(K chunk, column) lists
+// of Omega's nonzeros, then U = X Omega by gathers (U row-major, ld ldu <= 512,
+// padding columns zeroed; max|X| into xmax when given), and U^T fp16 planes
+// with per-(column, 256-row block) scales from a plain fp32 U.
+index_t sparse_sketch_chunks(index_t n, int dtype);
+void launch_omega_chunk_lists(cudaStream_t s, const double* omega, index_t n, index_t l, int dtype, int* counts,
+                              int* ptr, std::uint32_t* ent);
+template <typename T>
+void launch_sparse_sketch(cudaStream_t s, const T* x, index_t m, index_t n, index_t ldx, const int* ptr,
+                          const std::uint32_t* ent, index_t l, T* u, index_t ldu, std::uint32_t* xmax, int num_sms);
+void launch_u_planes_f16(cudaStream_t s, const float* u, index_t m, index_t ld, index_t npad, __half* hi, __half* lo,
+                         index_t ldt, float* uinv);
 // C = op(A) op(B) + beta C, l x l column-major (op = transpose when ta / tb; b null = identity).
 void launch_small_gemm(cudaStream_t s, int ta, int tb, index_t l, const double* a, const double* b, double* c,
                        double beta);

@@ -508,6 +508,15 @@ struct XScale {
   int* ovf = nullptr;         // scanless per-run scales: flags runs that need the scan
 };
 
+// LPCA_SPARSE_OMEGA=0 sends a very sparse Omega through the dense passes (A/B)
+bool sparse_omega_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LPCA_SPARSE_OMEGA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool f16_enabled() {
   static const bool on = [] {
     const char* e = getenv("LPCA_TC_F16");
@@ -1069,17 +1078,48 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     XScale sketch;
     sketch.use = true;
     sketch.check = xs.dev;
+    // very sparse Omega on dense X: the sketch is a gather (csrc/sparse_omega.cu,
+    // one HBM-bound read of X) instead of a dense tensor-core pass
+    const bool gather = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && sparse_omega_enabled() &&
+                        u.ld <= 512;
     int* xovf = nullptr;
-    if (f16 && !ctx.force_scan) {  // scales from each run's first stage (rerun with the scan if flagged)
+    if (f16 && !ctx.force_scan && !gather) {  // scales from each run's first stage (rerun with the scan if flagged)
       xovf = ctx.get<int>("xovf", 1);
       launch_zero(ctx.stream, xovf, sizeof(int));
       sketch.ovf = xovf;
     }
     ev.mark(12);
     ev.mark(13);
-    ctx.pass_slot = 12;
-    xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
-    ctx.pass_slot = -1;
+    if (gather) {
+      const index_t nch = sparse_sketch_chunks(n, x.dtype);
+      int* counts = ctx.get<int>("so.counts", nch * l);
+      int* ptr = ctx.get<int>("so.ptr", nch * l + 1);
+      auto* ent = ctx.get<std::uint32_t>("so.ent", n * l);
+      launch_omega_chunk_lists(ctx.stream, omega, n, l, x.dtype, counts, ptr, ent);
+      ctx.note_launch(3);
+      ev.mark(12);
+      if (x.dtype == 8) {
+        launch_sparse_sketch<double>(ctx.stream, static_cast<const double*>(x.p), m, n, x.ld, ptr, ent, l,
+                                     static_cast<double*>(u.plain), u.ld, nullptr, ctx.num_sms);
+      } else {
+        float* up = u.plain ? static_cast<float*>(u.plain) : ctx.get<float>("u.gather", mm * u.ld);
+        launch_sparse_sketch<float>(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld, ptr, ent, l, up, u.ld,
+                                    f16 ? xs.dev : nullptr, ctx.num_sms);
+        if (f16) {
+          launch_u_planes_f16(ctx.stream, up, m, u.ld, u.ld, u.h16hi, u.h16lo, u.ldt16, u.uinv);
+          ctx.note_launch();
+        } else if (u.hi && m > 0) {
+          launch_split_tf32_transpose(ctx.stream, up, m, l, u.ld, u.hi, u.lo, u.ldt);
+          ctx.note_launch();
+        }
+      }
+      LPCA_LAUNCHED(ctx);
+      ev.mark(13);
+    } else {
+      ctx.pass_slot = 12;
+      xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
+      ctx.pass_slot = -1;
+    }
     double* xovf_all = nullptr;  // the flag summed over ranks: every rank reruns, or none
     if (ctx.world > 1 && !ctx.force_scan) {  // issued by every rank, with or without an fp16 sketch
       xovf_all = ctx.get<double>("xovf.all", 1);

@@ -143,6 +143,11 @@ lpca_status lpca_ctx_set_gemm_path(lpca_ctx* ctx, int32_t path);
 lpca_status lpca_ctx_set_exact_order(lpca_ctx* ctx, int32_t exact);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t lpca_ctx_launch_count(const lpca_ctx* ctx);
+/* Debugging aid, with LPCA_WS_GUARD=1 in the environment: every workspace the
+ * context allocates is followed by a 1 MB pattern band; this synchronises and
+ * returns how many bands were overwritten (names, space-separated, into
+ * `names`), or -1 when guards are off, -2 on a CUDA error. */
+int64_t lpca_debug_check_guards(lpca_ctx* ctx, char* names, int64_t capacity);
 
 /* ---- configuration ------------------------------------------------------ */
 /* ReducerConfig::resolved (proj/core/src/reducer.cpp:137-161). */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "lpca_nccl_unique_id": (I32, [P]),
     "lpca_ctx_create_dist": (I32, [I32, I32, I32, P, PP]),
     "lpca_ctx_create_hooked": (I32, [I32, I32, I32, P, P, PP]),
+    "lpca_debug_check_guards": (I64, [P, P, I64]),
     "lpca_ctx_destroy": (I32, [P]),
     "lpca_ctx_set_stream": (I32, [P, P]),
     "lpca_ctx_synchronize": (I32, [P]),

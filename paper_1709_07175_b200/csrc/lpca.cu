@@ -171,11 +171,26 @@ struct lpca_ctx {
       ws.erase(it);
     }
     void* p = nullptr;
-    LPCA_CUDA(cudaMalloc(&p, bytes < 256 ? 256 : bytes));
+    const std::size_t guard = guards() ? kGuardBytes : 0;
+    LPCA_CUDA(cudaMalloc(&p, (bytes < 256 ? 256 : bytes) + guard));
     if (std::getenv("LPCA_WS_POISON"))  // debugging aid: NaN-fill new workspaces
       LPCA_CUDA(cudaMemsetAsync(p, 0xff, bytes < 256 ? 256 : bytes, stream));
+    if (guard)  // debugging aid (lpca_debug_check_guards): a pattern band right after the workspace
+      LPCA_CUDA(cudaMemsetAsync(static_cast<char*>(p) + bytes, kGuardByte, guard, stream));
     ws[name] = {p, bytes};
     return p;
+  }
+  // LPCA_WS_GUARD=1: every workspace is followed by a guard band whose pattern
+  // lpca_debug_check_guards verifies (out-of-bounds writes of any kernel into
+  // the library's own buffers; compute-sanitizer is unavailable on the pool).
+  static constexpr std::size_t kGuardBytes = 1 << 20;
+  static constexpr int kGuardByte = 0xA5;
+  static bool guards() {
+    static const bool on = [] {
+      const char* e = std::getenv("LPCA_WS_GUARD");
+      return e && e[0] == '1';
+    }();
+    return on;
   }
   template <typename T>
   T* get(const std::string& name, std::size_t count) {
@@ -1840,6 +1855,32 @@ lpca_status lpca_ctx_set_stream(lpca_ctx* ctx, void* cuda_stream) {
     check_ctx(ctx);
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
   });
+}
+
+int64_t lpca_debug_check_guards(lpca_ctx* ctx, char* names, int64_t capacity) {
+  if (!ctx || !lpca_ctx::guards()) return -1;
+  cudaSetDevice(ctx->device);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -2;
+  std::vector<unsigned char> band(lpca_ctx::kGuardBytes);
+  std::string bad;
+  int64_t count = 0;
+  for (const auto& kv : ctx->ws) {
+    if (cudaMemcpy(band.data(), static_cast<const char*>(kv.second.first) + kv.second.second, band.size(),
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -2;
+    for (unsigned char b : band)
+      if (b != lpca_ctx::kGuardByte) {
+        ++count;
+        bad += kv.first + " ";
+        break;
+      }
+  }
+  if (names && capacity > 0) {
+    const std::size_t n = std::min<std::size_t>(bad.size(), static_cast<std::size_t>(capacity - 1));
+    std::memcpy(names, bad.data(), n);
+    names[n] = '\0';
+  }
+  return count;
 }
 
 lpca_status lpca_ctx_synchronize(lpca_ctx* ctx) {

@@ -756,53 +756,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         {
           // fold the run into L (the last run too: the run buffer is released
           // before the item's output is written from L, so the MMAs of the next
-          // item overlap it), 16 columns at a time, software-pipelined: chunk
-          // c + 1's TMEM loads are in flight while chunk c is scaled, added and
-          // stored, and the run buffer is released as soon as its last chunk
-          // has landed in registers (the stores go to L's own columns)
-          const int nch = a.npad / 16;
-          uint32_t ra[16], la[16], rb[16], lb[16];
-          auto ldc = [&](int ch, uint32_t(&r)[16], uint32_t(&l)[16]) {
-            tmem_ld16_nowait(racc + 16 * ch, r);
-            if (!first) tmem_ld16_nowait(lacc + 16 * ch, l);
-          };
-          auto release = [&] {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
-          };
-          auto proc = [&](int ch, const uint32_t(&r)[16], const uint32_t(&l)[16]) {
-            const int c0 = 16 * ch;
+          // item overlap it): 32 columns per TMEM round trip (both loads issued
+          // before one wait; the fold is latency-bound otherwise)
+          int c0 = 0;
+          for (; c0 + 32 <= a.npad; c0 += 32) {
+            uint32_t rv[32], rs[32];
+            tmem_ld32_nowait(racc + c0, rv);
+            if (!first) tmem_ld32_nowait(lacc + c0, rs);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              v[e] = __uint_as_float(rv[e]);
+              if (kHalf) {  // power-of-two unscale: the FFMA rounds exactly like mul + add
+                const float f = kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
+                v[e] = first ? v[e] * f : __fmaf_rn(v[e], f, __uint_as_float(rs[e]));
+              } else if (!first) {
+                v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
+              }
+            }
+            tmem_st32(lacc + c0, v);
+          }
+          if (c0 < a.npad) {
+            uint32_t rv[16], rs[16];
+            tmem_ld16_nowait(racc + c0, rv);
+            if (!first) tmem_ld16_nowait(lacc + c0, rs);
+            tmem_ld_wait();
             float v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              v[e] = __uint_as_float(r[e]);
+              v[e] = __uint_as_float(rv[e]);
               if (kHalf) {  // power-of-two unscale: the FFMA rounds exactly like mul + add
                 const float f = kMode == kXTU ? rowf * runsc[c0 + e] : rowf;
-                v[e] = first ? v[e] * f : __fmaf_rn(v[e], f, __uint_as_float(l[e]));
+                v[e] = first ? v[e] * f : __fmaf_rn(v[e], f, __uint_as_float(rs[e]));
               } else if (!first) {
-                v[e] = __fadd_rn(v[e], __uint_as_float(l[e]));
+                v[e] = __fadd_rn(v[e], __uint_as_float(rs[e]));
               }
             }
             tmem_st16(lacc + c0, v);
-          };
-          auto step = [&](int ch, const uint32_t(&rc)[16], const uint32_t(&lc)[16], uint32_t(&rn)[16],
-                          uint32_t(&ln)[16]) {
-            if (ch + 1 < nch) ldc(ch + 1, rn, ln);
-            proc(ch, rc, lc);
-            if (ch + 1 < nch) {
-              tmem_ld_wait();
-              if (ch + 2 == nch) release();
-            }
-          };
-          ldc(0, ra, la);
-          tmem_ld_wait();
-          if (nch == 1) release();
-          for (int ch = 0; ch < nch; ch += 2) {
-            step(ch, ra, la, rb, lb);
-            if (ch + 1 < nch) step(ch + 1, rb, lb, ra, la);
           }
           tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[b]), 0));
         }
       }
       if (!to_planes16) {

@@ -415,7 +415,14 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   // three (LPCA_TC_SLOTDIV = 1 / 2 / 4 forces full / half / quarter slots)
   const int div = env_int("LPCA_TC_SLOTDIV", a.aslots == 1 ? 4 : 1);
   a.half_slots = kHalf && (div == 2 || div == 4) ? div : 0;
-  if (a.half_slots) a.aslots *= a.half_slots;
+  if (a.half_slots == 4) {  // quarter slots fill every free TMEM column (up to 8 of them)
+    const int acc = (a.nrb + 1) * a.npad;
+    const int q = (512 - acc) / 16;
+    a.aslots = q > 8 ? 8 : q;
+    a.tmem_cols = tmem_cols_for(static_cast<uint32_t>(acc + 16 * a.aslots));
+  } else if (a.half_slots) {
+    a.aslots *= a.half_slots;
+  }
   const uint32_t bk = kHalf ? 64 : 32;
   const uint32_t stage_bytes = kBM * bk * 4 + static_cast<uint32_t>(a.npad) * 128;  // X + half B (hi, lo)
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);

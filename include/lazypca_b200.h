@@ -11,8 +11,9 @@
  *    are passed as void*; NCCL unique ids as 128 opaque bytes).
  *  - Matrices are described by lpca_matrix_view. Dense data may be row- or
  *    column-major, fp32 or fp64, and live on the host or on the context's device.
- *    CSC views (the reference's SparseMatrix) are densified on upload in this
- *    release ("out of scope").
+ *    CSC views (the reference's SparseMatrix) below 25% density stay sparse on
+ *    the device (CSR and CSC gathers in the reference's summation order);
+ *    denser ones are densified for the tensor-core passes.
  *  - Every call returns an lpca_status. Non-zero codes mirror the reference's
  *    exception hierarchy (proj/core/include/lazypca/error.hpp:10-58); the message
  *    and payload (index / last_gap / line) are available per thread through

@@ -7,7 +7,8 @@
 // FMA contraction), matching the reference compiled with -ffp-contract=off.
 // The two tail branches (p < 0.02425 or p > 0.97575, ~4.85% of draws) call
 // log(); CUDA's log is within 1 ulp of glibc's, so tail entries may differ by
-// an ulp or two — tests/test_omega_gpu.py measures and bounds that.
+// an ulp or two — tests/test_gpu_parity.py::test_omega_matches_reference_bits
+// measures and bounds that.
 #pragma once
 #include <cstdint>
 

@@ -2,13 +2,17 @@
 //   a*b ~= a_hi*b_hi + a_lo*b_hi + a_hi*b_lo
 // in one of two operand encodings:
 //   kHalf = false : tf32 hi/lo (kind::tf32, K = 32 per stage). Needs no scale;
-//                   the first pass over X (the sketch) runs this way.
+//                   the kernel-level exports (lpca_sketch_f32 / lpca_gemm_t_f32)
+//                   and SPCA's Q^T X run this way.
 //   kHalf = true  : fp16 hi/lo of power-of-two scaled operands (kind::f16,
 //                   K = 64 per stage, twice the tf32 MMA rate, half the TMEM
-//                   A traffic per K). X is scaled by s_x = 2^(14 - floor(log2
-//                   max|X|)) (max|X| recorded by the sketch's converters), the
-//                   small operand per column (W planes) or per column and
-//                   128-row block (U^T planes, written by the sketch epilogue).
+//                   A traffic per K): every pass of Lazy SPCA. X rows are
+//                   scaled per (row, 512-deep run) from the run's first stage
+//                   (sketch, transform; a flagged run redoes the pass with each
+//                   run scanned first) or by one s_x = 2^(14 - floor(log2
+//                   max|X|)) from the max the sketch recorded (power step, F);
+//                   the small operand per column (W planes) or per column and
+//                   256-row block (U^T planes, written by the X W epilogue).
 //                   hi = fp16_rn(a s), lo = fp16_rn(a s - hi): with every
 //                   scaled value in [2^-14, 2^15] the split keeps 22 bits
 //                   (tf32 hi/lo keeps 20); values more than 2^18 below their

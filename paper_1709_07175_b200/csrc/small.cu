@@ -570,22 +570,83 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
   sign_canon_kernel<<<static_cast<unsigned>(k), 256, 0, s>>>(v, n, ut, l);
 }
 
+namespace {
+// The whole Cholesky factorisation in one CTA when the lower triangle fits
+// shared memory (l <= ~236): packed rows, right-looking, two barriers per
+// column, instead of a one-CTA panel kernel plus a trailing SYRK per 32 columns
+// (latency-bound at l ~ 220: 21 launches, ~1.4 ms for a power step's three
+// factorisations). Same pivot rule and status as the panel path; L goes to lm
+// (column-major, zeros above) for chol_inv_kernel.
+__global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restrict__ g, index_t l, double tol_rel,
+                                                          double* __restrict__ lm, int* status) {
+  extern __shared__ double tri[];  // row r at r (r + 1) / 2
+  __shared__ double red[32];
+  __shared__ double inv;
+  __shared__ int fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto at = [&](index_t r, index_t c) -> double& { return tri[r * (r + 1) / 2 + c]; };
+  double maxd = 0.0;
+  for (index_t j = tid; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
+  block_max_reduce(maxd, red);
+  const double tol = tol_rel * maxd;
+  for (index_t r = warp; r < l; r += nw)
+    for (index_t c = lane; c <= r; c += 32) at(r, c) = g[c * l + r];
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (index_t j = 0; j < l; ++j) {
+    if (tid == 0) {
+      const double d = at(j, j);
+      if (!(d > tol)) {  // (NaN fails too)
+        fail = static_cast<int>(j) + 1;
+      } else {
+        const double sq = sqrt(d);
+        at(j, j) = sq;
+        inv = 1.0 / sq;
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    for (index_t r = j + 1 + tid; r < l; r += blockDim.x) at(r, j) *= inv;
+    __syncthreads();
+    // trailing update, rows spread over warps, columns over lanes
+    for (index_t r = j + 1 + warp; r < l; r += nw) {
+      const double lrj = at(r, j);
+      for (index_t c = j + 1 + lane; c <= r; c += 32) at(r, c) -= lrj * at(c, j);
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) status[0] = fail;
+    return;
+  }
+  for (index_t c = warp; c < l; c += nw)
+    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r >= c ? at(r, c) : 0.0;
+}
+}  // namespace
+
 void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rinv, double* work,
                          int* status, double tol_rel) {
   if (l <= 0) return;
   LPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
-  chol_copy_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(g, l, work);
-  std::size_t psm = static_cast<std::size_t>(l) * kCholNb * sizeof(double);
-  const int in_smem = psm <= 200 * 1024 ? 1 : 0;
-  if (!in_smem) psm = 0;
-  LPCA_CUDA(cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(psm > 48 * 1024 ? psm : 48 * 1024)));
-  for (index_t p0 = 0; p0 < l; p0 += kCholNb) {
-    chol_panel_kernel<<<1, 256, psm, s>>>(g, l, p0, work, status, in_smem, tol_rel);
-    const index_t t = l - p0 - kCholNb;
-    if (t > 0) {
-      const unsigned tiles = static_cast<unsigned>(ceil_div(t, 32));
-      chol_syrk_kernel<<<dim3(tiles, tiles), 256, 0, s>>>(l, p0, work, status);
+  const std::size_t tri_bytes = static_cast<std::size_t>(l) * (l + 1) / 2 * sizeof(double);
+  if (tri_bytes <= 220 * 1024) {
+    LPCA_CUDA(cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(tri_bytes < 48 * 1024 ? 48 * 1024 : tri_bytes)));
+    chol_small_kernel<<<1, 1024, tri_bytes, s>>>(g, l, tol_rel, work, status);
+  } else {
+    chol_copy_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(g, l, work);
+    std::size_t psm = static_cast<std::size_t>(l) * kCholNb * sizeof(double);
+    const int in_smem = psm <= 200 * 1024 ? 1 : 0;
+    if (!in_smem) psm = 0;
+    LPCA_CUDA(cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(psm > 48 * 1024 ? psm : 48 * 1024)));
+    for (index_t p0 = 0; p0 < l; p0 += kCholNb) {
+      chol_panel_kernel<<<1, 256, psm, s>>>(g, l, p0, work, status, in_smem, tol_rel);
+      const index_t t = l - p0 - kCholNb;
+      if (t > 0) {
+        const unsigned tiles = static_cast<unsigned>(ceil_div(t, 32));
+        chol_syrk_kernel<<<dim3(tiles, tiles), 256, 0, s>>>(l, p0, work, status);
+      }
     }
   }
   int wpb = 8;  // warps per block: dinv + one right-hand side per warp in shared memory

@@ -36,9 +36,9 @@ def test_c4_shape_very_sparse_omega_power2(ctx):
     lp.apply_map(m64, x64, out=y64, ctx=ref_ctx)
     s32, s64 = m32.singular_values, m64.singular_values
     assert np.max(np.abs(s32 - s64) / s64) < 1e-4
-    assert np.max(O.principal_angles(m32.v[:, :k // 2], m64.v[:, :k // 2])) < 1e-3
+    assert np.max(O.principal_angles(m32.v[:, :k // 2], m64.v[:, :k // 2])) < 2e-5  # measured ~4e-7
     dy = y32.double() - y64
-    assert (dy.norm() / y64.norm()).item() < 1e-3
+    assert (dy.norm() / y64.norm()).item() < 5e-5  # measured ~2e-6
     del m64
     ref_ctx.close()
 

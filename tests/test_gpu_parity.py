@@ -214,10 +214,11 @@ def test_fp32_lazy_c2_shape_vs_reference(ctx, ref):
     print("fp32 sigma rel max", rel.max(), "normwise", np.abs(m.singular_values - rs).max() / rs[0])
     assert rel.max() < 1e-4
     ang = O.principal_angles(m.v[:, :50], rv[:, :50])
-    assert ang.max() < 1e-2
+    print("top-50 angle", ang.max())
+    assert ang.max() < 2e-5  # about 10x the measured
     y = torch.empty((20000, 100), dtype=torch.float32, device="cuda")
     lp.apply_map(m, x, out=y)
-    _dist_check(xh, y.cpu().numpy().astype(np.float64), ref.apply_map(xh, rv), tol=1e-3)
+    _dist_check(xh, y.cpu().numpy().astype(np.float64), ref.apply_map(xh, rv), tol=5e-5)
 
 
 def test_power_iteration_c3_shape_vs_oracle(ctx):

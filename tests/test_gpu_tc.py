@@ -40,10 +40,12 @@ def test_tc_matches_reference(ctx, ref, m, n, r, k, l):
     got = _fit(ctx, x, k, l, "tcgen05")
     rv, rs, _, _ = ref.reduce(2, xh, k, l, 7)
     rel = np.abs(got.singular_values - rs) / rs
-    print(f"m={m} n={n} l={l}: sigma rel max {rel.max():.3e}")
-    assert rel.max() < 1e-4
     kk = max(1, k // 2)
-    assert np.max(O.principal_angles(got.v[:, :kk], rv[:, :kk])) < 1e-3
+    ang = np.max(O.principal_angles(got.v[:, :kk], rv[:, :kk]))
+    print(f"m={m} n={n} l={l}: sigma rel max {rel.max():.3e}, top-k/2 angle {ang:.2e}")
+    assert rel.max() < 1e-4   # north_star's fp32 bar
+    assert rel.max() < 5e-5   # measured 1.9e-6 .. 5.3e-6
+    assert ang < 1e-4
 
 
 def test_tc_and_simt_paths_agree(ctx):
@@ -52,7 +54,7 @@ def test_tc_and_simt_paths_agree(ctx):
     b = _fit(ctx, x, 32, 48, "simt")
     rel = np.abs(a.singular_values - b.singular_values) / b.singular_values
     assert rel.max() < 2e-5, rel.max()
-    assert O.chordal_distance(a.v[:, :16], b.v[:, :16]) < 1e-3
+    assert O.chordal_distance(a.v[:, :16], b.v[:, :16]) < 1e-4
 
 
 def test_tc_transform_matches_fp64(ctx):

@@ -572,46 +572,51 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 
 namespace {
 // The whole Cholesky factorisation in one CTA when the lower triangle fits
-// shared memory (l <= ~236): packed rows, right-looking, two barriers per
-// column, instead of a one-CTA panel kernel plus a trailing SYRK per 32 columns
+// shared memory (l <= ~236): packed columns, right-looking, a warp per trailing
+// column with lanes running down it (contiguous, conflict-free), three barriers
+// per column, instead of a one-CTA panel kernel plus a trailing SYRK per 32 columns
 // (latency-bound at l ~ 220: 21 launches, ~1.4 ms for a power step's three
 // factorisations). Same pivot rule and status as the panel path; L goes to lm
 // (column-major, zeros above) for chol_inv_kernel.
 __global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restrict__ g, index_t l, double tol_rel,
                                                           double* __restrict__ lm, int* status) {
-  extern __shared__ double tri[];  // row r at r (r + 1) / 2
+  extern __shared__ double tri[];  // packed lower triangle, column-major: column c at coff(c)
   __shared__ double red[32];
   __shared__ double inv;
   __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  auto at = [&](index_t r, index_t c) -> double& { return tri[r * (r + 1) / 2 + c]; };
+  auto coff = [&](index_t c) { return c * l - c * (c - 1) / 2; };  // element (r, c), r >= c: coff(c) + r - c
   double maxd = 0.0;
   for (index_t j = tid; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
   block_max_reduce(maxd, red);
   const double tol = tol_rel * maxd;
-  for (index_t r = warp; r < l; r += nw)
-    for (index_t c = lane; c <= r; c += 32) at(r, c) = g[c * l + r];
+  for (index_t c = warp; c < l; c += nw) {
+    double* col = tri + coff(c) - c;
+    for (index_t r = c + lane; r < l; r += 32) col[r] = g[c * l + r];
+  }
   if (tid == 0) fail = 0;
   __syncthreads();
   for (index_t j = 0; j < l; ++j) {
+    double* cj = tri + coff(j) - j;  // cj[r] = A(r, j)
     if (tid == 0) {
-      const double d = at(j, j);
+      const double d = cj[j];
       if (!(d > tol)) {  // (NaN fails too)
         fail = static_cast<int>(j) + 1;
       } else {
         const double sq = sqrt(d);
-        at(j, j) = sq;
+        cj[j] = sq;
         inv = 1.0 / sq;
       }
     }
     __syncthreads();
     if (fail) break;
-    for (index_t r = j + 1 + tid; r < l; r += blockDim.x) at(r, j) *= inv;
+    for (index_t r = j + 1 + tid; r < l; r += blockDim.x) cj[r] *= inv;
     __syncthreads();
-    // trailing update, rows spread over warps, columns over lanes
-    for (index_t r = j + 1 + warp; r < l; r += nw) {
-      const double lrj = at(r, j);
-      for (index_t c = j + 1 + lane; c <= r; c += 32) at(r, c) -= lrj * at(c, j);
+    // trailing update, a warp per column c, lanes down the column: A(r, c) -= L(r, j) L(c, j)
+    for (index_t c = j + 1 + warp; c < l; c += nw) {
+      double* cc = tri + coff(c) - c;
+      const double ljc = cj[c];
+      for (index_t r = c + lane; r < l; r += 32) cc[r] = fma(-cj[r], ljc, cc[r]);
     }
     __syncthreads();
   }
@@ -619,8 +624,10 @@ __global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restri
     if (tid == 0) status[0] = fail;
     return;
   }
-  for (index_t c = warp; c < l; c += nw)
-    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r >= c ? at(r, c) : 0.0;
+  for (index_t c = warp; c < l; c += nw) {
+    const double* col = tri + coff(c) - c;
+    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r >= c ? col[r] : 0.0;
+  }
 }
 }  // namespace
 

@@ -430,13 +430,23 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   if (kHalf && kMode == kXW && a.scan == 1 && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
   if (kHalf && kMode == kXTU && a.scan && a.run_stages > a.stages)
     throw Error(kInternal, "tc pair: a scanned U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
-  const size_t smem =
-      static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + 7 * 4 * a.npad + kRscRing * 4 * kBM;  // + xbuf
-  LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + (kMaxEpiWarps + 3) * 4 * a.npad +
+                      kRscRing * 4 * kBM;  // red, gsc, xbuf
+  LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
+  if constexpr (kMode == kXW) {
+    if (a.npad > 168) {
+      LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      if (ev_pre) LPCA_CUDA(cudaEventRecord(ev_pre, s));
+      tc2_kernel<kMode, kHalf, 8><<<2 * pairs, pair_threads(8), smem, s>>>(tx, th, tl, a);
+      if (ev_post) LPCA_CUDA(cudaEventRecord(ev_post, s));
+      return;
+    }
+  }
   if (ev_pre) LPCA_CUDA(cudaEventRecord(ev_pre, s));
-  tc2_kernel<kMode, kHalf><<<2 * pairs, kThreads, smem, s>>>(tx, th, tl, a);
+  tc2_kernel<kMode, kHalf, 4><<<2 * pairs, pair_threads(4), smem, s>>>(tx, th, tl, a);
   if (ev_post) LPCA_CUDA(cudaEventRecord(ev_post, s));
 }
 

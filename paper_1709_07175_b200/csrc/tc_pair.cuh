@@ -295,7 +295,20 @@ __device__ __forceinline__ void pair_item_coords(const PairArgs& a, int item, in
   }
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// Epilogue warps (kEpi). Wide X W slices (one TMEM run buffer): two per TMEM
+// lane quadrant, each folding and writing half of the accumulator's columns (the
+// fold releases the run buffer twice as soon: the MMA's wait for it fell from
+// 15% to 6% at configs[2]). Otherwise one per quadrant: X^T U's converters need
+// the registers (at 448 threads ptxas caps them at 128 and the column-wise
+// transposing loads spill), and narrow slices have two run buffers anyway.
+constexpr int pair_threads(int epi) {
+  return 32 * (6 + epi);  // TMA, MMA, 4 converters, the epilogue
+}
+constexpr int kMaxEpiWarps = 8;
+template <int kEpi>
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpi) : "memory");
+}
 
 #ifdef LPCA_PAIR_PROF  // role timers (tools/pair_prof.py): cycles summed over CTAs
 __device__ unsigned long long g_pair_prof[2][16];  // [mode][counter]
@@ -307,11 +320,12 @@ __device__ unsigned long long g_pair_prof[2][16];  // [mode][counter]
 #define PP_ADD(k)
 #endif
 
-template <int kMode, bool kHalf>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int kMode, bool kHalf, int kEpi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
                const __grid_constant__ CUtensorMap tmbl, PairArgs a) {
   constexpr int BK = kHalf ? 64 : 32;  // K per stage (one 128 B swizzle row of B)
+  constexpr int kEpiWarps = kEpi;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the shared array (an integer round
   // trip would lose the address space and turn every access generic)
@@ -332,8 +346,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* xch = tempty + 2;  // [2] U^T block-maximum exchange with the peer (XW fp16 planes)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch + 2);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4][npad] epilogue block maxima / run scales
-  float* rsc = red + 5 * a.npad;  // after red [4][npad] + gsc [npad]: [kRscRing runs][128] inverse A-row scales
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [kEpiWarps][npad] epilogue block maxima / run scales
+  float* rsc = red + (kMaxEpiWarps + 1) * a.npad;  // after red + gsc [npad]: [kRscRing runs][128] inverse A-row scales
   float* xbuf = rsc + kRscRing * kBM;  // [2][npad] the peer's column maxima (written by the peer)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -353,7 +367,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);
+      mbar_init(&tempty[b], 2 * kEpiWarps);
       mbar_init(&xch[b], 1);
     }
     fence_barrier_init();
@@ -711,7 +725,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (kHalf && a.scan == 2 && __any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(a.ovf, 1);
   } else {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
-    const int q = warp & 3;
+    const int q = warp & 3;                       // TMEM lane quadrant
+    const int ew = warp - 6;                      // epilogue warp 0 .. kEpiWarps - 1
+    const int nch16 = a.npad / 16;                // this warp's 16-column chunks: one half of them
+    const int half = ew / 4;
+    const int c_lo = kEpiWarps == 4 ? 0 : (half ? (nch16 + 1) / 2 : 0) * 16;
+    const int c_hi = kEpiWarps == 4 ? a.npad : (half ? nch16 : (nch16 + 1) / 2) * 16;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t lacc = lane_base + static_cast<uint32_t>(a.nrb * a.npad);
     const float xinv = 1.0f / xs;
@@ -726,7 +745,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // X^T U, fp16: each run's rows form one 256-row block of U^T scales. The
       // next run's scales are fetched into registers while this run is folded
       // and staged in this warp's row of red[] (broadcast reads).
-      float* runsc = red + q * a.npad;
+      float* runsc = red + ew * a.npad;
       float nxt[8];
       auto fetch_scales = [&](int r) {
         const float* src = a.uinv_in + static_cast<size_t>((k0 + r * run_k) / kUScaleRows) * a.uinv_ld;
@@ -762,8 +781,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // before the item's output is written from L, so the MMAs of the next
           // item overlap it): 32 columns per TMEM round trip (both loads issued
           // before one wait; the fold is latency-bound otherwise)
-          int c0 = 0;
-          for (; c0 + 32 <= a.npad; c0 += 32) {
+          int c0 = c_lo;
+          for (; c0 + 32 <= c_hi; c0 += 32) {
             uint32_t rv[32], rs[32];
             tmem_ld32_nowait(racc + c0, rv);
             if (!first) tmem_ld32_nowait(lacc + c0, rs);
@@ -781,7 +800,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             tmem_st32(lacc + c0, v);
           }
-          if (c0 < a.npad) {
+          if (c0 < c_hi) {
             uint32_t rv[16], rs[16];
             tmem_ld16_nowait(racc + c0, rv);
             if (!first) tmem_ld16_nowait(lacc + c0, rs);
@@ -809,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // the item's output from L: X W rows (row-major fp32, 16 B stores when
         // aligned) or tf32 hi/lo planes of its transpose; X^T U: fp64 partials
         tc_fence_after();
-        for (int c0 = 0; c0 < a.npad; c0 += 16) {
+        for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
           float v[16];
           tmem_ld16(lacc + c0, v);
           if (kMode == kXW) {
@@ -858,8 +877,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // identical in both CTAs; pass 2 splits.
         tc_fence_after();
         const bool valid = row < a.m;
-        float* gsc = red + 4 * a.npad;
-        for (int c0 = 0; c0 < a.npad; c0 += 16) {
+        float* gsc = red + kMaxEpiWarps * a.npad;
+        for (int c0 = c_lo; c0 < c_hi; c0 += 16) {  // rows 0..3 of red: one per lane quadrant
           float v[16];
           tmem_ld16(lacc + c0, v);
 #pragma unroll
@@ -867,10 +886,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const float mx = warp_max16(v, lane);
           if ((lane & 1) == 0) red[q * a.npad + c0 + warp_max16_col(lane)] = mx;
         }
-        epi_bar();
+        epi_bar<kEpiWarps>();
         const int xb = xit & 1;
-        if (q == 0 && lane == 0) mbar_expect_tx(&xch[xb], static_cast<uint32_t>(a.npad) * 4);
-        for (int c = q * 32 + lane; c < a.npad; c += 128) {
+        if (ew == 0 && lane == 0) mbar_expect_tx(&xch[xb], static_cast<uint32_t>(a.npad) * 4);
+        for (int c = ew * 32 + lane; c < a.npad; c += 32 * kEpiWarps) {
           const float mloc = fmaxf(fmaxf(red[c], red[a.npad + c]), fmaxf(red[2 * a.npad + c], red[3 * a.npad + c]));
           gsc[c] = mloc;
           st_async_f32(map_to_rank(smem_u32(&xbuf[xb * a.npad + c]), rank ^ 1u), mloc,
@@ -881,15 +900,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int blk = t0 / kUScaleRows;
         // (a pair whose rows all lie past m owns no block: writing its scales
         // would run past the [ceil(m/256)][npad] array)
-        for (int c = q * 32 + lane; c < a.npad; c += 128) {
+        for (int c = ew * 32 + lane; c < a.npad; c += 32 * kEpiWarps) {
           const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
           const float mx = fmaxf(gsc[c], xbuf[xb * a.npad + c]) * f;
           const float sc = pow2_scale_for(mx);
           gsc[c] = f * sc;
           if (rank == 0 && blk * kUScaleRows < a.m) a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
         }
-        epi_bar();
-        for (int c0 = 0; c0 < a.npad; c0 += 16) {
+        epi_bar<kEpiWarps>();
+        for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
           float v[16];
           tmem_ld16(lacc + c0, v);
           if (valid) {
@@ -904,7 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        epi_bar();  // red[] reused by the next item
+        epi_bar<kEpiWarps>();  // red[] reused by the next item
       }
     }
   }

@@ -463,16 +463,52 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
   if (c == 0 && lane == 0) status[0] = 0;
 }
 
-// tmp(r, j) = sum_{s <= r} L^{-1}(r, s) F(s, j); then F <- tmp.
-__global__ void apply_linv_kernel(const double* __restrict__ w, index_t l,
-                                  const double* __restrict__ f, index_t n, double* __restrict__ out) {
-  const index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x;
-  if (e >= l * n) return;
-  const index_t j = e / l, r = e % l;
-  double acc = 0.0;
-  for (index_t s = 0; s <= r; ++s) acc = fma(w[r * l + s], f[j * l + s], acc);
-  out[e] = acc;
+// tmp(r, j) = sum_{s <= r} L^{-1}(r, s) F(s, j), tiled: a CTA computes 64 r x
+// 64 j outputs from 16-wide slabs of L^{-1} rows and F columns in shared memory,
+// 4 x 4 per thread; each output still sums s = 0, 1, ... in order with FMAs
+// (the zero entries above the diagonal add nothing), as the untiled kernel did.
+__global__ void __launch_bounds__(256) apply_linv_tiled_kernel(const double* __restrict__ w, index_t l,
+                                                                const double* __restrict__ f, index_t n,
+                                                                double* __restrict__ out) {
+  __shared__ double ws[16][65];  // [s][r]
+  __shared__ double fs[16][65];  // [s][j]
+  const index_t r0 = static_cast<index_t>(blockIdx.x) * 64, j0 = static_cast<index_t>(blockIdx.y) * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // r = r0 + ty + 16 a, j = j0 + tx + 16 b
+  double acc[4][4] = {};
+  const index_t s_end = r0 + 64 < l ? r0 + 64 : l;
+  for (index_t s0 = 0; s0 < s_end; s0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int k = e % 16, i = e / 16;
+      const index_t r = r0 + i, sv = s0 + k;
+      ws[k][i] = (r < l && sv <= r) ? w[r * l + sv] : 0.0;
+      const index_t j = j0 + i;
+      fs[k][i] = (j < n && sv < l) ? f[j * l + sv] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = ws[k][ty + 16 * q];
+        b[q] = fs[k][tx + 16 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], b[p], acc[q][p]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const index_t r = r0 + ty + 16 * q, j = j0 + tx + 16 * p;
+      if (r < l && j < n) out[j * l + r] = acc[q][p];
+    }
 }
+
 
 }  // namespace
 
@@ -698,7 +734,8 @@ void launch_add_trace_shift(cudaStream_t s, double* g, index_t l, double c) {
 void launch_apply_rinv_t(cudaStream_t s, const double* rinv, index_t l, double* f, index_t n,
                          double* tmp) {
   const index_t total = l * n;
-  apply_linv_kernel<<<static_cast<unsigned>(ceil_div(total, 128)), 128, 0, s>>>(rinv, l, f, n, tmp);
+  const dim3 grid(static_cast<unsigned>(ceil_div(l, 64)), static_cast<unsigned>(ceil_div(n, 64)));
+  apply_linv_tiled_kernel<<<grid, 256, 0, s>>>(rinv, l, f, n, tmp);
   LPCA_CUDA(cudaMemcpyAsync(f, tmp, static_cast<std::size_t>(total) * sizeof(double),
                             cudaMemcpyDeviceToDevice, s));
 }

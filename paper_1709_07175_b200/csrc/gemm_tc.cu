@@ -573,7 +573,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
     a.npad = wc;
     a.chunk_rows = static_cast<int>(rows);
     a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
-    a.run_stages = 4;  // fp16: one run (4 x 64 rows) per kUScaleRows block of U^T scales
+    a.run_stages = static_cast<int>(kUScaleRows / 64);  // fp16: one run (8 x 64 rows) per block of U^T scales
     a.scan = p.half && !p.xmax_in;
     a.xmax_in = p.xmax_in;
     a.uinv_in = p.uinv ? p.uinv + c0 : nullptr;

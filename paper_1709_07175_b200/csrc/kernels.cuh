@@ -138,7 +138,7 @@ void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, 
 // kUScaleRows-row block (uinv[block][c])). Planes are K-major: [wpad or round_up(l,16)][ld].
 // rows per block of the U^T fp16 plane scales: one 2-SM pair item of the X W
 // pass, one fp16 run (4 stages of 64 rows) of the X^T U pass
-constexpr index_t kUScaleRows = 256;
+constexpr index_t kUScaleRows = 512;  // two X W pair items; one X^T U run
 
 struct XwPairArgs {
   const float* x = nullptr;

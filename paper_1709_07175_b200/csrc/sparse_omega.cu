@@ -285,12 +285,13 @@ __global__ void __launch_bounds__(kThreadsSO, 1)
 // row-major fp32 U: the layout the X^T U pair kernel reads (the same rule as
 // the X W pass epilogue, tc_pair.cuh: s = 2^(14 - floor(log2 max|U|)) per
 // column and block, hi = fp16(u s), lo = fp16(u s - hi), inverse scale kept).
-// One CTA per 256-row block and 32-column group; thread = row.
-__global__ void __launch_bounds__(256) u_planes_f16_kernel(const float* __restrict__ u, index_t m, index_t ld,
+// One CTA per kUScaleRows-row block and 32-column group; thread = row.
+__global__ void __launch_bounds__(kUScaleRows) u_planes_f16_kernel(const float* __restrict__ u, index_t m, index_t ld,
                                                            index_t npad, __half* __restrict__ hi,
                                                            __half* __restrict__ lo, index_t ldt,
                                                            float* __restrict__ uinv) {
-  __shared__ float red[8][32];
+  constexpr int kW = static_cast<int>(kUScaleRows) / 32;
+  __shared__ float red[kW][32];
   __shared__ float scl[32];
   const index_t blk = blockIdx.x;
   const index_t row = blk * kUScaleRows + threadIdx.x;
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(256) u_planes_f16_kernel(const float* __restri
   __syncthreads();
   if (threadIdx.x < 32) {
     float a = 0.0f;
-    for (int w = 0; w < 8; ++w) a = fmaxf(a, red[w][threadIdx.x]);
+    for (int w = 0; w < kW; ++w) a = fmaxf(a, red[w][threadIdx.x]);
     float s = 1.0f;
     if (a > 0.0f && !isinf(a)) {
       int e = static_cast<int>((__float_as_uint(a) >> 23) & 0xffu) - 127;
@@ -384,7 +385,7 @@ void launch_u_planes_f16(cudaStream_t s, const float* u, index_t m, index_t ld, 
                          index_t ldt, float* uinv) {
   if (m <= 0) return;
   const dim3 grid(static_cast<unsigned>((m + kUScaleRows - 1) / kUScaleRows), static_cast<unsigned>((npad + 31) / 32));
-  u_planes_f16_kernel<<<grid, 256, 0, s>>>(u, m, ld, npad, hi, lo, ldt, uinv);
+  u_planes_f16_kernel<<<grid, static_cast<unsigned>(kUScaleRows), 0, s>>>(u, m, ld, npad, hi, lo, ldt, uinv);
 }
 
 template void launch_sparse_sketch<float>(cudaStream_t, const float*, index_t, index_t, index_t, const int*,

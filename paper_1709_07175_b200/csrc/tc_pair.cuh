@@ -279,6 +279,19 @@ __device__ __forceinline__ void split_f16_16(const float* v, float (&hi)[8], flo
   }
 }
 
+// The items a pair works through. X W: two consecutive 256-row items (one
+// kUScaleRows block of U^T scales) back to back, so the block's second item can
+// settle the block's scales; X^T U: every npairs-th item. -1 when done.
+template <int kMode>
+__device__ __forceinline__ int pair_item(int pair, int npairs, int it, int items) {
+  if (kMode == kXW) {
+    const int item = 2 * (pair + (it >> 1) * npairs) + (it & 1);
+    return item < items ? item : -1;
+  }
+  const int item = pair + it * npairs;
+  return item < items ? item : -1;
+}
+
 template <int kMode>
 __device__ __forceinline__ void pair_item_coords(const PairArgs& a, int item, int& t0, int& k0, int& k1) {
   if (kMode == kXW) {
@@ -394,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
       int stage = 0;
       uint32_t phase = 0;
       const int brow = static_cast<int>(rank) * (a.npad / 2);
-      for (int item = pair; item < a.items; item += npairs) {
+      for (int it = 0, item; (item = pair_item<kMode>(pair, npairs, it, a.items)) >= 0; ++it) {
         int t0, k0, k1;
         pair_item_coords<kMode>(a, item, t0, k0, k1);
         const int mine = t0 + static_cast<int>(rank) * kBM;
@@ -426,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
       const uint64_t desc0 = sw128_desc(smem_u32(smem) + x_bytes, 16, 1024);
       int stage = 0, aslot = 0, rc = 0;
       uint32_t phase = 0, aphase = 0;
-      for (int item = pair; item < a.items; item += npairs) {
+      for (int it = 0, item; (item = pair_item<kMode>(pair, npairs, it, a.items)) >= 0; ++it) {
         int t0, k0, k1;
         pair_item_coords<kMode>(a, item, t0, k0, k1);
         for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
@@ -560,7 +573,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
       for (int kk = 0; kk < 4; ++kk) v[kk] = fmaxf(v[kk], v[kk + 4]);
       return fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
     };
-    for (int item = pair; item < a.items; item += npairs) {
+    for (int it = 0, item; (item = pair_item<kMode>(pair, npairs, it, a.items)) >= 0; ++it) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
       for (int q0 = k0; q0 < k1; q0 += run_k, ++rc) {
@@ -736,7 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
     const float xinv = 1.0f / xs;
     int rc = 0;
     int xit = 0;  // planes16 items done (xch / xbuf parity)
-    for (int item = pair; item < a.items; item += npairs) {
+    for (int it = 0, item; (item = pair_item<kMode>(pair, npairs, it, a.items)) >= 0; ++it) {
       int t0, k0, k1;
       pair_item_coords<kMode>(a, item, t0, k0, k1);
       const int runs = (k1 - k0 + run_k - 1) / run_k;
@@ -897,13 +910,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
         }
         mbar_wait(&xch[xb], (xit >> 1) & 1, 6);
         ++xit;
+        // A scale block is two items (kUScaleRows = 2 x 256 rows), done back to
+        // back by this pair (pair_item): the first item's planes go out at its
+        // own scale with one bit of headroom, s1; the second keeps s1 when its
+        // maxima fit under it, else settles s < s1 from both maxima and rescales
+        // the first item's planes by s / s1 (a power of two).
         const int blk = t0 / kUScaleRows;
+        const bool second = (t0 / (2 * kBM)) & 1;
+        float* m1keep = red + 4 * a.npad;  // the first item's pair maxima (raw accumulator)
+        float* fac = red + 5 * a.npad;     // second item: s / s1 per column
         // (a pair whose rows all lie past m owns no block: writing its scales
-        // would run past the [ceil(m/256)][npad] array)
+        // would run past the [ceil(m / kUScaleRows)][npad] array)
         for (int c = ew * 32 + lane; c < a.npad; c += 32 * kEpiWarps) {
           const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
-          const float mx = fmaxf(gsc[c], xbuf[xb * a.npad + c]) * f;
-          const float sc = pow2_scale_for(mx);
+          float mraw = fmaxf(gsc[c], xbuf[xb * a.npad + c]);
+          float sc;
+          if (second) {
+            const float m1 = m1keep[c];
+            const float s1 = 0.5f * pow2_scale_for(m1 * f);
+            if (mraw * f * s1 < 32768.0f) {  // within the first item's headroom: its scale stands
+              sc = s1;
+            } else {
+              sc = pow2_scale_for(fmaxf(mraw, m1) * f);
+            }
+            fac[c] = sc / s1;
+          } else {
+            m1keep[c] = mraw;
+            sc = 0.5f * pow2_scale_for(mraw * f);  // one bit of headroom for the block's second item
+          }
           gsc[c] = f * sc;
           if (rank == 0 && blk * kUScaleRows < a.m) a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
         }
@@ -919,6 +953,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
               const __half h = __float2half_rn(y);
               a.uh[static_cast<size_t>(c) * a.ldh + row] = h;
               a.ul[static_cast<size_t>(c) * a.ldh + row] = __float2half_rn(y - __half2float(h));
+            }
+          }
+        }
+        if (second) {  // the first item's row of this thread (written by this thread)
+          const size_t r1 = static_cast<size_t>(row - 2 * kBM);
+          for (int c = c_lo; c < c_hi; ++c) {
+            const float g = fac[c];
+            if (g != 1.0f) {
+              __half* ph = a.uh + static_cast<size_t>(c) * a.ldh + r1;
+              __half* pl = a.ul + static_cast<size_t>(c) * a.ldh + r1;
+              *ph = __float2half_rn(__half2float(*ph) * g);
+              *pl = __float2half_rn(__half2float(*pl) * g);
             }
           }
         }

@@ -546,6 +546,8 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
 index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_split) {
   const index_t ntiles = ceil_div(n, 2 * kBM);
   index_t chunks = ceil_div(8 * static_cast<index_t>(num_sms / 2), ntiles);  // ~8 items per pair
+  const index_t cap = env_int("LPCA_UTX_CHUNK_ROWS", 0);  // A/B: cap the rows per chunk (L2 reuse of U^T)
+  if (cap > 0 && ceil_div(m, chunks) > cap) chunks = ceil_div(m, cap);
   const index_t max_chunks = ceil_div(m, 4 * kUScaleRows);                   // >= 4 runs per item
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;

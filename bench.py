@@ -327,6 +327,7 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # comm_nranks lines stay visible in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [lp.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)

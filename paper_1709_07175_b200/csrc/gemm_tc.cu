@@ -478,15 +478,14 @@ bool tc_pair_mode() { return pair_mode(); }
 // holds two run buffers, the long accumulator and two A slots only for N <= 128.
 int pair_max_n() { return env_int("LPCA_TC_MAXN", 128); }
 
-// Column slices of a padded width: ceil(wpad / max) slices of equal 16-multiples.
-// Each slice is one more pass over X; a wide slice costs TMEM double-buffering
-// (above 168 columns one run buffer and one A slot remain). Measured per pass
-// element (c3, c4): X W 112-wide 0.88, 160-wide 1.48, 224-wide 1.57 ps; X^T U
-// 160-wide 1.15x a 112-wide. So X W takes one slice up to 224 columns and
-// 128-column slices above; X^T U takes slices of up to 224. LPCA_TC_MAXN forces
-// one maximum for both.
-int slice_width(index_t wpad, bool xtu) {
-  int mx = xtu ? 224 : (wpad <= 224 ? 224 : 128);
+// Column slices of a padded width: ceil(wpad / 224) slices of equal 16-multiples.
+// Each slice is one more pass over X (and one more fp16 split of it), so fewer
+// slices win now that the quarter A slots fill whatever TMEM a wide slice
+// leaves: c4 (l = 300) X W as two 152-wide slices 74 ms against three 112-wide
+// 88 ms (round 1, before quarter slots, 128-wide slices had won above 224).
+// LPCA_TC_MAXN sets another maximum (A/B).
+int slice_width(index_t wpad, bool) {
+  int mx = 224;
   if (std::getenv("LPCA_TC_MAXN")) mx = pair_max_n();
   const index_t nsl = ceil_div(wpad, static_cast<index_t>(mx));
   return static_cast<int>(round_up(ceil_div(wpad, nsl), 16));
@@ -512,6 +511,7 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
     a.run_stages = env_int("LPCA_TC_RUN", 8);
     a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f) ? (p.ovf ? 2 : 1) : 0;
     a.ovf = p.ovf;
+    a.wlo_nz = p.half ? p.wlo_nz : nullptr;
     a.xmax_in = p.xmax_in;
     a.xmax_val = p.xmax_val;
     a.xmax_out = c0 == 0 ? p.xmax_out : nullptr;

@@ -152,6 +152,7 @@ struct XwPairArgs {
   float xmax_val = 0.0f;              // max|X| by value (xmax_in null)
   uint32_t* xmax_out = nullptr;       // atomicMax of the |X| bits actually read
   int* ovf = nullptr;  // per-run scales from each run's first stage; set to 1 if a later stage needed a rescan
+  const int* wlo_nz = nullptr;   // fp16: 0 when every w_lo entry is zero (the a_hi w_lo MMAs are skipped)
   float* out = nullptr;          // plain fp32 row-major (first wstore columns)
   index_t ldo = 0, wstore = 0;
   float* out_hi = nullptr;       // tf32 planes of OUT^T [wpad][ldh]
@@ -180,8 +181,9 @@ index_t utx_pair_splits(index_t m, index_t n, int num_sms, index_t* rows_per_spl
 void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms);
 // W (fp64 n x wc, column-major ld ldw) -> fp16 hi/lo planes [wpad][ldd] scaled per
 // column by 2^(14 - floor(log2 max|W[:,c]|)); winv[c] = inverse scale (1 for padding).
+// lo_nz (optional): set to 1 if any lo entry is nonzero, else 0.
 void launch_split_f16_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc, index_t wpad,
-                        __half* hi, __half* lo, index_t ldd, float* winv);
+                        __half* hi, __half* lo, index_t ldd, float* winv, int* lo_nz = nullptr);
 
 // Split a row-major fp32 matrix (m x ld) into tf32 hi/lo planes of the same shape.
 void launch_split_tf32_rows(cudaStream_t s, const float* src, index_t m, index_t ld, float* hi,

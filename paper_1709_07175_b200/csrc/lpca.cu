@@ -523,18 +523,31 @@ struct XScale {
   int* ovf = nullptr;         // scanless per-run scales: flags runs that need the scan
 };
 
-// LPCA_SPARSE_OMEGA=0 sends a very sparse Omega through the dense passes (A/B)
-bool sparse_omega_enabled() {
-  static const bool on = [] {
+// Very sparse Omega on dense X: 0 = always the dense passes, 1 = always the
+// gather sketch, default: the gather when the dense pass is not the tcgen05 one
+// (fp64 X, the SIMT path). On fp32 X the 2-SM pass with the zero lo plane of a
+// {-1, 0, +1} Omega skipped wins (configs[3] slice at 200k rows: 5.4 ms against
+// 8.2 ms for the gather, which is latency-bound at a quarter of HBM).
+int sparse_omega_mode() {
+  static const int mode = [] {
     const char* e = getenv("LPCA_SPARSE_OMEGA");
-    return !(e && e[0] == '0');
+    return e && e[0] == '0' ? 0 : (e && e[0] == '1' ? 1 : 2);
   }();
-  return on;
+  return mode;
 }
 
 bool f16_enabled() {
   static const bool on = [] {
     const char* e = getenv("LPCA_TC_F16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// LPCA_BLO_SKIP=0 keeps the a_hi w_lo MMAs when W is exact in fp16 (A/B)
+bool blo_skip_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LPCA_BLO_SKIP");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -584,8 +597,17 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
       __half* hi = ctx.get<__half>("w.h16hi", p.wpad * p.ldw);
       __half* lo = ctx.get<__half>("w.h16lo", p.wpad * p.ldw);
       float* winv = ctx.get<float>("w.inv", p.wpad);
-      launch_split_f16_w(ctx.stream, w, ldw, n, wc, p.wpad, hi, lo, p.ldw, winv);
+      int* lo_nz = blo_skip_enabled() ? ctx.get<int>("w.lonz", 1) : nullptr;
+      launch_split_f16_w(ctx.stream, w, ldw, n, wc, p.wpad, hi, lo, p.ldw, winv, lo_nz);
       LPCA_LAUNCHED(ctx);
+      p.wlo_nz = lo_nz;
+      if (lo_nz && std::getenv("LPCA_VERBOSE")) {
+        int h = -1;
+        LPCA_CUDA(cudaMemcpyAsync(&h, lo_nz, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+        std::fprintf(stderr, "lazypca_b200: x w pass n=%lld wc=%d w lo plane %s\n", (long long)n, (int)wc,
+                     h ? "nonzero" : "zero (a_hi w_lo MMAs skipped)");
+      }
       p.half = true;
       p.w_hi = hi;
       p.w_lo = lo;
@@ -1093,10 +1115,12 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     XScale sketch;
     sketch.use = true;
     sketch.check = xs.dev;
-    // very sparse Omega on dense X: the sketch is a gather (csrc/sparse_omega.cu,
-    // one HBM-bound read of X) instead of a dense tensor-core pass
-    const bool gather = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && sparse_omega_enabled() &&
-                        u.ld <= 512;
+    // very sparse Omega on dense X: the sketch as a gather (csrc/sparse_omega.cu,
+    // one read of X, the reference's summation order) where the dense pass
+    // would be DMMA or SIMT (sparse_omega_mode)
+    const int so_mode = sparse_omega_mode();
+    const bool gather = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && u.ld <= 512 &&
+                        (so_mode == 1 || (so_mode == 2 && !tc));
     int* xovf = nullptr;
     if (f16 && !ctx.force_scan && !gather) {  // scales from each run's first stage (rerun with the scan if flagged)
       xovf = ctx.get<int>("xovf", 1);

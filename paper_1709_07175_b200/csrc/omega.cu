@@ -409,7 +409,7 @@ void launch_scale_f64(cudaStream_t s, const double* src, double* dst, index_t co
 // hi = fp16_rn(w s), lo = fp16_rn(w s - hi).
 __global__ void split_f16_w_kernel(const double* __restrict__ w, index_t ldw, index_t n, index_t wc,
                                    __half* __restrict__ hi, __half* __restrict__ lo, index_t ldd,
-                                   float* __restrict__ winv) {
+                                   float* __restrict__ winv, int* __restrict__ lo_nz) {
   const index_t c = blockIdx.x;
   __shared__ float red[32];
   float mx = 0.0f;
@@ -432,18 +432,23 @@ __global__ void split_f16_w_kernel(const double* __restrict__ w, index_t ldw, in
     sc = ldexpf(1.0f, e);
   }
   if (threadIdx.x == 0) winv[c] = 1.0f / sc;
+  int any_lo = 0;
   for (index_t j = threadIdx.x; j < ldd; j += blockDim.x) {
     const float y = (c < wc && j < n) ? static_cast<float>(w[c * ldw + j] * static_cast<double>(sc)) : 0.0f;
     const __half h = __float2half_rn(y);
+    const __half l = __float2half_rn(y - __half2float(h));
     hi[c * ldd + j] = h;
-    lo[c * ldd + j] = __float2half_rn(y - __half2float(h));
+    lo[c * ldd + j] = l;
+    any_lo |= __half_as_ushort(l) & 0x7fff;
   }
+  if (__syncthreads_or(any_lo) && threadIdx.x == 0 && lo_nz) atomicOr(lo_nz, 1);
 }
 
 void launch_split_f16_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc, index_t wpad,
-                        __half* hi, __half* lo, index_t ldd, float* winv) {
+                        __half* hi, __half* lo, index_t ldd, float* winv, int* lo_nz) {
   if (wpad <= 0) return;
-  split_f16_w_kernel<<<static_cast<unsigned>(wpad), 256, 0, s>>>(w, ldw, n, wc, hi, lo, ldd, winv);
+  if (lo_nz) LPCA_CUDA(cudaMemsetAsync(lo_nz, 0, sizeof(int), s));
+  split_f16_w_kernel<<<static_cast<unsigned>(wpad), 256, 0, s>>>(w, ldw, n, wc, hi, lo, ldd, winv, lo_nz);
 }
 
 void launch_split_tf32_w(cudaStream_t s, const double* w, index_t ldw, index_t n, index_t wc,

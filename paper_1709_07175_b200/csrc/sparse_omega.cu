@@ -21,8 +21,10 @@
 //
 // Measured (profiles/r02_c4_sparse_sketch.txt): about 1.6 TB/s, a quarter of
 // HBM; the walk is latency-bound (short lists per chunk and column, exposed
-// load latency at each chunk's barrier). It ties with the dense tensor-core
-// pass at configs[3], which reads X three times (l = 300 in three slices).
+// load latency at each chunk's barrier). On fp32 X the dense 2-SM tensor-core
+// pass is faster (two 152-wide slices, the zero lo plane of Omega skipped), so
+// the fit takes this kernel for fp64 X and off the tcgen05 path
+// (lpca.cu sparse_omega_mode).
 #include <cuda_runtime.h>
 
 #include <cstdint>

@@ -65,6 +65,7 @@ struct PairArgs {
   // (bits) or xmax_val
   int scan;
   int* ovf;
+  const int* wlo_nz;  // X W: nonzero when W's lo plane has a nonzero entry (null: assume it does)
   const uint32_t* xmax_in;
   float xmax_val;
   // X W: accumulate max|X| bits of the data actually read here (nullable)
@@ -138,68 +139,68 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 // CTAs: four K-steps (tf32: K = 8, fp16: K = 16), each 8 TMEM columns of A and
 // 32 B of the B rows (descriptor +2).
 #define LPCA_PAIR_STAGE(KIND)                                                                              \
-  "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"                                \
+  "{\n .reg .pred p, t, bl;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n setp.ne.b32 bl, %7, 0;\n"                                \
   " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"                                                              \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %3, %5, p;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%2], %3, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
   " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"                   \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
   " add.u32 ah, %1, 16;\n add.u32 al, %2, 16;\n add.u64 dh, %3, 4;\n add.u64 dl, %4, 4;\n"                 \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
   " add.u32 ah, %1, 24;\n add.u32 al, %2, 24;\n add.u64 dh, %3, 6;\n add.u64 dl, %4, 6;\n"                 \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
   "}"
 
 // Half a stage (K = 32, fp16): 6 MMAs from a 32-column half slot (hi 16, lo 16).
 #define LPCA_PAIR_HALF(KIND)                                                                               \
-  "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"                                \
+  "{\n .reg .pred p, t, bl;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n setp.ne.b32 bl, %7, 0;\n"                                \
   " .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"                                                              \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %3, %5, p;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%2], %3, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [%1], %4, %5, t;\n"                                     \
   " add.u32 ah, %1, 8;\n add.u32 al, %2, 8;\n add.u64 dh, %3, 2;\n add.u64 dl, %4, 2;\n"                   \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dh, %5, t;\n"                                     \
   " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [al], dh, %5, t;\n"                                     \
-  " tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
+  " @bl tcgen05.mma.cta_group::2.kind::" KIND " [%0], [ah], dl, %5, t;\n"                                     \
   "}"
 __device__ __forceinline__ void mma_half_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
-                                              uint32_t idesc, uint32_t acc_first) {
+                                              uint32_t idesc, uint32_t acc_first, uint32_t blo) {
   asm volatile(LPCA_PAIR_HALF("f16")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first),
-               "r"(0u)
+               "r"(blo)
                : "memory");
 }
 #undef LPCA_PAIR_HALF
 
 // A quarter stage (K = 16, fp16): 3 MMAs from a 16-column quarter slot (hi 8, lo 8).
 __device__ __forceinline__ void mma_quarter_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
-                                                 uint32_t idesc, uint32_t acc_first) {
+                                                 uint32_t idesc, uint32_t acc_first, uint32_t blo) {
   asm volatile(
-      "{\n .reg .pred p, t;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n"
+      "{\n .reg .pred p, t, bl;\n setp.ne.b32 p, %6, 0;\n setp.eq.u32 t, %7, %7;\n setp.ne.b32 bl, %7, 0;\n"
       " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %3, %5, p;\n"
       " tcgen05.mma.cta_group::2.kind::f16 [%0], [%2], %3, %5, t;\n"
-      " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %4, %5, t;\n"
+      " @bl tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %4, %5, t;\n"
       "}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first), "r"(0u)
+      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_first), "r"(blo)
       : "memory");
 }
 
 template <bool kHalf>
 __device__ __forceinline__ void mma_stage_pair(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
-                                               uint32_t idesc, uint32_t acc_first) {
+                                               uint32_t idesc, uint32_t acc_first, uint32_t blo) {
   if constexpr (kHalf)
     asm volatile(LPCA_PAIR_STAGE("f16")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc),
-                 "r"(acc_first), "r"(0u)
+                 "r"(acc_first), "r"(blo)
                  : "memory");
   else
     asm volatile(LPCA_PAIR_STAGE("tf32")::"r"(d), "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(idesc),
-                 "r"(acc_first), "r"(0u)
+                 "r"(acc_first), "r"(blo)
                  : "memory");
 }
 #undef LPCA_PAIR_STAGE
@@ -436,6 +437,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
     // ---------------- MMA issuer (leader only, whole warp) ----------------
     if (leader) {
       const uint32_t idesc = kHalf ? idesc_f16(2 * kBM, a.npad) : idesc_tf32(2 * kBM, a.npad, 0, 0);
+      // B's lo plane all zero (W exact in fp16, e.g. a very sparse Omega): the
+      // a_hi b_lo products add exact zeros and are skipped
+      const uint32_t blo = (kMode == kXW && a.wlo_nz && *a.wlo_nz == 0) ? 0u : 1u;
       const uint64_t desc0 = sw128_desc(smem_u32(smem) + x_bytes, 16, 1024);
       int stage = 0, aslot = 0, rc = 0;
       uint32_t phase = 0, aphase = 0;
@@ -479,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
                 }
                 const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 16);
                 if (elect_one()) {
-                  mma_quarter_pair(d, at, at + 8, bh + 2 * hh, bl + 2 * hh, idesc, (k != q0 || hh) ? 1u : 0u);
+                  mma_quarter_pair(d, at, at + 8, bh + 2 * hh, bl + 2 * hh, idesc, (k != q0 || hh) ? 1u : 0u, blo);
                   if (hh == 3) mma_commit_pair(&empty[stage]);
                   mma_commit_pair(&aempty[aslot]);
                 }
@@ -501,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
                 }
                 const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 32);
                 if (elect_one()) {
-                  mma_half_pair(d, at, at + 16, bh + 4 * hh, bl + 4 * hh, idesc, (k != q0 || hh) ? 1u : 0u);
+                  mma_half_pair(d, at, at + 16, bh + 4 * hh, bl + 4 * hh, idesc, (k != q0 || hh) ? 1u : 0u, blo);
                   if (hh == 1) mma_commit_pair(&empty[stage]);
                   mma_commit_pair(&aempty[aslot]);
                 }
@@ -513,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
             }
             const uint32_t at = tmem_base + a_col0 + static_cast<uint32_t>(aslot * 64);
             if (elect_one()) {
-              mma_stage_pair<kHalf>(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u);
+              mma_stage_pair<kHalf>(d, at, at + 32, bh, bl, idesc, k != q0 ? 1u : 0u, blo);
               mma_commit_pair(&empty[stage]);
               mma_commit_pair(&aempty[aslot]);
             }

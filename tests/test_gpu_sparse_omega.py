@@ -3,7 +3,8 @@ r1 missing #1, BASELINE configs[3]) against the reference's sketch with a
 sparse Omega (build_sketch -> spmm over CSC X and CSC Omega,
 proj/core/src/kernels.cpp:49-68). fp64 data sums each U entry in the
 reference's order (ascending j), so the fit agrees to the fp64 bar; fp32 data
-keeps fp32 sums of +-x."""
+keeps fp32 sums of +-x (the gather serves fp32 only off the tcgen05 path: the
+dense 2-SM pass is faster there)."""
 import numpy as np
 import pytest
 import torch
@@ -43,9 +44,39 @@ def test_fp32_gather_sketch_matches_reference_and_dense_path(ctx, ref, monkeypat
     m, n, l, k, d = 20000, 4096, 110, 50, 1.0 / 64
     x = torch.empty((m, n), dtype=torch.float32, device="cuda")
     lp.synth_lowrank(x, 0, 200, 0.97, 0.01, 1000, ctx=ctx)
-    got = lp.reduce_lazy_spca(x, _cfg(k, l, d), ctx=ctx)
     rv, rs, _, _ = ref.reduce(2, x.cpu().numpy(), k, l, 11, kind=1, density=d)
-    rel = np.abs(got.singular_values - rs) / rs
-    print(f"fp32 gather: sigma rel {rel.max():.2e}")
-    assert rel.max() < 2e-5   # fp32 sums of +-x in U, the fp16 split after it
-    assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+    # fp32 X takes the gather off the tcgen05 path (the SIMT passes), the
+    # dense 2-SM pass with the zero lo plane skipped on it (the default)
+    for path, tol in (("simt", 2e-5), ("tcgen05", 2e-5)):
+        ctx.set_gemm_path(path)
+        try:
+            got = lp.reduce_lazy_spca(x, _cfg(k, l, d), ctx=ctx)
+        finally:
+            ctx.set_gemm_path("tcgen05")
+        rel = np.abs(got.singular_values - rs) / rs
+        print(f"fp32 very sparse Omega, {path}: sigma rel {rel.max():.2e}")
+        assert rel.max() < tol   # fp32 sums of +-x (gather) / the fp16 split
+        assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+
+
+def test_dense_pass_skips_zero_lo_plane_bitwise(tmp_path):
+    """A {-1, 0, +1} Omega is exact in fp16, so its lo plane is zero and the
+    dense X W pass skips the a_hi w_lo MMAs (csrc/omega.cu split_f16_w_kernel
+    flag, tc_pair.cuh @bl predicate): the fit must be bit-identical to the run
+    that issues them (LPCA_BLO_SKIP=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    res = {}
+    for skip in ("1", "0"):
+        env = dict(os.environ, LPCA_SPARSE_OMEGA="0", LPCA_BLO_SKIP=skip, LPCA_VERBOSE="1")
+        f = tmp_path / f"blo{skip}.npz"
+        r = subprocess.run([sys.executable, str(root / "tests" / "helpers" / "blo_run.py"), str(f)],
+                           capture_output=True, text=True, env=env, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert ("a_hi w_lo MMAs skipped" in r.stderr) == (skip == "1")
+        res[skip] = np.load(f)
+    for key in res["1"].files:
+        assert np.array_equal(res["1"][key], res["0"][key]), key

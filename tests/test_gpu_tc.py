@@ -33,9 +33,11 @@ def _fit(ctx, x, k, l, path, q=0, method=lp.ReducerMethod.lazy_spca, seed=7):
     (20000, 4096, 200, 100, 110),  # c2 shape
     (9000, 2048, 300, 200, 220),   # l > 128: two M halves in U^T X (configs[2] rho)
     (4000, 300, 40, 16, 256),     # l = 256 boundary
+    (6000, 2048, 400, 200, 300),  # two 152-wide column slices (configs[3] l)
+    (4000, 2048, 600, 300, 460),  # three 160-wide column slices
 ])
 def test_tc_matches_reference(ctx, ref, m, n, r, k, l):
-    x = _x(m, n, r, 0.98 if l > 128 else 0.97)
+    x = _x(m, n, r, 0.99 if l > 400 else (0.98 if l > 128 else 0.97))
     xh = x.cpu().numpy()
     got = _fit(ctx, x, k, l, "tcgen05")
     rv, rs, _, _ = ref.reduce(2, xh, k, l, 7)
@@ -44,7 +46,7 @@ def test_tc_matches_reference(ctx, ref, m, n, r, k, l):
     ang = np.max(O.principal_angles(got.v[:, :kk], rv[:, :kk]))
     print(f"m={m} n={n} l={l}: sigma rel max {rel.max():.3e}, top-k/2 angle {ang:.2e}")
     assert rel.max() < 1e-4   # north_star's fp32 bar
-    assert rel.max() < 5e-5   # measured 1.9e-6 .. 5.3e-6
+    assert rel.max() < 5e-5   # measured 2.8e-6 .. 1.2e-5
     assert ang < 1e-4
 
 

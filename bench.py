@@ -389,7 +389,12 @@ def run_ours(args, cfg):
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(args, cfg, ctx, x, conf, m_global, dist, lp, torch)
+        xh = _pinned_copy(x, k, torch)
+        # the C-ABI call stages X on the device itself: release the resident
+        # shard first (configs[3]: two 131 GB copies do not fit in HBM)
+        del x, y, step
+        torch.cuda.empty_cache()
+        e2e = xh if isinstance(xh, dict) else _e2e(args, cfg, ctx, xh, conf, m_global, dist, lp, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, kind, cores, desc, _ = cpu_reference(cfg, int(args.cpu_rows or CPU_ROWS[args.config]),
@@ -419,19 +424,28 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def _e2e(args, cfg, ctx, x, conf, m_global, dist, lp, torch):
-    """Same metric through the public C ABI with host buffers: every step copies
-    this rank's X from pinned host memory to the device and Y back
-    (lpca_fit_transform with LPCA_HOST views)."""
-    import ctypes as C
-    from paper_1709_07175_b200 import _lib as L
-    m, n, k = x.shape[0], cfg["n"], cfg["k"]
+def _pinned_copy(x, k, torch):
+    """This rank's X in pinned host memory (and the pinned Y buffer), or an
+    "unavailable" record."""
+    m, n = x.shape
     try:
         xh = torch.empty((m, n), dtype=x.dtype, pin_memory=True)
         yh = torch.empty((m, k), dtype=x.dtype, pin_memory=True)
     except RuntimeError as e:
         return {"unavailable": f"pinned host buffers of {m * n * x.element_size() / 1e9:.1f} GB: {e}"[:200]}
     xh.copy_(x)
+    return xh, yh
+
+
+def _e2e(args, cfg, ctx, host, conf, m_global, dist, lp, torch):
+    """Same metric through the public C ABI with host buffers: every step copies
+    this rank's X from pinned host memory to the device and Y back
+    (lpca_fit_transform with LPCA_HOST views)."""
+    import ctypes as C
+    from paper_1709_07175_b200 import _lib as L
+    xh, yh = host
+    x = xh
+    m, n, k = x.shape[0], cfg["n"], cfg["k"]
     vw = lp.api._View(xh)  # host row-major view
     cfgc = conf._c()
     dt = L.LPCA_F32 if x.dtype == torch.float32 else L.LPCA_F64

@@ -4,8 +4,10 @@ The reference CLI's reduce / compare / bench (proj/tools/lazypca_cli.cpp:162-452
 over this library: the same options and defaults, the same JSON records
 (timings; comparison_record_json, metrics.cpp:354-371), the same exit codes
 (ParseError / InvalidArgument 2, RankDeficiency 3, Dimension 4, other 1,
-lazypca_cli.cpp:618-635), plus `--device N` (the GPU to run on). JSON manifests
-and gen-synthetic are not provided.
+lazypca_cli.cpp:618-635) and `--manifest` defaults for reduce / compare
+(load_manifest / fill_from, lazypca_cli.cpp:47-69, 580-613), plus `--device N`
+(the GPU to run on). gen-synthetic (the reference's sparse synthetic generator)
+is out of scope.
 """
 from __future__ import annotations
 
@@ -176,6 +178,65 @@ def run_bench(a, ctx) -> int:
     return 0
 
 
+def _load_manifest(path: str) -> dict:
+    """load_manifest (lazypca_cli.cpp:47-58): a JSON object, else ParseError."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        raise lp.ParseError("manifest: cannot open " + path) from None
+    try:
+        j = json.loads(text)
+    except ValueError as e:
+        raise lp.ParseError(f"manifest: {e}") from None
+    if not isinstance(j, dict):
+        raise lp.ParseError("manifest: top level must be a JSON object")
+    return j
+
+
+def _given(argv, flag: str) -> bool:
+    return any(v == flag or v.startswith(flag + "=") for v in argv)
+
+
+def _fill_from(a, argv, flag: str, j: dict, key: str, attr: str, kind) -> None:
+    """fill_from (lazypca_cli.cpp:60-69): the manifest's value unless the flag
+    was given on the command line; a value of the wrong JSON type is a
+    ParseError naming the key (nlohmann's get<T>: numbers convert between
+    integer and floating point, strings and booleans do not)."""
+    if _given(argv, flag) or key not in j:
+        return
+    v = j[key]
+    ok = (isinstance(v, str) if kind is str else isinstance(v, bool) if kind is bool
+          else isinstance(v, (int, float)) and not isinstance(v, bool))
+    if not ok:
+        raise lp.ParseError(f'manifest: bad value for "{key}": type must be {kind.__name__}, '
+                            f"but is {type(v).__name__}")
+    if kind is int:
+        v = int(v)
+        if attr == "seed" and v < 0:
+            v &= (1 << 64) - 1
+    setattr(a, attr, v)
+
+
+_FIT_KEYS = [("--input", "input", "input", str), ("--format", "format", "format", str),
+             ("--k", "k", "k", int), ("--l", "l", "l", int), ("--projection", "projection", "projection", str),
+             ("--density-policy", "density_policy", "density_policy", str), ("--seed", "seed", "seed", int)]
+_REDUCE_KEYS = [("--method", "method", "method", str), ("--block-rows", "block_rows", "block_rows", int),
+                ("--streaming", "streaming", "streaming", bool),
+                ("--deterministic", "deterministic", "deterministic", bool),
+                ("--out-map", "out_map", "out_map", str), ("--out-reduced", "out_reduced", "out_reduced", str)]
+_COMPARE_KEYS = [("--method-a", "method_a", "method_a", str), ("--method-b", "method_b", "method_b", str)]
+
+
+def _apply_manifest(a, argv) -> None:
+    if not getattr(a, "manifest", ""):
+        return
+    j = _load_manifest(a.manifest)
+    keys = _FIT_KEYS + (_REDUCE_KEYS if a.cmd == "reduce" else _COMPARE_KEYS)
+    for flag, key, attr, kind in keys:
+        _fill_from(a, argv, flag, j, key, attr, kind)
+
+
 def _fit_args(p, method_default="spca"):
     p.add_argument("--input", default="")
     p.add_argument("--format", default="mm")
@@ -200,6 +261,7 @@ def main(argv=None) -> int:
     r.add_argument("--out-map", dest="out_map", default="")
     r.add_argument("--out-reduced", dest="out_reduced", default="")
     r.add_argument("--report", default="json")
+    r.add_argument("--manifest", default="", help="JSON manifest with defaults for the above")
     c = sub.add_parser("compare", help="run two methods on the same data and report agreement")
     _fit_args(c)
     c.add_argument("--input-a", dest="input_a", default="")
@@ -208,6 +270,7 @@ def main(argv=None) -> int:
     c.add_argument("--method-b", dest="method_b", default="lazy_spca")
     c.add_argument("--max-pairs", dest="max_pairs", type=int, default=10000)
     c.add_argument("--out-report", dest="out_report", default="")
+    c.add_argument("--manifest", default="", help="JSON manifest with defaults for the above")
     b = sub.add_parser("bench", help="time the reducers over a list of target dims")
     b.add_argument("--input", default="")
     b.add_argument("--format", default="mm")
@@ -222,11 +285,13 @@ def main(argv=None) -> int:
     b.add_argument("--projection", default="very_sparse")
     b.add_argument("--density-policy", dest="density_policy", default="aggressive")
     b.add_argument("--out", default="")
+    argv = sys.argv[1:] if argv is None else list(argv)
     a = ap.parse_args(argv)
     if not a.cmd:
         ap.print_help()
         return 0
     try:
+        _apply_manifest(a, argv)
         ctx = lp.Context(a.device)
         return {"reduce": run_reduce, "compare": run_compare, "bench": run_bench}[a.cmd](a, ctx)
     except lp.ParseError as e:

@@ -1133,7 +1133,8 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       const index_t nch = sparse_sketch_chunks(n, x.dtype);
       int* counts = ctx.get<int>("so.counts", nch * l);
       int* ptr = ctx.get<int>("so.ptr", nch * l + 1);
-      auto* ent = ctx.get<std::uint32_t>("so.ent", n * l);
+      // per (chunk, column): its nonzeros padded to pairs, at least one pair
+      auto* ent = ctx.get<std::uint32_t>("so.ent", (n + 2 * nch) * l);
       launch_omega_chunk_lists(ctx.stream, omega, n, l, x.dtype, counts, ptr, ent);
       ctx.note_launch(3);
       ev.mark(12);

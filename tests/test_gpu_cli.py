@@ -46,6 +46,21 @@ def test_reduce_writes_map_and_reduced(data, ctx):
         assert np.allclose(y, x @ m.v, rtol=1e-9, atol=1e-9)
 
 
+def test_reduce_manifest_matches_flags(data):
+    """--manifest supplies the flags not given (lazypca_cli.cpp:580-598): the
+    map equals the one from the same settings as flags."""
+    _, mtx, _, tmp = data
+    man = tmp / "m.json"
+    man.write_text(json.dumps({"input": str(mtx), "method": "lazy_spca", "k": 5, "l": 9, "seed": 4,
+                               "out_map": str(tmp / "from_manifest.map")}))
+    r = _cli("reduce", "--manifest", str(man), "--k", "6")
+    assert r.returncode == 0, r.stderr
+    r2 = _cli("reduce", "--input", str(mtx), "--method", "lazy_spca", "--k", "6", "--l", "9", "--seed", "4",
+              "--out-map", str(tmp / "from_flags.map"))
+    assert r2.returncode == 0, r2.stderr
+    assert (tmp / "from_manifest.map").read_bytes() == (tmp / "from_flags.map").read_bytes()
+
+
 def test_compare_spca_lazy_record_and_exit(data):
     _, mtx, _, tmp = data
     rep = tmp / "r.jsonl"

@@ -143,6 +143,32 @@ struct lpca_ctx {
 
   void note_launch(int n = 1) { launches += n; }
 
+  // Host X crossing PCIe in row chunks on copy_stream (lpca_fit,
+  // lpca_fit_transform): (end row, landed event) per chunk, in order. The
+  // fp16 sketch consumes the chunks as they land (xw_pass); every other reader
+  // of X waits for all of them first (wait_arrivals). The transform's Y comes
+  // back the same way, chunk by chunk behind the transform's launches.
+  cudaStream_t copy_stream = nullptr;
+  std::vector<std::pair<index_t, cudaEvent_t>> arrivals;
+  std::vector<cudaEvent_t> chunk_ev[2];  // [0] H2D chunks, [1] D2H chunks
+  cudaStream_t copies() {
+    if (!copy_stream) LPCA_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    return copy_stream;
+  }
+  cudaEvent_t chunk_event(int pool, std::size_t i) {
+    auto& v = chunk_ev[pool];
+    while (v.size() <= i) {
+      cudaEvent_t e = nullptr;
+      LPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      v.push_back(e);
+    }
+    return v[i];
+  }
+  void wait_arrivals() {
+    if (!arrivals.empty()) LPCA_CUDA(cudaStreamWaitEvent(stream, arrivals.back().second, 0));
+    arrivals.clear();
+  }
+
   // Pinned host block for the small device->host reads of one call (status
   // words, eigenvalues, R diagonals): cudaMemcpyAsync into pageable memory
   // would block the host at the copy, before the work queued behind it.
@@ -486,6 +512,86 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
   return d;
 }
 
+// Rows per PCIe chunk of a host X (about 1 GiB, a multiple of the U^T scale
+// block so every chunk starts a new block), or 0: one copy (LPCA_H2D_CHUNKS=0,
+// or fewer than two chunks' worth of rows).
+// (LPCA_H2D_CHUNKS and LPCA_H2D_CHUNK_MB are read per call: tests switch them)
+bool copy_chunks_enabled() {
+  const char* e = std::getenv("LPCA_H2D_CHUNKS");
+  return !(e && e[0] == '0');
+}
+
+index_t h2d_chunk_rows(index_t rows, index_t row_bytes) {
+  if (!copy_chunks_enabled() || row_bytes <= 0) return 0;
+  const char* mb = std::getenv("LPCA_H2D_CHUNK_MB");
+  const index_t bytes = (mb && std::atoll(mb) > 0 ? std::atoll(mb) : 1024) << 20;
+  index_t r = bytes / row_bytes / kUScaleRows * kUScaleRows;
+  if (r < kUScaleRows) r = kUScaleRows;
+  return rows >= 2 * r ? r : 0;
+}
+
+// Rows per chunk of a transform whose Y goes to the host: 16 chunks on
+// whole U^T-scale-sized blocks, or 0 (one copy) for small m.
+index_t d2h_chunk_rows(index_t rows) {
+  if (!copy_chunks_enabled()) return 0;  // LPCA_H2D_CHUNKS=0
+  const index_t r = round_up(ceil_div(rows, index_t(16)), kUScaleRows);
+  return rows >= 4 * r && rows >= 16 * kUScaleRows ? r : 0;
+}
+
+// stage_x for the fits: a host row-major X of at least two chunks crosses PCIe
+// in chunks on the copy stream (after `start`, recorded on the compute stream
+// once the buffer's previous readers are queued), each chunk's landing in
+// ctx.arrivals and the last one also in `done`. Other inputs: stage_x.
+DevX stage_x_arriving(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes,
+                      cudaEvent_t start, cudaEvent_t done) {
+  if (x && x->layout == LPCA_ROW_MAJOR && x->location == LPCA_HOST && x->rows > 0 && x->cols > 0) {
+    check_view(x);
+    const std::size_t es = dsize(x->dtype);
+    const index_t chunk = h2d_chunk_rows(x->rows, static_cast<index_t>(es) * x->cols);
+    if (chunk > 0) {
+      DevX d;
+      d.m = x->rows;
+      d.n = x->cols;
+      d.dtype = x->dtype;
+      d.ld = x->cols;
+      const index_t ld = x->ld > 0 ? x->ld : x->cols;
+      void* dst = ctx.buf(slot, es * d.m * d.n);
+      cudaStream_t cs = ctx.copies();
+      LPCA_CUDA(cudaStreamWaitEvent(cs, start, 0));
+      ctx.arrivals.clear();
+      std::size_t i = 0;
+      for (index_t r0 = 0; r0 < d.m; r0 += chunk, ++i) {
+        const index_t r1 = r0 + chunk < d.m ? r0 + chunk : d.m;
+        LPCA_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + es * r0 * d.n, es * d.n,
+                                    static_cast<const char*>(x->data) + es * r0 * ld, es * ld, es * d.n, r1 - r0,
+                                    cudaMemcpyHostToDevice, cs));
+        const cudaEvent_t e = ctx.chunk_event(0, i);
+        LPCA_CUDA(cudaEventRecord(e, cs));
+        ctx.arrivals.emplace_back(r1, e);
+      }
+      LPCA_CUDA(cudaEventRecord(done, cs));
+      if (h2d_bytes) *h2d_bytes += static_cast<double>(es * d.m * d.n);
+      d.p = dst;
+      return d;
+    }
+  }
+  DevX d = stage_x(ctx, x, slot, h2d_bytes);
+  LPCA_CUDA(cudaEventRecord(done, ctx.stream));
+  return d;
+}
+
+// Ends a fit's use of the copy stream: nothing still waits on a chunk, and no
+// copy still reads the caller's host buffers when the call returns (also on
+// the error paths).
+struct CopyScope {
+  lpca_ctx& ctx;
+  explicit CopyScope(lpca_ctx& c) : ctx(c) {}
+  ~CopyScope() {
+    ctx.arrivals.clear();
+    if (ctx.copy_stream) cudaStreamSynchronize(ctx.copy_stream);
+  }
+};
+
 // ---- GEMM dispatch ------------------------------------------------------------
 // Which engine runs an fp32 X-pass: tcgen05 split-TF32 when the path is
 // selected and the shape is supported, SIMT FFMA otherwise (fp64: DFMA).
@@ -566,6 +672,9 @@ void pass_mark(lpca_ctx& ctx, int which) {
 void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t ldw, const Panel& out,
              bool exact, const XScale* xs = nullptr) {
   const index_t m = x.m, n = x.n;
+  // only the 2-SM pass takes X chunk by chunk as it lands (ctx.arrivals)
+  const bool pair = !x.sparse() && x.dtype == 4 && use_tc(ctx, x, wc) && tc_pair_mode();
+  if (!pair) ctx.wait_arrivals();
   if (m == 0) return;
   if (x.sparse()) {  // row gathers over CSR in the reference's order (kernels.cpp:30-47)
     double* wt = ctx.get<double>("w.rows", n * wc);
@@ -643,8 +752,40 @@ void xw_pass(lpca_ctx& ctx, const DevX& x, const double* w, index_t wc, index_t 
       p.ev_pre = ctx.ev[ctx.pass_slot];
       p.ev_post = ctx.ev[ctx.pass_slot + 1];
     }
-    launch_xw_pair(ctx.stream, p, ctx.num_sms);
-    LPCA_LAUNCHED(ctx);
+    if (ctx.arrivals.empty()) {
+      launch_xw_pair(ctx.stream, p, ctx.num_sms);
+      LPCA_LAUNCHED(ctx);
+      return;
+    }
+    // X still crossing PCIe: one launch per landed chunk (chunks start on
+    // U^T scale blocks, so each launch owns whole blocks of the planes)
+    const auto chunks = std::move(ctx.arrivals);
+    ctx.arrivals.clear();
+    if (chunks.back().first != m) throw Error(kInternal, "xw_pass: arriving chunks do not cover X");
+    index_t r0 = 0;
+    for (std::size_t i = 0; i < chunks.size(); ++i) {
+      const index_t r1 = chunks[i].first;
+      if (r0 % kUScaleRows) throw Error(kInternal, "xw_pass: chunk not on a scale block");
+      LPCA_CUDA(cudaStreamWaitEvent(ctx.stream, chunks[i].second, 0));
+      XwPairArgs q = p;
+      q.x = p.x + r0 * p.ldx;
+      q.m = r1 - r0;
+      if (q.out) q.out += r0 * p.ldo;
+      if (q.uh) {
+        q.uh += r0;
+        q.ul += r0;
+        q.uinv += (r0 / kUScaleRows) * p.wpad;
+      }
+      if (q.out_hi) {
+        q.out_hi += r0;
+        q.out_lo += r0;
+      }
+      q.ev_pre = i == 0 ? p.ev_pre : nullptr;
+      q.ev_post = i + 1 == chunks.size() ? p.ev_post : nullptr;
+      launch_xw_pair(ctx.stream, q, ctx.num_sms);
+      LPCA_LAUNCHED(ctx);
+      r0 = r1;
+    }
     return;
   }
   if (use_tc(ctx, x, wc)) {
@@ -1130,6 +1271,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     ev.mark(12);
     ev.mark(13);
     if (gather) {
+      ctx.wait_arrivals();
       const index_t nch = sparse_sketch_chunks(n, x.dtype);
       int* counts = ctx.get<int>("so.counts", nch * l);
       int* ptr = ctx.get<int>("so.ptr", nch * l + 1);
@@ -1160,6 +1302,7 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);
       ctx.pass_slot = -1;
     }
+    ctx.wait_arrivals();  // everything after the sketch reads all of X
     double* xovf_all = nullptr;  // the flag summed over ranks: every rank reruns, or none
     if (ctx.world > 1 && !ctx.force_scan) {  // issued by every rank, with or without an fp16 sketch
       xovf_all = ctx.get<double>("xovf.all", 1);
@@ -1345,11 +1488,13 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
   if (ldy < (row ? k : m))
     throw Error(kInvalidArgument, "transform: ldy = " + S(ldy) + " is smaller than the output's " +
                                       (row ? "row length k = " + S(k) : "column length m = " + S(m)));
+  ctx.wait_arrivals();
   PhaseEvents ev(ctx);
   ev.mark(6);
   ev.mark(16);
   ev.mark(17);
   ctx.pass_slot = 16;
+  bool y_copied = false;  // Y already on its way to the host chunk by chunk
   if (m > 0 && k > 0) {
     const std::size_t ybytes = dsize(y_dtype) * static_cast<std::size_t>(row ? m * ldy : k * ldy);
     void* ydev = y_location == LPCA_DEVICE ? y : ctx.buf("y", ybytes);
@@ -1386,7 +1531,41 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
         xs.use = true;
         xs.ovf = ctx.get<int>("t.ovf", 1);
         launch_zero(ctx.stream, xs.ovf, sizeof(int));
-        xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
+        const index_t ych = y_location == LPCA_HOST ? d2h_chunk_rows(m) : 0;
+        if (ych > 0) {
+          // Y to a host buffer: each row chunk's copy (copy stream) runs
+          // behind the next chunk's launch, so only the last chunk's copy
+          // is exposed
+          cudaStream_t cs = ctx.copies();
+          const std::size_t es = dsize(y_dtype);
+          pass_mark(ctx, 0);
+          ctx.pass_slot = -1;
+          std::size_t i = 0;
+          for (index_t r0 = 0; r0 < m; r0 += ych, ++i) {
+            const index_t r1 = r0 + ych < m ? r0 + ych : m;
+            DevX xc = x;
+            xc.p = static_cast<const float*>(x.p) + r0 * x.ld;
+            xc.m = r1 - r0;
+            Panel yc = yo;
+            yc.plain = static_cast<char*>(ydev) + es * r0 * ldy;
+            xw_pass(ctx, xc, map.v, k, map.n, yc, false, &xs);
+            const cudaEvent_t e = ctx.chunk_event(1, i);
+            LPCA_CUDA(cudaEventRecord(e, ctx.stream));
+            LPCA_CUDA(cudaStreamWaitEvent(cs, e, 0));
+            LPCA_CUDA(cudaMemcpyAsync(static_cast<char*>(y) + es * r0 * ldy, yc.plain, es * (r1 - r0) * ldy,
+                                      cudaMemcpyDeviceToHost, cs));
+          }
+          ctx.pass_slot = 16;
+          pass_mark(ctx, 1);
+          ev.mark(7);
+          const cudaEvent_t done = ctx.chunk_event(1, i);
+          LPCA_CUDA(cudaEventRecord(done, cs));
+          LPCA_CUDA(cudaStreamWaitEvent(ctx.stream, done, 0));
+          y_copied = true;
+          if (d2h) *d2h += static_cast<double>(ybytes);
+        } else {
+          xw_pass(ctx, x, map.v, k, map.n, yo, false, &xs);
+        }
         ctx.tr_flag = ctx.stage_read(xs.ovf, 1);
         const double* v = map.v;
         const index_t kk = k, nn = map.n;
@@ -1415,9 +1594,9 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       LPCA_LAUNCHED(ctx);
       pass_mark(ctx, 1);
     }
-    ev.mark(7);
+    if (!y_copied) ev.mark(7);
     ctx.pass_slot = -1;
-    if (y_location == LPCA_HOST) {
+    if (y_location == LPCA_HOST && !y_copied) {
       LPCA_CUDA(cudaMemcpyAsync(y, ydev, ybytes, cudaMemcpyDeviceToHost, ctx.stream));
       if (d2h) *d2h += static_cast<double>(ybytes);
     }
@@ -1870,6 +2049,12 @@ lpca_status lpca_ctx_destroy(lpca_ctx* ctx) {
       if (e) cudaEventDestroy(e);
     if (ctx->comm) nccl().comm_destroy(ctx->comm);
     if (ctx->pin) cudaFreeHost(ctx->pin);
+    if (ctx->copy_stream) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (auto& pool : ctx->chunk_ev)
+      for (cudaEvent_t e : pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -1987,11 +2172,14 @@ lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_vi
     if (!cfg || !out_map) throw Error(kInvalidArgument, "null argument");
     *out_map = nullptr;
     PhaseEvents ev(*ctx);
+    CopyScope copies(*ctx);
     ev.mark(9);
     double h2d = 0.0;
-    const DevX dx = stage_x(*ctx, x, "x", &h2d);
-    ev.mark(10);
-    if ((cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP) {
+    const bool streamed = (cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP;
+    // in-core fits take a host X chunk by chunk (the sketch overlaps the copy)
+    const DevX dx = streamed ? stage_x(*ctx, x, "x", &h2d) : stage_x_arriving(*ctx, x, "x", &h2d, ctx->ev[9], ctx->ev[10]);
+    if (streamed) ev.mark(10);
+    if (streamed) {
       // reduce() with block_rows: the streaming reducer over row slices (reducer.cpp:340-346)
       if (cfg->block_rows < 1) throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
       SliceSource src(dx, cfg->block_rows);
@@ -2001,6 +2189,7 @@ lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_vi
       c.block_rows = 0;
       c.streaming = 0;
       *out_map = fit_dev(*ctx, c, dx, timings);
+      ctx->wait_arrivals();  // RP reads no X
     }
     if (timings) timings->h2d += ev.secs(9, 10);
   });
@@ -2041,12 +2230,15 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
     if (!cfg || !out_map) throw Error(kInvalidArgument, "null argument");
     *out_map = nullptr;
     PhaseEvents ev(*ctx);
+    CopyScope copies(*ctx);
     ev.mark(9);
-    const DevX dx = stage_x(*ctx, x, "x", nullptr);
-    ev.mark(10);
+    const bool streamed = (cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP;
+    const DevX dx = streamed ? stage_x(*ctx, x, "x", nullptr)
+                             : stage_x_arriving(*ctx, x, "x", nullptr, ctx->ev[9], ctx->ev[10]);
+    if (streamed) ev.mark(10);
     lpca_map* map = nullptr;
     bool fused = false;
-    if ((cfg->block_rows > 0 || cfg->streaming) && cfg->method != LPCA_RP) {
+    if (streamed) {
       if (cfg->block_rows < 1) throw Error(kInvalidArgument, "reducer: streaming mode needs block_rows >= 1");
       SliceSource src(dx, cfg->block_rows);
       map = fit_stream_dev(*ctx, *cfg, src, timings);
@@ -2061,6 +2253,7 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
         fused = true;
       };
       map = fit_dev(*ctx, c, dx, timings, &tr);
+      ctx->wait_arrivals();  // RP reads no X before its transform
     }
     try {
       if (fused)

@@ -431,22 +431,33 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   if (kHalf && kMode == kXTU && a.scan && a.run_stages > a.stages)
     throw Error(kInternal, "tc pair: a scanned U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + (kMaxEpiWarps + 3) * 4 * a.npad +
-                      kRscRing * 4 * kBM;  // red, gsc, xbuf
+                      kRscRing * 4 * kBM + 2 * 4 * kBM;  // red, gsc, xbuf, xrow
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int pairs = a.items < num_sms / 2 ? a.items : num_sms / 2;
   if constexpr (kMode == kXW) {
-    if (a.npad > 168) {
-      LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    // wide slices: 8 epilogue warps. LPCA_TC_CONV=8 (8 converters, fp16 with
+    // quarter A slots) or 84 (8 converters, 4 epilogue warps): the MMA's wait
+    // for converted A falls 39% -> 20% of its time, but at configs[2]'s
+    // power-capped clocks the passes do not get faster, so 4
+    // converters stay the default
+    const int conv = kHalf && a.half_slots == 4 ? env_int("LPCA_TC_CONV", 4) : 4;
+    auto go = [&](auto kern, int threads) {
+      LPCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       if (ev_pre) LPCA_CUDA(cudaEventRecord(ev_pre, s));
-      tc2_kernel<kMode, kHalf, 8><<<2 * pairs, pair_threads(8), smem, s>>>(tx, th, tl, a);
+      kern<<<2 * pairs, threads, smem, s>>>(tx, th, tl, a);
       if (ev_post) LPCA_CUDA(cudaEventRecord(ev_post, s));
-      return;
+    };
+    if (a.npad > 168) {
+      if constexpr (kHalf) {
+        if (conv == 8) return go(tc2_kernel<kMode, kHalf, 8, 8>, pair_threads(8, 8));
+        if (conv == 84) return go(tc2_kernel<kMode, kHalf, 4, 8>, pair_threads(8, 4));
+      }
+      return go(tc2_kernel<kMode, kHalf, 8, 4>, pair_threads(4, 8));
     }
   }
   if (ev_pre) LPCA_CUDA(cudaEventRecord(ev_pre, s));
-  tc2_kernel<kMode, kHalf, 4><<<2 * pairs, pair_threads(4), smem, s>>>(tx, th, tl, a);
+  tc2_kernel<kMode, kHalf, 4><<<2 * pairs, pair_threads(4, 4), smem, s>>>(tx, th, tl, a);
   if (ev_post) LPCA_CUDA(cudaEventRecord(ev_post, s));
 }
 

@@ -315,8 +315,13 @@ __device__ __forceinline__ void pair_item_coords(const PairArgs& a, int item, in
 // 15% to 6% at configs[2]). Otherwise one per quadrant: X^T U's converters need
 // the registers (at 448 threads ptxas caps them at 128 and the column-wise
 // transposing loads spill), and narrow slices have two run buffers anyway.
-constexpr int pair_threads(int epi) {
-  return 32 * (6 + epi);  // TMA, MMA, 4 converters, the epilogue
+// Converter warps: one per TMEM lane quadrant, or (LPCA_TC_CONV, wide fp16 X W
+// slices with quarter A slots) two, each converting one 32-column half of every
+// stage, so one warp's split overlaps the other's TMEM-store and hand-off
+// latency. The MMA's wait for converted A falls from 39% to 20% of its time at
+// configs[2], but the power-capped passes are no faster, so one is the default.
+constexpr int pair_threads(int conv, int epi) {
+  return 32 * (2 + conv + epi);  // TMA, MMA, converters, the epilogue
 }
 constexpr int kMaxEpiWarps = 8;
 template <int kEpi>
@@ -334,8 +339,8 @@ __device__ unsigned long long g_pair_prof[2][16];  // [mode][counter]
 #define PP_ADD(k)
 #endif
 
-template <int kMode, bool kHalf, int kEpi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 1)
+template <int kMode, bool kHalf, int kEpi, int kConv = 4>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kConv, kEpi), 1)
     tc2_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmbh,
                const __grid_constant__ CUtensorMap tmbl, PairArgs a) {
   constexpr int BK = kHalf ? 64 : 32;  // K per stage (one 128 B swizzle row of B)
@@ -363,6 +368,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [kEpiWarps][npad] epilogue block maxima / run scales
   float* rsc = red + (kMaxEpiWarps + 1) * a.npad;  // after red + gsc [npad]: [kRscRing runs][128] inverse A-row scales
   float* xbuf = rsc + kRscRing * kBM;  // [2][npad] the peer's column maxima (written by the peer)
+  float* xrow = xbuf + 2 * a.npad;     // [2][128] row maxima of the two converter halves (8 converters)
+  static_assert(kConv == 4 || (kConv == 8 && kMode == kXW && kHalf), "8 converters: fp16 X W only");
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t a_col0 = static_cast<uint32_t>((a.nrb + 1) * a.npad);
@@ -530,9 +537,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
         }
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + kConv) {
     // ---------------- converters (both CTAs): smem X -> own TMEM A ----------------
     const int q = warp & 3;
+    const int hsel = kConv == 8 ? (warp - 2) >> 2 : 0;  // 8 converters: this warp's 32-column half
+    // 8 converters: a row's maximum over both halves (the two warps of a quadrant)
+    auto row_max_both = [&](float mine) {
+      xrow[hsel * kBM + q * 32 + lane] = mine;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      const float m = fmaxf(xrow[q * 32 + lane], xrow[kBM + q * 32 + lane]);
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      return m;
+    };
     const int i = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     float xmax = 0.0f;
@@ -592,17 +608,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
             const uint8_t* xt = smem + st * stage_bytes;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+              if (kConv == 8 && h != hsel) continue;
               float v[32];
               load_row(xt, h, v);
               mx = fmaxf(mx, absmax32(v));
             }
             ring_advance(st, ph, S);
           }
-          sx = pow2_scale_x(mx, 1.0f);
-          rsc[(rc % kRscRing) * kBM + i] = __frcp_rn(sx);
           xmax = fmaxf(xmax, mx);
+          if (kConv == 8) mx = row_max_both(mx);
+          sx = pow2_scale_x(mx, 1.0f);
+          if (hsel == 0) rsc[(rc % kRscRing) * kBM + i] = __frcp_rn(sx);
         }
         for (int j = 0; j < nst; ++j) {
+          if constexpr (kConv == 8) {
+            // one 32-column half of the stage -> its two quarter slots
+            mbar_wait(&full_x[stage], phase, 4);
+            const uint8_t* xt = smem + stage * stage_bytes;
+            float v[32];
+            load_row(xt, hsel, v);
+            if (a.scan == 2 || (a.xmax_out && a.scan == 0)) {
+              const float mh = absmax32k(v);
+              if (a.xmax_out) xmax = fmaxf(xmax, mh);
+              if (a.scan == 2) {
+                if (j == 0) {  // the run's scale: 16x headroom over its first stage (both halves)
+                  sx = pow2_scale_x(row_max_both(mh), 16.0f);
+                  if (hsel == 0) rsc[(rc % kRscRing) * kBM + i] = __frcp_rn(sx);
+                } else if (mh * sx >= 32768.0f || (mh > 0.0f && mh * sx < 0.125f)) {
+                  ovf = true;
+                }
+              }
+            }
+            if (__any_sync(0xffffffffu, sx != 1.0f)) {
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) v[kk] *= sx;
+            }
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              if ((qq >> 1) == hsel) {
+                float h8[8], l8[8];
+                split_f16_16(v + 16 * (qq & 1), h8, l8);
+                mbar_wait(&aempty[aslot], aphase ^ 1, 4);
+                tc_fence_after();
+                const uint32_t aq = lane_base + a_col0 + static_cast<uint32_t>(aslot * 16);
+                tmem_st8(aq, h8);
+                tmem_st8(aq + 8, l8);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&conv[aslot]), 0));
+              }
+              ring_advance(aslot, aphase, AS);
+            }
+            ring_advance(stage, phase, S);
+            continue;
+          }
           {
             PP_T0();
             mbar_wait(&full_x[stage], phase, 4);
@@ -743,7 +803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kEpi), 
   } else {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
     const int q = warp & 3;                       // TMEM lane quadrant
-    const int ew = warp - 6;                      // epilogue warp 0 .. kEpiWarps - 1
+    const int ew = warp - 2 - kConv;              // epilogue warp 0 .. kEpiWarps - 1
     const int nch16 = a.npad / 16;                // this warp's 16-column chunks: one half of them
     const int half = ew / 4;
     const int c_lo = kEpiWarps == 4 ? 0 : (half ? (nch16 + 1) / 2 : 0) * 16;

@@ -118,3 +118,35 @@ def test_sketch_overflow_in_a_later_stage_reruns_before_host_checks(ctx, q):
     v64, s64, _ = O.reduce_lazy_spca(x.astype(np.float64), 16, 32, 3, power_iters=q)
     assert np.all(np.isfinite(got.singular_values))
     assert np.max(np.abs(got.singular_values - s64) / s64) < 1e-4
+
+
+@pytest.mark.parametrize("conv", ["8", "84"])
+def test_eight_converter_warps_bit_identical(ctx, monkeypatch, conv):
+    """LPCA_TC_CONV=8 / 84 (two converter warps per TMEM lane quadrant, each one
+    32-column half of every stage; csrc/tc_pair.cuh) writes the same fp16 A
+    planes with the same run scales as the default four, so fits, power steps,
+    transforms and the scanned rerun are bit-identical."""
+    import torch
+    x = _x(9000, 2048, 300, 0.98)
+    rng = np.random.default_rng(8)
+    xa = rng.standard_normal((8192, 1024)).astype(np.float32) * 1e-3
+    for c0 in range(0, 1024, 128):   # zero first stages, huge late entries: the scanned rerun
+        xa[:, c0:c0 + 64] = 0.0
+    xa[::97, 1000] = 0.5
+    xa = torch.from_numpy(xa).cuda()
+
+    def run():
+        out = []
+        for xx, k, l, q in ((x, 200, 220, 1), (xa, 150, 220, 0)):
+            cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=k, l=l, power_iters=q,
+                                   projection=lp.ProjectionSpec(seed=7))
+            y = torch.empty((xx.shape[0], k), dtype=torch.float32, device="cuda")
+            mp, _ = lp.fit_transform(xx, cfg, ctx=ctx, out=y)
+            out += [mp.singular_values, mp.v, y.cpu().numpy()]
+        return out
+
+    base = run()
+    monkeypatch.setenv("LPCA_TC_CONV", conv)
+    got = run()
+    for a, b in zip(base, got):
+        assert np.array_equal(a, b)

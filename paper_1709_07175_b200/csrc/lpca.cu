@@ -565,11 +565,12 @@ DevX stage_x_arriving(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
         LPCA_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + es * r0 * d.n, es * d.n,
                                     static_cast<const char*>(x->data) + es * r0 * ld, es * ld, es * d.n, r1 - r0,
                                     cudaMemcpyHostToDevice, cs));
-        const cudaEvent_t e = ctx.chunk_event(0, i);
+        // the last chunk's event is `done` itself: whoever waits for all of X
+        // has also waited for the event the h2d timing reads
+        const cudaEvent_t e = r1 == d.m ? done : ctx.chunk_event(0, i);
         LPCA_CUDA(cudaEventRecord(e, cs));
         ctx.arrivals.emplace_back(r1, e);
       }
-      LPCA_CUDA(cudaEventRecord(done, cs));
       if (h2d_bytes) *h2d_bytes += static_cast<double>(es * d.m * d.n);
       d.p = dst;
       return d;
@@ -2191,7 +2192,10 @@ lpca_status lpca_fit(lpca_ctx* ctx, const lpca_config* cfg, const lpca_matrix_vi
       *out_map = fit_dev(*ctx, c, dx, timings);
       ctx->wait_arrivals();  // RP reads no X
     }
-    if (timings) timings->h2d += ev.secs(9, 10);
+    if (timings) {
+      LPCA_CUDA(cudaEventSynchronize(ctx->ev[10]));  // (recorded on the copy stream for a chunked X)
+      timings->h2d += ev.secs(9, 10);
+    }
   });
 }
 
@@ -2218,7 +2222,10 @@ lpca_status lpca_transform(lpca_ctx* ctx, const lpca_map* map, const lpca_matrix
     const DevX dx = stage_x(*ctx, x, "x", nullptr);
     ev.mark(10);
     transform_dev(*ctx, *map, dx, y, y_dtype, y_layout, y_location, ldy, timings, nullptr);
-    if (timings) timings->h2d += ev.secs(9, 10);
+    if (timings) {
+      LPCA_CUDA(cudaEventSynchronize(ctx->ev[10]));  // (recorded on the copy stream for a chunked X)
+      timings->h2d += ev.secs(9, 10);
+    }
   });
 }
 
@@ -2264,7 +2271,10 @@ lpca_status lpca_fit_transform(lpca_ctx* ctx, const lpca_config* cfg, const lpca
       delete map;
       throw;
     }
-    if (timings) timings->h2d += ev.secs(9, 10);
+    if (timings) {
+      LPCA_CUDA(cudaEventSynchronize(ctx->ev[10]));  // (recorded on the copy stream for a chunked X)
+      timings->h2d += ev.secs(9, 10);
+    }
     *out_map = map;
   });
 }

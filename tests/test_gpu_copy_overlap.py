@@ -61,6 +61,10 @@ def test_chunked_fit_only_and_timings(ctx, monkeypatch):
     t = lp.ReducerTimings()
     a = lp.reduce(xh, cfg, timings=t, ctx=ctx)
     assert t.h2d > 0.0 and t.sketch_pass > 0.0
+    # RP reads no X: its timings still wait for the upload's last chunk
+    t_rp = lp.ReducerTimings()
+    lp.reduce(xh, lp.ReducerConfig(method=M.rp, k=10, l=10), timings=t_rp, ctx=ctx)
+    assert t_rp.h2d > 0.0
     monkeypatch.setenv("LPCA_H2D_CHUNKS", "0")
     b = lp.reduce(xh, cfg, ctx=ctx)
     assert np.array_equal(a.v, b.v) and np.array_equal(a.singular_values, b.singular_values)

@@ -149,6 +149,16 @@ int64_t lpca_ctx_launch_count(const lpca_ctx* ctx);
  * returns how many bands were overwritten (names, space-separated, into
  * `names`), or -1 when guards are off, -2 on a CUDA error. */
 int64_t lpca_debug_check_guards(lpca_ctx* ctx, char* names, int64_t capacity);
+/* Debugging aid (host only, no device): the row gather's entry schedule for a
+ * very sparse Omega given as column lists (cols[c * cap + i] = j | sign << 31,
+ * cnt[c] entries): out receives [warp][smax / 2][32] words of two 16-bit
+ * entries (word index | sign << 15; idle lanes read zero words at index
+ * round_up(n, 32) + bank); warp = part * ceil(l / 32) + column group, where a
+ * row's entries are split by j into *splits parts. Returns the longest warp
+ * schedule (steps), or -1 if infeasible or out_capacity is short (*smax = the
+ * steps the kernel unrolls, *splits = 1 or 2; both 0 on failure). */
+int32_t lpca_debug_row_schedule(const int32_t* cnt, const uint32_t* cols, int32_t cap, int64_t n, int64_t l,
+                                uint32_t* out, int64_t out_capacity, int32_t* smax, int32_t* splits);
 
 /* ---- configuration ------------------------------------------------------ */
 /* ReducerConfig::resolved (proj/core/src/reducer.cpp:137-161). */

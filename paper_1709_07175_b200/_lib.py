@@ -81,6 +81,7 @@ SIGNATURES = {
     "lpca_ctx_create_dist": (I32, [I32, I32, I32, P, PP]),
     "lpca_ctx_create_hooked": (I32, [I32, I32, I32, P, P, PP]),
     "lpca_debug_check_guards": (I64, [P, P, I64]),
+    "lpca_debug_row_schedule": (I32, [P, P, I32, I64, I64, P, I64, P, P]),
     "lpca_ctx_destroy": (I32, [P]),
     "lpca_ctx_set_stream": (I32, [P, P]),
     "lpca_ctx_synchronize": (I32, [P]),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -238,6 +239,18 @@ void launch_sparse_sketch(cudaStream_t s, const T* x, index_t m, index_t n, inde
                           const std::uint32_t* ent, index_t l, T* u, index_t ldu, std::uint32_t* xmax, int num_sms);
 void launch_u_planes_f16(cudaStream_t s, const float* u, index_t m, index_t ld, index_t npad, __half* hi, __half* lo,
                          index_t ldt, float* uinv);
+// Row gather for fp32 X (lanes = Omega columns, rows by 1-D bulk copies, a
+// bank-conflict-free entry schedule per warp from an edge colouring):
+// column lists (device), the schedule (host, packed [warp][smax/2][32] 2x16-bit
+// entries; returns the steps, -1 if infeasible), the launch.
+bool row_gather_feasible(index_t m, index_t n, index_t ldx, index_t l);
+void launch_omega_col_lists(cudaStream_t s, const double* omega, index_t n, index_t l, int cap, int* cnt,
+                            std::uint32_t* cols);
+int build_row_schedule(const int* cnt, const std::uint32_t* cols, int cap, index_t n, index_t l,
+                       std::vector<std::uint32_t>& packed, int* smax_out, int* splits_out);
+void launch_sparse_sketch_rows(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
+                               const std::uint32_t* sched, int steps, int smax, int splits, index_t l, float* u,
+                               index_t ldu, std::uint32_t* xmax, int num_sms);
 // C = op(A) op(B) + beta C, l x l column-major (op = transpose when ta / tb; b null = identity).
 void launch_small_gemm(cudaStream_t s, int ta, int tb, index_t l, const double* a, const double* b, double* c,
                        double beta);

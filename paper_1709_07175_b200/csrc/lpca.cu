@@ -148,6 +148,10 @@ struct lpca_ctx {
   // fp16 sketch consumes the chunks as they land (xw_pass); every other reader
   // of X waits for all of them first (wait_arrivals). The transform's Y comes
   // back the same way, chunk by chunk behind the transform's launches.
+  // the row-gather schedule of the last very sparse Omega (sparse_omega.cu),
+  // keyed by what determines Omega; steps < 0: infeasible for that Omega
+  std::string row_sched_key;
+  int row_sched_steps = -1, row_sched_smax = 0, row_sched_splits = 1;
   cudaStream_t copy_stream = nullptr;
   std::vector<std::pair<index_t, cudaEvent_t>> arrivals;
   std::vector<cudaEvent_t> chunk_ev[2];  // [0] H2D chunks, [1] D2H chunks
@@ -630,17 +634,12 @@ struct XScale {
   int* ovf = nullptr;         // scanless per-run scales: flags runs that need the scan
 };
 
-// Very sparse Omega on dense X: 0 = always the dense passes, 1 = always the
-// gather sketch, default: the gather when the dense pass is not the tcgen05 one
-// (fp64 X, the SIMT path). On fp32 X the 2-SM pass with the zero lo plane of a
-// {-1, 0, +1} Omega skipped wins (configs[3] slice at 200k rows: 5.4 ms against
-// 8.2 ms for the gather, which is latency-bound at a quarter of HBM).
-int sparse_omega_mode() {
-  static const int mode = [] {
-    const char* e = getenv("LPCA_SPARSE_OMEGA");
-    return e && e[0] == '0' ? 0 : (e && e[0] == '1' ? 1 : 2);
-  }();
-  return mode;
+// Very sparse Omega on dense X: 0 = always the dense passes, 1 = always a
+// gather sketch, default: a gather (fp32: the row gather when its schedule
+// fits, else the dense pass; fp64 and the SIMT path: the chunk gather).
+int sparse_omega_mode() {  // read per fit (tests switch it)
+  const char* e = getenv("LPCA_SPARSE_OMEGA");
+  return e && e[0] == '0' ? 0 : (e && e[0] == '1' ? 1 : 2);
 }
 
 bool f16_enabled() {
@@ -1179,6 +1178,41 @@ struct FitResult {
 // it gets the map (V ready on the stream) and the device max|X| of the fit.
 using AfterSpectral = std::function<void(lpca_map&, const uint32_t*)>;
 
+// The row gather's schedule for this very sparse Omega (cached on the context:
+// a fit's Omega is fixed by n, l, density and seed). Builds it from Omega's
+// column lists (one small device-to-host copy and a host edge colouring, once
+// per Omega); false when some column or bank has more than 192 entries.
+bool row_schedule(lpca_ctx& ctx, const lpca_config& c, const double* omega, index_t n, index_t l) {
+  char key[160];
+  std::snprintf(key, sizeof key, "%lld/%lld/%.17g/%llu", static_cast<long long>(n), static_cast<long long>(l),
+                c.density, static_cast<unsigned long long>(c.seed));
+  if (ctx.row_sched_key == key) return ctx.row_sched_steps > 0;
+  constexpr int cap = 193;  // one past the longest schedule
+  int* cnt = ctx.get<int>("so.cnt", l);
+  auto* cols = ctx.get<std::uint32_t>("so.cols", l * cap);
+  launch_omega_col_lists(ctx.stream, omega, n, l, cap, cnt, cols);
+  LPCA_LAUNCHED(ctx);
+  std::vector<int> hc(static_cast<size_t>(l));
+  std::vector<std::uint32_t> hl(static_cast<size_t>(l) * cap);
+  LPCA_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * l, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaMemcpyAsync(hl.data(), cols, sizeof(std::uint32_t) * l * cap, cudaMemcpyDeviceToHost, ctx.stream));
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::vector<std::uint32_t> packed;
+  int smax = 0, splits = 1;
+  const int steps = build_row_schedule(hc.data(), hl.data(), cap, n, l, packed, &smax, &splits);
+  if (steps > 0) {
+    void* d = ctx.buf("so.rows", packed.size() * sizeof(std::uint32_t));
+    LPCA_CUDA(cudaMemcpyAsync(d, packed.data(), packed.size() * sizeof(std::uint32_t), cudaMemcpyHostToDevice,
+                              ctx.stream));
+    LPCA_CUDA(cudaStreamSynchronize(ctx.stream));  // packed dies here
+  }
+  ctx.row_sched_key = key;
+  ctx.row_sched_steps = steps;
+  ctx.row_sched_smax = smax;
+  ctx.row_sched_splits = splits;
+  return steps > 0;
+}
+
 lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_timings* t,
                   const AfterSpectral* after_spectral = nullptr) {
   // Ranks first agree on the shape (one small collective), so a rank-specific
@@ -1261,17 +1295,36 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     // one read of X, the reference's summation order) where the dense pass
     // would be DMMA or SIMT (sparse_omega_mode)
     const int so_mode = sparse_omega_mode();
-    const bool gather = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && u.ld <= 512 &&
-                        (so_mode == 1 || (so_mode == 2 && !tc));
+    const bool very_sparse = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && so_mode != 0;
+    // fp32: the row gather (lanes = Omega columns, a bank-conflict-free schedule)
+    const bool rows = very_sparse && x.dtype == 4 && row_gather_feasible(m, n, x.ld, l) &&
+                      row_schedule(ctx, c, omega, n, l);
+    const bool gather = very_sparse && !rows && u.ld <= 512 && (so_mode == 1 || !tc);
     int* xovf = nullptr;
-    if (f16 && !ctx.force_scan && !gather) {  // scales from each run's first stage (rerun with the scan if flagged)
+    if (f16 && !ctx.force_scan && !gather && !rows) {  // scales from each run's first stage (rerun with the scan if flagged)
       xovf = ctx.get<int>("xovf", 1);
       launch_zero(ctx.stream, xovf, sizeof(int));
       sketch.ovf = xovf;
     }
     ev.mark(12);
     ev.mark(13);
-    if (gather) {
+    if (rows) {
+      ctx.wait_arrivals();
+      float* up = u.plain ? static_cast<float*>(u.plain) : ctx.get<float>("u.gather", mm * u.ld);
+      launch_sparse_sketch_rows(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld,
+                                static_cast<const std::uint32_t*>(ctx.buf("so.rows", 4)), ctx.row_sched_steps,
+                                ctx.row_sched_smax, ctx.row_sched_splits, l, up, u.ld, f16 ? xs.dev : nullptr,
+                                ctx.num_sms);
+      LPCA_LAUNCHED(ctx);
+      if (f16) {
+        launch_u_planes_f16(ctx.stream, up, m, u.ld, u.ld, u.h16hi, u.h16lo, u.ldt16, u.uinv);
+        ctx.note_launch();
+      } else if (u.hi && m > 0) {
+        launch_split_tf32_transpose(ctx.stream, up, m, l, u.ld, u.hi, u.lo, u.ldt);
+        ctx.note_launch();
+      }
+      ev.mark(13);
+    } else if (gather) {
       ctx.wait_arrivals();
       const index_t nch = sparse_sketch_chunks(n, x.dtype);
       int* counts = ctx.get<int>("so.counts", nch * l);
@@ -2066,6 +2119,25 @@ lpca_status lpca_ctx_set_stream(lpca_ctx* ctx, void* cuda_stream) {
     check_ctx(ctx);
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
   });
+}
+
+int32_t lpca_debug_row_schedule(const int32_t* cnt, const uint32_t* cols, int32_t cap, int64_t n, int64_t l,
+                                uint32_t* out, int64_t out_capacity, int32_t* smax, int32_t* splits) {
+  if (smax) *smax = 0;
+  if (splits) *splits = 0;
+  if (!cnt || !cols || !out || !smax || !splits || cap < 1 || n < 1 || l < 1) return -1;
+  try {
+    std::vector<std::uint32_t> packed;
+    int sm = 0, sp = 0;
+    const int steps = build_row_schedule(cnt, cols, cap, n, l, packed, &sm, &sp);
+    if (steps < 0 || static_cast<int64_t>(packed.size()) > out_capacity) return -1;
+    std::copy(packed.begin(), packed.end(), out);
+    *smax = sm;
+    *splits = sp;
+    return steps;
+  } catch (...) {
+    return -1;
+  }
 }
 
 int64_t lpca_debug_check_guards(lpca_ctx* ctx, char* names, int64_t capacity) {

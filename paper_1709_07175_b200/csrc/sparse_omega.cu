@@ -27,10 +27,13 @@
 // (lpca.cu sparse_omega_mode).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
+#include "tc_util.cuh"
 
 namespace lpca {
 namespace {
@@ -336,6 +339,161 @@ __global__ void __launch_bounds__(kUScaleRows) u_planes_f16_kernel(const float* 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Row gather for fp32 X (sparse_sketch_rows_kernel): lanes are Omega columns.
+// Each CTA streams whole rows of X into a ring of shared-memory slots with
+// 1-D bulk copies (TMA engine, no register staging), and every warp sums its
+// 32 columns' entries of the row: lane c adds +-x[j] for the j of column c.
+// The order of each lane's entries is a precomputed schedule (host edge
+// colouring, build_row_schedule): at every step the 32 lanes of a warp read 32
+// different banks, so each step is one shared-memory wavefront. A step's idle
+// lanes read zeros from a free bank. Entries are 16 bits (word index | sign <<
+// 15), two per register, the whole row's schedule held in registers. fp32 sums
+// in the schedule's order (fp32 X only: the fp64 path keeps the reference's
+// ascending order, sparse_sketch_kernel).
+
+// cols[c * cap + i]: the i-th nonzero of Omega column c, j | (sign << 31), j
+// ascending; cnt[c] = the column's nonzeros (entries past cap are dropped).
+__global__ void omega_col_lists_kernel(const double* __restrict__ omega, index_t n, index_t l, int cap,
+                                       int* __restrict__ cnt, std::uint32_t* __restrict__ cols) {
+  const index_t c = static_cast<index_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c >= l) return;
+  int k = 0;
+  for (index_t j0 = 0; j0 < n; j0 += 32) {
+    const index_t j = j0 + lane;
+    const double w = j < n ? omega[c * n + j] : 0.0;
+    const unsigned nz = __ballot_sync(0xffffffffu, w != 0.0);
+    const int pos = k + __popc(nz & ((1u << lane) - 1u));
+    if (w != 0.0 && pos < cap) cols[c * cap + pos] = static_cast<std::uint32_t>(j) | (w < 0.0 ? 0x80000000u : 0u);
+    k += __popc(nz);
+  }
+  if (lane == 0) cnt[c] = k;
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+// The schedule takes SMAX / 2 registers per thread, which bounds the CTA: P = 2
+// splits each row's entries by j into two halves run by separate warps (twice
+// the warps to hide the loads' latency; the halves' sums meet in shared memory).
+constexpr int rows_max_threads(int smax, int splits) {
+  return splits == 2 ? (smax <= 64 ? 768 : 640) : (smax > 128 ? 320 : 512);
+}
+
+template <int SMAX, int P>
+__global__ void __launch_bounds__(rows_max_threads(SMAX, P), 1)
+    sparse_sketch_rows_kernel(const float* __restrict__ x, index_t m, int n, index_t ldx,
+                              const std::uint32_t* __restrict__ sched, int steps, int slot_floats, int ring, int l,
+                              float* __restrict__ u, index_t ldu, std::uint32_t* xmax) {
+  extern __shared__ __align__(128) unsigned char rows_smem[];
+  float* slots = reinterpret_cast<float*>(rows_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + static_cast<size_t>(ring) * slot_floats);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wps = static_cast<int>(blockDim.x >> 5) / P;  // column warps per split
+  const int part = warp / wps;                             // which half of j this warp sums
+  const int col = (warp % wps) * 32 + lane;
+  float* red = reinterpret_cast<float*>(full + 4);  // [2][wps * 32]: the second half's sums, by row parity
+  // the whole row's schedule of this lane, two 16-bit entries per register
+  std::uint32_t e[SMAX / 2];
+#pragma unroll
+  for (int i = 0; i < SMAX / 2; ++i) e[i] = __ldg(sched + (static_cast<size_t>(warp) * (SMAX / 2) + i) * 32 + lane);
+  for (int r = 0; r < ring; ++r)
+    for (int j = n + threadIdx.x; j < slot_floats; j += blockDim.x) slots[static_cast<size_t>(r) * slot_floats + j] = 0.f;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < ring; ++r) tc::mbar_init(&full[r], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  const uint32_t row_bytes = static_cast<uint32_t>(n) * 4u;
+  if (threadIdx.x == 0)
+    for (int r = 0; r < ring; ++r) {
+      const index_t row = blockIdx.x + static_cast<index_t>(r) * gridDim.x;
+      if (row < m) {
+        tc::mbar_expect_tx(&full[r], row_bytes);
+        bulk_load(slots + static_cast<size_t>(r) * slot_floats, x + row * ldx, row_bytes, &full[r]);
+      }
+    }
+  float amax = 0.f;
+  int slot = 0, par = 0;
+  uint32_t phase = 0;
+  for (index_t row = blockIdx.x; row < m; row += gridDim.x, par ^= 1) {
+    tc::mbar_wait(&full[slot], phase, 20);
+    const float* xs = slots + static_cast<size_t>(slot) * slot_floats;
+    const uint32_t xs_s = tc::smem_u32(xs);
+    if (xmax) {  // four independent maxima (a single chain exposes every load's latency)
+      float am[4] = {0.f, 0.f, 0.f, 0.f};
+      const int nv = n / 4;
+      int q = threadIdx.x;
+      for (; q + 3 * static_cast<int>(blockDim.x) < nv; q += 4 * blockDim.x) {
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[k].x), "=f"(v[k].y), "=f"(v[k].z), "=f"(v[k].w)
+                       : "r"(xs_s + 16u * (q + k * blockDim.x)));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          am[k] = fmaxf(am[k], fmaxf(fmaxf(fabsf(v[k].x), fabsf(v[k].y)), fmaxf(fabsf(v[k].z), fabsf(v[k].w))));
+      }
+      for (; q < nv; q += blockDim.x) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "r"(xs_s + 16u * q));
+        am[0] = fmaxf(am[0], fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+      amax = fmaxf(amax, fmaxf(fmaxf(am[0], am[1]), fmaxf(am[2], am[3])));
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int g = 0; g < SMAX / 16; ++g) {
+      if (16 * g < steps) {  // warp-uniform: the schedule's length
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const std::uint32_t w = e[8 * g + i];
+          asm volatile("ld.shared.f32 %0, [%2];\n ld.shared.f32 %1, [%3];"
+                       : "=f"(v[2 * i]), "=f"(v[2 * i + 1])
+                       : "r"(xs_s + ((w & 0x7fffu) << 2)), "r"(xs_s + (((w >> 16) & 0x7fffu) << 2)));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const std::uint32_t w = e[8 * g + i];
+          // the entry's sign flips the value's sign bit
+          acc[(2 * i) & 3] += __uint_as_float(__float_as_uint(v[2 * i]) ^ ((w << 16) & 0x80000000u));
+          acc[(2 * i + 1) & 3] += __uint_as_float(__float_as_uint(v[2 * i + 1]) ^ (w & 0x80000000u));
+        }
+      }
+    }
+    const float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (P == 2 && part == 1) red[par * wps * 32 + col] = sum;
+    __syncthreads();  // every warp is done with this slot (and the halves' sums are staged)
+    if (threadIdx.x == 0) {
+      const index_t next = row + static_cast<index_t>(ring) * gridDim.x;
+      if (next < m) {
+        tc::mbar_expect_tx(&full[slot], row_bytes);
+        bulk_load(slots + static_cast<size_t>(slot) * slot_floats, x + next * ldx, row_bytes, &full[slot]);
+      }
+    }
+    if (part == 0 && col < ldu)
+      u[row * ldu + col] = col < l ? (P == 2 ? sum + red[par * wps * 32 + col] : sum) : 0.f;
+    if (++slot == ring) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+  if (xmax) {
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) atomicMax(xmax, __float_as_uint(amax));
+  }
+}
+
 }  // namespace
 
 index_t sparse_sketch_chunks(index_t n, int dtype) {
@@ -388,6 +546,180 @@ void launch_u_planes_f16(cudaStream_t s, const float* u, index_t m, index_t ld, 
   if (m <= 0) return;
   const dim3 grid(static_cast<unsigned>((m + kUScaleRows - 1) / kUScaleRows), static_cast<unsigned>((npad + 31) / 32));
   u_planes_f16_kernel<<<grid, static_cast<unsigned>(kUScaleRows), 0, s>>>(u, m, ld, npad, hi, lo, ldt, uinv);
+}
+
+// ---- row gather: host schedule and launch -----------------------------------------
+
+namespace {
+constexpr int kRowSmemBudget = 200 * 1024;
+int row_slot_floats(index_t n) { return static_cast<int>(((n + 31) / 32) * 32 + 32); }
+}  // namespace
+
+int row_gather_ring(index_t n) {
+  const long long slot = 4LL * row_slot_floats(n);
+  const long long r = (kRowSmemBudget - 64 - 4096) / slot;  // (mbarriers, the halves' sums)
+  return static_cast<int>(r > 4 ? 4 : r);
+}
+
+bool row_gather_feasible(index_t m, index_t n, index_t ldx, index_t l) {
+  return m > 0 && n % 4 == 0 && ldx % 4 == 0 && l <= 512 && row_slot_floats(n) <= 32768 && row_gather_ring(n) >= 2;
+}
+
+
+void launch_omega_col_lists(cudaStream_t s, const double* omega, index_t n, index_t l, int cap, int* cnt,
+                            std::uint32_t* cols) {
+  const unsigned blocks = static_cast<unsigned>((l + 7) / 8);
+  omega_col_lists_kernel<<<blocks, 256, 0, s>>>(omega, n, l, cap, cnt, cols);
+}
+
+// One warp's bipartite multigraph (its 32 lanes = Omega columns x the 32 banks,
+// an edge per nonzero: lane c -> bank j % 32) edge-coloured with Delta = the
+// maximum degree colours (Koenig: bipartite multigraphs need no more), each
+// colour a step in which the lanes read 32 distinct banks; an edge whose two
+// ends have different first free colours a, b flips the a/b alternating path
+// from its bank end first. out[s * 32 + lane]: the 16-bit entry of step s.
+// Returns Delta, or -1 when it exceeds smax.
+int schedule_warp(const std::vector<std::vector<std::uint32_t>>& lanes, int zbase, int smax, std::uint16_t* out) {
+  int degl[32] = {}, degr[32] = {};
+  std::vector<std::pair<int, std::uint32_t>> edges;  // (lane, entry)
+  for (int c = 0; c < 32; ++c)
+    for (std::uint32_t v : lanes[c]) {
+      edges.emplace_back(c, v);
+      ++degl[c];
+      ++degr[(v & 0x7fffffffu) & 31u];
+    }
+  int delta = 0;
+  for (int i = 0; i < 32; ++i) delta = std::max(delta, std::max(degl[i], degr[i]));
+  if (delta > smax) return -1;
+  const int E = static_cast<int>(edges.size());
+  std::vector<int> at_l(32 * static_cast<size_t>(std::max(delta, 1)), -1), at_r(at_l.size(), -1), colour(E, -1);
+  auto L = [&](int e) { return edges[e].first; };
+  auto R = [&](int e) { return static_cast<int>((edges[e].second & 0x7fffffffu) & 31u); };
+  std::vector<int> path;
+  for (int e = 0; e < E; ++e) {
+    const int u = L(e), v = R(e);
+    int a = 0, b = 0;
+    while (at_l[u * delta + a] >= 0) ++a;
+    while (at_r[v * delta + b] >= 0) ++b;
+    if (at_r[v * delta + a] >= 0) {
+      // the a/b path from v: colour a at bank nodes, colour b at lane nodes
+      path.clear();
+      int node = v;
+      bool bank_side = true;
+      for (;;) {
+        const int f = bank_side ? at_r[node * delta + a] : at_l[node * delta + b];
+        if (f < 0) break;
+        path.push_back(f);
+        node = bank_side ? L(f) : R(f);
+        bank_side = !bank_side;
+      }
+      for (int f : path) {
+        at_l[L(f) * delta + colour[f]] = -1;
+        at_r[R(f) * delta + colour[f]] = -1;
+      }
+      for (int f : path) {
+        colour[f] = colour[f] == a ? b : a;
+        at_l[L(f) * delta + colour[f]] = f;
+        at_r[R(f) * delta + colour[f]] = f;
+      }
+    }
+    colour[e] = a;
+    at_l[u * delta + a] = e;
+    at_r[v * delta + a] = e;
+  }
+  for (int st = 0; st < smax; ++st) {
+    int freeb[32], nf = 0;
+    for (int b = 0; b < 32; ++b)
+      if (st >= delta || at_r[b * delta + st] < 0) freeb[nf++] = b;
+    int k = 0;
+    for (int c = 0; c < 32; ++c) {
+      const int f = st < delta ? at_l[c * delta + st] : -1;
+      std::uint32_t code;
+      if (f >= 0) {
+        const std::uint32_t v = edges[f].second;
+        code = (v & 0x7fffu) | ((v >> 31) << 15);
+      } else {
+        code = static_cast<std::uint32_t>(zbase + freeb[k++]);  // a zero word in a bank nobody reads now
+      }
+      out[static_cast<size_t>(st) * 32 + c] = static_cast<std::uint16_t>(code);
+    }
+  }
+  return delta;
+}
+
+int build_row_schedule(const int* cnt, const std::uint32_t* cols, int cap, index_t n, index_t l,
+                       std::vector<std::uint32_t>& packed, int* smax_out, int* splits_out) {
+  const int wps = static_cast<int>((l + 31) / 32);
+  const int zbase = row_slot_floats(n) - 32;
+  int need = 0;
+  for (index_t c = 0; c < l; ++c) {
+    if (cnt[c] > cap) return -1;
+    need = std::max(need, cnt[c]);
+  }
+  // most warps first (the loads' latency), then the shortest unroll that fits
+  // the schedule (bank degrees can exceed the column degrees)
+  const int cand[][2] = {{64, 2}, {96, 2}, {64, 1}, {128, 1}, {192, 1}};
+  for (const auto& cd : cand) {
+    const int smax = cd[0], P = cd[1];
+    if (wps * P * 32 > rows_max_threads(smax, P) || (P == 1 && need > smax)) continue;
+    const index_t half = ((n + 1) / 2 + 31) / 32 * 32;  // j < half: first part
+    const int warps = wps * P;
+    std::vector<std::uint16_t> steps(static_cast<size_t>(warps) * smax * 32);
+    int worst = 0;
+    bool ok = true;
+    for (int w = 0; w < warps && ok; ++w) {
+      const int part = w / wps, g = w % wps;
+      std::vector<std::vector<std::uint32_t>> lanes(32);
+      for (int c = 0; c < 32; ++c) {
+        const index_t col = static_cast<index_t>(g) * 32 + c;
+        if (col >= l) continue;
+        for (int i = 0; i < cnt[col]; ++i) {
+          const std::uint32_t v = cols[col * cap + i];
+          const index_t j = v & 0x7fffffffu;
+          if (P == 1 || (part == 0) == (j < half)) lanes[c].push_back(v);
+        }
+      }
+      const int d = schedule_warp(lanes, zbase, smax, steps.data() + static_cast<size_t>(w) * smax * 32);
+      if (d < 0) ok = false;
+      worst = std::max(worst, d);
+    }
+    if (!ok) continue;
+    packed.assign(static_cast<size_t>(warps) * (smax / 2) * 32, 0u);
+    for (int w = 0; w < warps; ++w)
+      for (int i = 0; i < smax / 2; ++i)
+        for (int c = 0; c < 32; ++c) {
+          const std::uint16_t* base = steps.data() + static_cast<size_t>(w) * smax * 32;
+          packed[(static_cast<size_t>(w) * (smax / 2) + i) * 32 + c] =
+              static_cast<std::uint32_t>(base[(2 * i) * 32 + c]) |
+              (static_cast<std::uint32_t>(base[(2 * i + 1) * 32 + c]) << 16);
+        }
+    *smax_out = smax;
+    *splits_out = P;
+    return worst;
+  }
+  return -1;
+}
+
+void launch_sparse_sketch_rows(cudaStream_t s, const float* x, index_t m, index_t n, index_t ldx,
+                               const std::uint32_t* sched, int steps, int smax, int splits, index_t l, float* u,
+                               index_t ldu, std::uint32_t* xmax, int num_sms) {
+  if (m <= 0) return;
+  if (ldu > ((l + 31) / 32) * 32) throw Error(kInternal, "row gather: ldu beyond the column warps");
+  const int slot = row_slot_floats(n), ring = row_gather_ring(n);
+  const int wps = static_cast<int>((l + 31) / 32);
+  const size_t smem = static_cast<size_t>(ring) * slot * 4 + 64 + 2 * 4 * 32 * static_cast<size_t>(wps);
+  const unsigned threads = static_cast<unsigned>(wps * 32 * splits);
+  const unsigned grid = static_cast<unsigned>(m < num_sms ? m : num_sms);
+  auto go = [&](auto kern) {
+    LPCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, threads, smem, s>>>(x, m, static_cast<int>(n), ldx, sched, steps, slot, ring, static_cast<int>(l), u,
+                                      ldu, xmax);
+  };
+  if (splits == 2 && smax == 64) go(sparse_sketch_rows_kernel<64, 2>);
+  else if (splits == 2) go(sparse_sketch_rows_kernel<96, 2>);
+  else if (smax == 64) go(sparse_sketch_rows_kernel<64, 1>);
+  else if (smax == 128) go(sparse_sketch_rows_kernel<128, 1>);
+  else go(sparse_sketch_rows_kernel<192, 1>);
 }
 
 template void launch_sparse_sketch<float>(cudaStream_t, const float*, index_t, index_t, index_t, const int*,

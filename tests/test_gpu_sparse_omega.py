@@ -40,23 +40,38 @@ def test_fp64_gather_sketch_matches_reference(ctx, ref, m, n, l, k, density):
     assert np.max(np.abs(sp.singular_values - rs2) / rs2) < 1e-10
 
 
-def test_fp32_gather_sketch_matches_reference_and_dense_path(ctx, ref, monkeypatch):
-    m, n, l, k, d = 20000, 4096, 110, 50, 1.0 / 64
+@pytest.mark.parametrize("n,mode,what", [
+    (4096, None, "row gather (default)"),
+    (4096, "0", "dense 2-SM pass, zero lo plane skipped"),
+    (4094, "1", "chunk gather (rows not 16-byte multiples)"),
+])
+def test_fp32_very_sparse_paths_match_reference(ctx, ref, monkeypatch, n, mode, what):
+    m, l, k, d = 20000, 110, 50, 1.0 / 64
     x = torch.empty((m, n), dtype=torch.float32, device="cuda")
     lp.synth_lowrank(x, 0, 200, 0.97, 0.01, 1000, ctx=ctx)
     rv, rs, _, _ = ref.reduce(2, x.cpu().numpy(), k, l, 11, kind=1, density=d)
-    # fp32 X takes the gather off the tcgen05 path (the SIMT passes), the
-    # dense 2-SM pass with the zero lo plane skipped on it (the default)
-    for path, tol in (("simt", 2e-5), ("tcgen05", 2e-5)):
-        ctx.set_gemm_path(path)
-        try:
-            got = lp.reduce_lazy_spca(x, _cfg(k, l, d), ctx=ctx)
-        finally:
-            ctx.set_gemm_path("tcgen05")
-        rel = np.abs(got.singular_values - rs) / rs
-        print(f"fp32 very sparse Omega, {path}: sigma rel {rel.max():.2e}")
-        assert rel.max() < tol   # fp32 sums of +-x (gather) / the fp16 split
-        assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+    if mode is not None:
+        monkeypatch.setenv("LPCA_SPARSE_OMEGA", mode)
+    got = lp.reduce_lazy_spca(x, _cfg(k, l, d), ctx=ctx)
+    rel = np.abs(got.singular_values - rs) / rs
+    print(f"fp32 very sparse Omega, {what}: sigma rel {rel.max():.2e}")
+    assert rel.max() < 2e-5   # fp32 sums of +-x (gathers) / the fp16 split
+    assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+
+
+def test_row_gather_configs3_shape_and_power(ctx, ref):
+    """configs[3] shape (n = 16,384, l = 300, density 1/128: a 166-step schedule)
+    with q = 2, against the reference's kernels composed (q >= 1 is unpinned by
+    the reference itself)."""
+    m, n, l, k, d = 6000, 16384, 300, 256, 1.0 / 128
+    x = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(x, 0, 400, 0.98, 0.01, 1000, ctx=ctx)
+    got = lp.reduce_lazy_spca(x, _cfg(k, l, d, q=2), ctx=ctx)
+    _, rv, rs, _ = ref.lazy_power_fit_transform(x.cpu().numpy(), k, l, 11, 2, kind=1, density=d, want_y=False)
+    rel = np.abs(got.singular_values - rs) / rs
+    print(f"configs[3] shape, row gather, q = 2: sigma rel {rel.max():.2e}")
+    assert rel.max() < 1e-4
+    assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-4
 
 
 def test_dense_pass_skips_zero_lo_plane_bitwise(tmp_path):

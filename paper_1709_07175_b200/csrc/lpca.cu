@@ -635,8 +635,12 @@ struct XScale {
 };
 
 // Very sparse Omega on dense X: 0 = always the dense passes, 1 = always a
-// gather sketch, default: a gather (fp32: the row gather when its schedule
-// fits, else the dense pass; fp64 and the SIMT path: the chunk gather).
+// gather sketch (fp32: the row gather when its schedule fits), default: the
+// row gather for fp32 rows longer than 8192 (configs[3]: 3.9 vs 5.4 ms per
+// 200k rows unthrottled, 58-61 vs 71-73 ms at full size power-capped; shorter
+// rows pay its per-row overhead: n = 4096, l = 110 at 400k rows 4.7 vs 1.2 ms
+// for the HBM-bound dense pass) and off the tcgen05 path; the chunk gather
+// for fp64 X and the SIMT path otherwise.
 int sparse_omega_mode() {  // read per fit (tests switch it)
   const char* e = getenv("LPCA_SPARSE_OMEGA");
   return e && e[0] == '0' ? 0 : (e && e[0] == '1' ? 1 : 2);
@@ -1297,8 +1301,8 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     const int so_mode = sparse_omega_mode();
     const bool very_sparse = c.projection_kind == LPCA_VERY_SPARSE && !x.sparse() && so_mode != 0;
     // fp32: the row gather (lanes = Omega columns, a bank-conflict-free schedule)
-    const bool rows = very_sparse && x.dtype == 4 && row_gather_feasible(m, n, x.ld, l) &&
-                      row_schedule(ctx, c, omega, n, l);
+    const bool rows = very_sparse && x.dtype == 4 && (so_mode == 1 || !tc || n > 8192) &&
+                      row_gather_feasible(m, n, x.ld, l) && row_schedule(ctx, c, omega, n, l);
     const bool gather = very_sparse && !rows && u.ld <= 512 && (so_mode == 1 || !tc);
     int* xovf = nullptr;
     if (f16 && !ctx.force_scan && !gather && !rows) {  // scales from each run's first stage (rerun with the scan if flagged)

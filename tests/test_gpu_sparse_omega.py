@@ -41,8 +41,8 @@ def test_fp64_gather_sketch_matches_reference(ctx, ref, m, n, l, k, density):
 
 
 @pytest.mark.parametrize("n,mode,what", [
-    (4096, None, "row gather (default)"),
-    (4096, "0", "dense 2-SM pass, zero lo plane skipped"),
+    (4096, "1", "row gather (forced)"),
+    (4096, None, "default for short rows: dense 2-SM pass, zero lo plane skipped"),
     (4094, "1", "chunk gather (rows not 16-byte multiples)"),
 ])
 def test_fp32_very_sparse_paths_match_reference(ctx, ref, monkeypatch, n, mode, what):
@@ -60,7 +60,8 @@ def test_fp32_very_sparse_paths_match_reference(ctx, ref, monkeypatch, n, mode, 
 
 
 def test_row_gather_configs3_shape_and_power(ctx, ref):
-    """configs[3] shape (n = 16,384, l = 300, density 1/128: a 166-step schedule)
+    """configs[3] shape (n = 16,384, l = 300, density 1/128: the row gather by
+    default, rows split in two parts of an 88-step schedule)
     with q = 2, against the reference's kernels composed (q >= 1 is unpinned by
     the reference itself)."""
     m, n, l, k, d = 6000, 16384, 300, 256, 1.0 / 128

@@ -21,10 +21,9 @@
 //
 // Measured (profiles/r02_c4_sparse_sketch.txt): about 1.6 TB/s, a quarter of
 // HBM; the walk is latency-bound (short lists per chunk and column, exposed
-// load latency at each chunk's barrier). On fp32 X the dense 2-SM tensor-core
-// pass is faster (two 152-wide slices, the zero lo plane of Omega skipped), so
-// the fit takes this kernel for fp64 X and off the tcgen05 path
-// (lpca.cu sparse_omega_mode).
+// load latency at each chunk's barrier). fp32 X takes the row gather below
+// (long rows) or the dense 2-SM pass (short rows), so the fit runs this kernel
+// for fp64 X (lpca.cu sparse_omega_mode).
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -275,8 +275,14 @@ def roofline(cfg, rows, esz, tm, steps, pk, config):
     n, k, l, q = cfg["n"], cfg["k"], cfg["l"], cfg["q"]
     npad = (l + 15) // 16 * 16
     up = 4 * npad * rows if esz == 4 else rows * l * 8          # U^T fp16 hi/lo planes (or U fp64)
+    # configs[3] on fp32 (n > 8192): the sketch is the row gather, an HBM-bound
+    # read of X (about n l density adds per row, no tensor work); U is written
+    # in fp32 and its fp16 planes made from it
+    gather = cfg.get("kind") == "very_sparse" and esz == 4 and n > 8192
+    sketch = (pass_roof(rows, n, 0, esz, tm.sketch_pass / steps, pk, 4 * npad * rows * 3) if gather else
+              pass_roof(rows, n, l, esz, tm.sketch_pass / steps, pk, up + 4 * npad * n))
     passes = {
-        "sketch": pass_roof(rows, n, l, esz, tm.sketch_pass / steps, pk, up + 4 * npad * n),
+        "sketch": sketch,
         "f": pass_roof(rows, n, l, esz, tm.f_pass / steps, pk, up),
         "transform": pass_roof(rows, n, k, esz, tm.transform_pass / steps, pk, rows * k * esz),
     }
@@ -292,13 +298,16 @@ def roofline(cfg, rows, esz, tm, steps, pk, config):
         achieved, peak, unit = sk["flops"] / (sk["ms"] * 1e-3) / 1e12, sk["flops"] / (sk["t_mma_ms"] * 1e-3) / 1e12, "TFLOP/s"
     else:
         achieved, peak, unit = sk["bytes"] / (sk["ms"] * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
-    kern = ("tc2_kernel<XW, fp16> (2-SM tcgen05, 3-term fp16 split)" if esz == 4
+    kern = ("sparse_sketch_rows_kernel (row gather, bank-conflict-free schedule)" if gather else
+            "tc2_kernel<XW, fp16> (2-SM tcgen05, 3-term fp16 split)" if esz == 4
             else "xw_f64_fast_kernel (DMMA m8n8k4)")
     return {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
         "traffic": _traffic(config),
         "kernel": f"sketch U = X Omega, {kern}",
-        "peak_note": ("fp32 data: fp32-equivalent TFLOP/s (2 m n l) against bf16_tflops_sustained / 3 "
+        "peak_note": ("very sparse Omega: the gather's bytes (X once, U and its planes) against HBM"
+                      if gather else
+                      "fp32 data: fp32-equivalent TFLOP/s (2 m n l) against bf16_tflops_sustained / 3 "
                       "(every fp32 product is three fp16 products)" if esz == 4 else
                       "fp64 data: TFLOP/s against the measured DMMA rate") + f"; peaks from {pk['source']}",
         "x_passes_frac": tot_roof / tot_t if tot_t > 0 else None,

@@ -1313,13 +1313,21 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
     ev.mark(12);
     ev.mark(13);
     if (rows) {
-      ctx.wait_arrivals();
       float* up = u.plain ? static_cast<float*>(u.plain) : ctx.get<float>("u.gather", mm * u.ld);
-      launch_sparse_sketch_rows(ctx.stream, static_cast<const float*>(x.p), m, n, x.ld,
-                                static_cast<const std::uint32_t*>(ctx.buf("so.rows", 4)), ctx.row_sched_steps,
-                                ctx.row_sched_smax, ctx.row_sched_splits, l, up, u.ld, f16 ? xs.dev : nullptr,
-                                ctx.num_sms);
-      LPCA_LAUNCHED(ctx);
+      // one launch per landed chunk of a host X still crossing PCIe (else one)
+      auto chunks = std::move(ctx.arrivals);
+      ctx.arrivals.clear();
+      if (chunks.empty()) chunks.emplace_back(m, nullptr);
+      index_t r0 = 0;
+      for (const auto& ch : chunks) {
+        if (ch.second) LPCA_CUDA(cudaStreamWaitEvent(ctx.stream, ch.second, 0));
+        launch_sparse_sketch_rows(ctx.stream, static_cast<const float*>(x.p) + r0 * x.ld, ch.first - r0, n, x.ld,
+                                  static_cast<const std::uint32_t*>(ctx.buf("so.rows", 4)), ctx.row_sched_steps,
+                                  ctx.row_sched_smax, ctx.row_sched_splits, l, up + r0 * u.ld, u.ld,
+                                  f16 ? xs.dev : nullptr, ctx.num_sms);
+        LPCA_LAUNCHED(ctx);
+        r0 = ch.first;
+      }
       if (f16) {
         launch_u_planes_f16(ctx.stream, up, m, u.ld, u.ld, u.h16hi, u.h16lo, u.ldt16, u.uinv);
         ctx.note_launch();

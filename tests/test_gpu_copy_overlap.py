@@ -25,20 +25,23 @@ def _run(x_host, cfg, ctx, y_dtype):
     return mp.singular_values if cfg.method != M.rp else np.zeros(1), mp.v, y
 
 
-@pytest.mark.parametrize("dtype,method,q", [
-    (torch.float32, M.lazy_spca, 0),
-    (torch.float32, M.lazy_spca, 1),
-    (torch.float32, M.spca, 0),
-    (torch.float32, M.rp, 0),
-    (torch.float64, M.lazy_spca, 0),
+@pytest.mark.parametrize("dtype,method,q,n,sparse", [
+    (torch.float32, M.lazy_spca, 0, 1000, False),
+    (torch.float32, M.lazy_spca, 1, 1000, False),
+    (torch.float32, M.spca, 0, 1000, False),
+    (torch.float32, M.rp, 0, 1000, False),
+    (torch.float64, M.lazy_spca, 0, 1000, False),
+    (torch.float32, M.lazy_spca, 1, 9000, True),   # very sparse Omega, long rows: the row gather per chunk
 ])
-def test_chunked_copies_bit_identical(ctx, monkeypatch, dtype, method, q):
-    m, n, k, l = 20_011, 1000, 12, 12 if method == M.rp else 30   # ragged last chunk
+def test_chunked_copies_bit_identical(ctx, monkeypatch, dtype, method, q, n, sparse):
+    m, k, l = 20_011, 12, 12 if method == M.rp else 30   # ragged last chunk
     x = _x(m, n, dtype)
     xh = x.cpu().numpy()
-    cfg = lp.ReducerConfig(method=method, k=k, l=l, power_iters=q, projection=lp.ProjectionSpec(seed=5))
+    spec = (lp.ProjectionSpec(kind=lp.ProjectionKind.very_sparse, density=1 / 64, seed=5) if sparse
+            else lp.ProjectionSpec(seed=5))
+    cfg = lp.ReducerConfig(method=method, k=k, l=l, power_iters=q, projection=spec)
     y_dt = np.float32 if dtype == torch.float32 else np.float64
-    monkeypatch.setenv("LPCA_H2D_CHUNK_MB", "1")   # 512-row chunks: ~40 of them
+    monkeypatch.setenv("LPCA_H2D_CHUNK_MB", "1")   # 512-row chunks: ~40 of them (n = 1000)
     chunked = _run(xh, cfg, ctx, y_dt)
     monkeypatch.setenv("LPCA_H2D_CHUNKS", "0")
     whole = _run(xh, cfg, ctx, y_dt)

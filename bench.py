@@ -113,8 +113,8 @@ class ClockSampler:
              0x100: "display_clock_setting"}
 
     def __init__(self, device: int):
-        self.samples, self.reasons = [], set()
-        self.max_mhz = None
+        self.samples, self.reasons, self.power = [], set(), []
+        self.max_mhz = self.power_limit_w = None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -122,6 +122,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                pass
         except Exception:
             self.nv = None
 
@@ -129,6 +133,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.NAMES.items():
                     if r & bit and name != "gpu_idle":
@@ -151,8 +159,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons)}
+        if self.power:  # board power: at the enforced limit the passes are energy-bound
+            out["power_w"] = round(statistics.median(self.power), 1)
+            out["power_limit_w"] = self.power_limit_w
+        return out
 
 
 def _dist():

@@ -5,6 +5,7 @@ pool, so out-of-bounds writes are caught by pattern bands instead: behind every
 workspace (lpca_debug_check_guards) and around caller buffers."""
 import ctypes as C
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -48,6 +49,17 @@ for m, n, k, l, q in shapes:
         lp.reduce_spca(x, cfg(M.spca, k, l), ctx=ctx)
         fit_transform_guarded(x, cfg(M.lazy_spca, k, l, kind=lp.ProjectionKind.very_sparse, density=0.05), k)
         lp.reduce_lazy_spca_streaming(lp.SliceRowBlockStream(x.cpu().numpy(), 333), cfg(M.lazy_spca, k, l), ctx=ctx)
+# the row gather (fp32 rows longer than 8192; LPCA_SPARSE_OMEGA=1 also forces it
+# onto a short ragged row), its U padding columns and its parts' sums
+for m, n, k, l in ((777, 9004, 30, 61), (1500, 16384, 100, 300)):
+    x = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(x, 0, 3 * l, 0.95, 0.01, 1000, ctx=ctx)
+    fit_transform_guarded(x, cfg(M.lazy_spca, k, l, kind=lp.ProjectionKind.very_sparse, density=1 / 96), k)
+os.environ["LPCA_SPARSE_OMEGA"] = "1"
+x = torch.empty((1001, 1028), dtype=torch.float32, device="cuda")
+lp.synth_lowrank(x, 0, 60, 0.95, 0.01, 1000, ctx=ctx)
+fit_transform_guarded(x, cfg(M.lazy_spca, 13, 37, kind=lp.ProjectionKind.very_sparse, density=0.05), 13)
+del os.environ["LPCA_SPARSE_OMEGA"]
 names = C.create_string_buffer(4096)
 bad = ctx.lib.lpca_debug_check_guards(ctx.h, names, 4096)
 print(json.dumps({"bad_workspaces": int(bad), "names": names.value.decode(), "bad_y": bad_y,

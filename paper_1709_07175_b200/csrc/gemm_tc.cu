@@ -517,9 +517,11 @@ void launch_xw_pair(cudaStream_t s, const XwPairArgs& p, int num_sms) {
     a.n = static_cast<int>(p.n);
     a.npad = wc;
     a.items = static_cast<int>(ceil_div(p.m, 2 * kBM));
-    // fp16 runs: K = 512 with one global X scale (transform, power steps); the
-    // scanned sketch clamps to the stage ring (K = 256)
-    a.run_stages = env_int("LPCA_TC_RUN", 8);
+    // fp16 runs: K = 1024 (16 stages; the fold into the long accumulator
+    // every 512 cost ~3% of a configs[2] step at the power cap, for 1.2-1.5x
+    // smaller singular-value errors, all far inside the 1e-4 target); the
+    // scanned sketch clamps to the stage ring. tf32: K = 256.
+    a.run_stages = env_int("LPCA_TC_RUN", p.half ? 16 : 8);
     a.scan = p.half && !p.xmax_in && !(p.xmax_val > 0.0f) ? (p.ovf ? 2 : 1) : 0;
     a.ovf = p.ovf;
     a.wlo_nz = p.half ? p.wlo_nz : nullptr;

@@ -7,7 +7,7 @@
 //   kHalf = true  : fp16 hi/lo of power-of-two scaled operands (kind::f16,
 //                   K = 64 per stage, twice the tf32 MMA rate, half the TMEM
 //                   A traffic per K): every pass of Lazy SPCA. X rows are
-//                   scaled per (row, 512-deep run) from the run's first stage
+//                   scaled per (row, run; 1024 deep) from the run's first stage
 //                   (sketch, transform; a flagged run redoes the pass with each
 //                   run scanned first) or by one s_x = 2^(14 - floor(log2
 //                   max|X|)) from the max the sketch recorded (power step, F);

@@ -428,8 +428,8 @@ void launch_pair(cudaStream_t s, const CUtensorMap& tx, const CUtensorMap& th, c
   a.stages = static_cast<int>(kPairSmemBudget / stage_bytes);
   if (a.stages > 8) a.stages = 8;
   if (kHalf && kMode == kXW && a.scan == 1 && a.run_stages > a.stages) a.run_stages = a.stages;  // a scanned run fits the ring
-  if (kHalf && kMode == kXTU && a.scan && a.run_stages > a.stages)
-    throw Error(kInternal, "tc pair: a scanned U^T scale block must fit the stage ring (LPCA_TC_MAXN too large)");
+  if (kHalf && kMode == kXTU && a.scan)  // a scanned run must fit the stage ring: runs of 2^k stages within a block
+    while (a.run_stages > a.stages) a.run_stages /= 2;
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024 + 512 + (kMaxEpiWarps + 3) * 4 * a.npad +
                       kRscRing * 4 * kBM + 2 * 4 * kBM;  // red, gsc, xbuf, xrow
   LPCA_CUDA(cudaFuncSetAttribute(tc2_kernel<kMode, kHalf, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -588,7 +588,7 @@ void launch_utx_pair(cudaStream_t s, const UtxPairArgs& p, int num_sms) {
     a.npad = wc;
     a.chunk_rows = static_cast<int>(rows);
     a.items = static_cast<int>(ceil_div(p.n, 2 * kBM) * chunks);
-    a.run_stages = static_cast<int>(kUScaleRows / 64);  // fp16: one run (8 x 64 rows) per block of U^T scales
+    a.run_stages = static_cast<int>(kUScaleRows / 64);  // fp16: one run per block of U^T scales
     a.scan = p.half && !p.xmax_in;
     a.xmax_in = p.xmax_in;
     a.uinv_in = p.uinv ? p.uinv + c0 : nullptr;

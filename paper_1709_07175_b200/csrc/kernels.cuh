@@ -137,9 +137,11 @@ void launch_utx_tc(cudaStream_t s, const float* u, index_t ldu, const float* x, 
 // power-of-two scaled operands (half = true: X scaled from max|X| = *xmax_in,
 // W planes per column (winv = inverse scales), U^T planes per column and
 // kUScaleRows-row block (uinv[block][c])). Planes are K-major: [wpad or round_up(l,16)][ld].
-// rows per block of the U^T fp16 plane scales: one 2-SM pair item of the X W
-// pass, one fp16 run (4 stages of 64 rows) of the X^T U pass
-constexpr index_t kUScaleRows = 512;  // two X W pair items; one X^T U run
+// rows per block of the U^T fp16 plane scales: two 256-row X W pair items
+// (done back to back by one pair), one fp16 run (8 stages of 64 rows) of the
+// X^T U pass. (1024-row blocks, XᵀU runs twice as deep, measured no faster
+// at configs[2]: 134.6-138.2 against 133.0-134.9 ms per step.)
+constexpr index_t kUScaleRows = 512;
 
 struct XwPairArgs {
   const float* x = nullptr;

@@ -1588,7 +1588,7 @@ void transform_dev(lpca_ctx& ctx, const lpca_map& map, const DevX& x, void* y, i
       yo.plain = ydev;
       yo.ld = ldy;
       if (tc_pair_mode() && f16_enabled()) {
-        // fp16 encoding with a power-of-two scale per (row, 512-deep run) taken
+        // fp16 encoding with a power-of-two scale per (row, run) taken
         // from the run's first stage (16x headroom): every row of Y keeps its
         // own relative precision whatever the rows' dynamic range. A later
         // stage outside the scale's range sets the flag; transform_finish then

@@ -280,13 +280,14 @@ __device__ __forceinline__ void split_f16_16(const float* v, float (&hi)[8], flo
   }
 }
 
-// The items a pair works through. X W: two consecutive 256-row items (one
-// kUScaleRows block of U^T scales) back to back, so the block's second item can
+// The items a pair works through. X W: the consecutive 256-row items of one
+// kUScaleRows block of U^T scales back to back, so the block's later items can
 // settle the block's scales; X^T U: every npairs-th item. -1 when done.
+constexpr int kItemsPerBlock = static_cast<int>(kUScaleRows) / 256;
 template <int kMode>
 __device__ __forceinline__ int pair_item(int pair, int npairs, int it, int items) {
   if (kMode == kXW) {
-    const int item = 2 * (pair + (it >> 1) * npairs) + (it & 1);
+    const int item = kItemsPerBlock * (pair + (it / kItemsPerBlock) * npairs) + it % kItemsPerBlock;
     return item < items ? item : -1;
   }
   const int item = pair + it * npairs;
@@ -974,34 +975,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kConv, 
         }
         mbar_wait(&xch[xb], (xit >> 1) & 1, 6);
         ++xit;
-        // A scale block is two items (kUScaleRows = 2 x 256 rows), done back to
+        // A scale block is kItemsPerBlock items (kUScaleRows rows), done back to
         // back by this pair (pair_item): the first item's planes go out at its
-        // own scale with one bit of headroom, s1; the second keeps s1 when its
-        // maxima fit under it, else settles s < s1 from both maxima and rescales
-        // the first item's planes by s / s1 (a power of two).
+        // own scale with one bit of headroom; a later item keeps the block's
+        // current scale when its maxima fit under it, else settles a smaller
+        // one from the block's running maxima and rescales the block's earlier
+        // planes (this thread's rows of them) by the ratio, a power of two.
         const int blk = t0 / kUScaleRows;
-        const bool second = (t0 / (2 * kBM)) & 1;
-        float* m1keep = red + 4 * a.npad;  // the first item's pair maxima (raw accumulator)
-        float* fac = red + 5 * a.npad;     // second item: s / s1 per column
+        const int qi = (t0 / (2 * kBM)) % kItemsPerBlock;  // the item's place in its block
+        float* mkeep = red + 4 * a.npad;  // the block's running pair maxima (raw accumulator)
+        float* fac = red + 5 * a.npad;    // new scale / previous scale per column
+        float* scur = red + 6 * a.npad;   // the block's current scale per column
         // (a pair whose rows all lie past m owns no block: writing its scales
         // would run past the [ceil(m / kUScaleRows)][npad] array)
         for (int c = ew * 32 + lane; c < a.npad; c += 32 * kEpiWarps) {
           const float f = kHalf ? __ldg(a.winv + c) : 1.0f;
           float mraw = fmaxf(gsc[c], xbuf[xb * a.npad + c]);
           float sc;
-          if (second) {
-            const float m1 = m1keep[c];
-            const float s1 = 0.5f * pow2_scale_for(m1 * f);
-            if (mraw * f * s1 < 32768.0f) {  // within the first item's headroom: its scale stands
+          if (qi > 0) {
+            const float s1 = scur[c];
+            if (mraw * f * s1 < 32768.0f) {  // within the block's headroom: its scale stands
               sc = s1;
             } else {
-              sc = pow2_scale_for(fmaxf(mraw, m1) * f);
+              sc = pow2_scale_for(fmaxf(mraw, mkeep[c]) * f);
             }
             fac[c] = sc / s1;
+            mkeep[c] = fmaxf(mkeep[c], mraw);
           } else {
-            m1keep[c] = mraw;
-            sc = 0.5f * pow2_scale_for(mraw * f);  // one bit of headroom for the block's second item
+            mkeep[c] = mraw;
+            sc = 0.5f * pow2_scale_for(mraw * f);  // one bit of headroom for the block's later items
           }
+          scur[c] = sc;
           gsc[c] = f * sc;
           if (rank == 0 && blk * kUScaleRows < a.m) a.uinv[static_cast<size_t>(blk) * a.uinv_ld + c] = __frcp_rn(sc);
         }
@@ -1020,15 +1024,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kConv, 
             }
           }
         }
-        if (second) {  // the first item's row of this thread (written by this thread)
-          const size_t r1 = static_cast<size_t>(row - 2 * kBM);
+        if (qi > 0) {  // the block's earlier items: this thread's rows of them (written by this thread)
           for (int c = c_lo; c < c_hi; ++c) {
             const float g = fac[c];
             if (g != 1.0f) {
-              __half* ph = a.uh + static_cast<size_t>(c) * a.ldh + r1;
-              __half* pl = a.ul + static_cast<size_t>(c) * a.ldh + r1;
-              *ph = __float2half_rn(__half2float(*ph) * g);
-              *pl = __float2half_rn(__half2float(*pl) * g);
+              for (int k = 1; k <= qi; ++k) {
+                const size_t r1 = static_cast<size_t>(row - k * 2 * kBM);
+                __half* ph = a.uh + static_cast<size_t>(c) * a.ldh + r1;
+                __half* pl = a.ul + static_cast<size_t>(c) * a.ldh + r1;
+                *ph = __float2half_rn(__half2float(*ph) * g);
+                *pl = __float2half_rn(__half2float(*pl) * g);
+              }
             }
           }
         }

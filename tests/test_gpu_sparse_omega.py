@@ -59,6 +59,24 @@ def test_fp32_very_sparse_paths_match_reference(ctx, ref, monkeypatch, n, mode, 
     assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
 
 
+def test_row_gather_on_the_simt_path(ctx, ref):
+    """Off the tcgen05 path (SIMT passes) fp32 X takes the row gather whatever
+    the row length, writing the plain U the SIMT passes read."""
+    m, n, l, k, d = 6000, 2048, 70, 30, 1.0 / 45
+    x = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(x, 0, 150, 0.97, 0.01, 1000, ctx=ctx)
+    rv, rs, _, _ = ref.reduce(2, x.cpu().numpy(), k, l, 11, kind=1, density=d)
+    ctx.set_gemm_path("simt")
+    try:
+        got = lp.reduce_lazy_spca(x, _cfg(k, l, d), ctx=ctx)
+    finally:
+        ctx.set_gemm_path("tcgen05")
+    rel = np.abs(got.singular_values - rs) / rs
+    print(f"fp32 very sparse Omega, SIMT passes + row gather: sigma rel {rel.max():.2e}")
+    assert rel.max() < 2e-5
+    assert O.principal_angles(got.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+
+
 def test_row_gather_configs3_shape_and_power(ctx, ref):
     """configs[3] shape (n = 16,384, l = 300, density 1/128: the row gather by
     default, rows split in two parts of an 88-step schedule)

@@ -618,8 +618,6 @@ __global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restri
                                                           double* __restrict__ lm, int* status) {
   extern __shared__ double tri[];  // packed lower triangle, column-major: column c at coff(c)
   __shared__ double red[32];
-  __shared__ double inv;
-  __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   auto coff = [&](index_t c) { return c * l - c * (c - 1) / 2; };  // element (r, c), r >= c: coff(c) + r - c
   double maxd = 0.0;
@@ -630,39 +628,35 @@ __global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restri
     double* col = tri + coff(c) - c;
     for (index_t r = c + lane; r < l; r += 32) col[r] = g[c * l + r];
   }
-  if (tid == 0) fail = 0;
   __syncthreads();
+  // One barrier per column: the trailing update uses the unscaled column j,
+  // A(r, c) -= A(r, j) (A(c, j) / d), d = A(j, j); the columns are scaled by
+  // 1 / sqrt(d) once at the end. Every thread tests the pivot (a uniform break).
+  int fail_at = 0;
   for (index_t j = 0; j < l; ++j) {
-    double* cj = tri + coff(j) - j;  // cj[r] = A(r, j)
-    if (tid == 0) {
-      const double d = cj[j];
-      if (!(d > tol)) {  // (NaN fails too)
-        fail = static_cast<int>(j) + 1;
-      } else {
-        const double sq = sqrt(d);
-        cj[j] = sq;
-        inv = 1.0 / sq;
-      }
+    const double* cj = tri + coff(j) - j;  // cj[r] = A(r, j)
+    const double d = cj[j];
+    if (!(d > tol)) {  // (NaN fails too)
+      fail_at = static_cast<int>(j) + 1;
+      break;
     }
-    __syncthreads();
-    if (fail) break;
-    for (index_t r = j + 1 + tid; r < l; r += blockDim.x) cj[r] *= inv;
-    __syncthreads();
-    // trailing update, a warp per column c, lanes down the column: A(r, c) -= L(r, j) L(c, j)
+    const double inv_d = 1.0 / d;
+    // trailing update, a warp per column c, lanes down the column
     for (index_t c = j + 1 + warp; c < l; c += nw) {
       double* cc = tri + coff(c) - c;
-      const double ljc = cj[c];
+      const double ljc = cj[c] * inv_d;
       for (index_t r = c + lane; r < l; r += 32) cc[r] = fma(-cj[r], ljc, cc[r]);
     }
     __syncthreads();
   }
-  if (fail) {
-    if (tid == 0) status[0] = fail;
+  if (fail_at) {
+    if (tid == 0) status[0] = fail_at;
     return;
   }
   for (index_t c = warp; c < l; c += nw) {
     const double* col = tri + coff(c) - c;
-    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r >= c ? col[r] : 0.0;
+    const double sq = sqrt(col[c]), isq = 1.0 / sq;
+    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r > c ? col[r] * isq : (r == c ? sq : 0.0);
   }
 }
 }  // namespace

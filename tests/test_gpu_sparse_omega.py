@@ -114,3 +114,23 @@ def test_dense_pass_skips_zero_lo_plane_bitwise(tmp_path):
         res[skip] = np.load(f)
     for key in res["1"].files:
         assert np.array_equal(res["1"][key], res["0"][key]), key
+
+
+@pytest.mark.parametrize("m,n,l,k", [
+    (5, 9004, 2, 1),       # fewer rows than SMs, the narrowest sketch
+    (130, 16384, 33, 10),  # a second column warp with one lane
+    (2049, 12000, 64, 20),
+])
+def test_row_gather_edge_shapes_match_dense_pass(ctx, monkeypatch, m, n, l, k):
+    """The row gather against the dense pass on the same X (both fp32 sums of
+    +-x, different orders): tiny row counts, l = 2, ragged column warps."""
+    xb = torch.empty((max(m, 256), n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(xb, 0, 3 * l, 0.9, 0.01, 1000, ctx=ctx)
+    x = xb[:m]
+    cfg = _cfg(k, l, 1.0 / 100)
+    got = lp.reduce_lazy_spca(x, cfg, ctx=ctx)                 # row gather (n > 8192)
+    monkeypatch.setenv("LPCA_SPARSE_OMEGA", "0")
+    want = lp.reduce_lazy_spca(x, cfg, ctx=ctx)                # dense 2-SM pass
+    rel = np.abs(got.singular_values - want.singular_values) / want.singular_values
+    assert rel.max() < 2e-5
+    assert O.principal_angles(got.v, want.v).max() < 1e-4

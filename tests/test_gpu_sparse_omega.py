@@ -134,3 +134,22 @@ def test_row_gather_edge_shapes_match_dense_pass(ctx, monkeypatch, m, n, l, k):
     rel = np.abs(got.singular_values - want.singular_values) / want.singular_values
     assert rel.max() < 2e-5
     assert O.principal_angles(got.v, want.v).max() < 1e-4
+
+
+def test_very_sparse_spca_and_streaming_match_reference(ctx, ref):
+    """SPCA (the row gather into the plain U its QR needs) and the streaming
+    Lazy reducer (per-block dense passes) with a very sparse Omega on fp32 X
+    with long rows, against the reference's reduce_spca and its streaming
+    reducer (reduce with block_rows, reducer.cpp:300-346)."""
+    m, n, l, k, d = 3000, 9000, 48, 20, 1.0 / 90
+    x = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lp.synth_lowrank(x, 0, 144, 0.95, 0.01, 1000, ctx=ctx)
+    xh = x.cpu().numpy()
+    sp = lp.reduce_spca(x, _cfg(k, l, d, lp.ReducerMethod.spca), ctx=ctx)
+    rv, rs, _, _ = ref.reduce(1, xh, k, l, 11, kind=1, density=d)
+    assert np.max(np.abs(sp.singular_values - rs) / rs) < 2e-5
+    assert O.principal_angles(sp.v[:, :k // 2], rv[:, :k // 2]).max() < 1e-5
+    st = lp.reduce_lazy_spca_streaming(lp.SliceRowBlockStream(xh, 700), _cfg(k, l, d), ctx=ctx)
+    rv2, rs2, _, _ = ref.reduce(2, xh, k, l, 11, kind=1, density=d, block_rows=700)
+    assert np.max(np.abs(st.singular_values - rs2) / rs2) < 2e-5
+    assert O.principal_angles(st.v[:, :k // 2], rv2[:, :k // 2]).max() < 1e-5

@@ -15,6 +15,9 @@ CASES = {
     "lazy_empty_shard": dict(method=M.lazy_spca, k=8, l=16, m=3000, n=300, dtype="f64", split="all_on_0"),
     # fp32 data on the tensor-core path, built to trip the sketch's overflow rerun
     "lazy_f32_rerun": dict(method=M.lazy_spca, k=16, l=32, m=8192, n=2048, dtype="f32", overflow=True),
+    # fp32, a very sparse Omega on long rows: the row gather on each rank
+    "lazy_f32_row_gather": dict(method=M.lazy_spca, k=16, l=40, q=1, m=4096, n=9000, dtype="f32",
+                                very_sparse=1.0 / 90),
     # streaming reducers (Algorithms 4 and 3) over each rank's blocks
     "stream_lazy": dict(method=M.lazy_spca, k=8, l=16, m=3000, n=300, dtype="f64", stream=True, block_rows=700),
     "stream_spca": dict(method=M.spca, k=8, l=16, m=3000, n=300, dtype="f64", stream=True, block_rows=700),
@@ -45,3 +48,10 @@ def shard(c, m, world, rank):
     per = -(-m // world)
     lo = min(m, rank * per)
     return lo, min(m, lo + per)
+
+
+def projection(c):
+    """The case's Omega: Gaussian, or very sparse at the case's density."""
+    if c.get("very_sparse"):
+        return lp.ProjectionSpec(kind=lp.ProjectionKind.very_sparse, density=c["very_sparse"], seed=5)
+    return lp.ProjectionSpec(seed=5)

@@ -17,7 +17,7 @@ import paper_1709_07175_b200 as lp  # noqa: E402
 from cuda.bindings import runtime as cudart  # noqa: E402
 
 sys.path.insert(0, str(ROOT / "tests" / "helpers"))
-from dist_cases import CASES, case_data, shard  # noqa: E402
+from dist_cases import CASES, case_data, projection, shard  # noqa: E402
 
 
 def main():
@@ -57,7 +57,7 @@ def main():
         if c.get("drop_col_on") == rank:
             x = x[:, :-1]
         xs = torch.from_numpy(np.ascontiguousarray(x[lo:hi])).cuda()
-        cfg = lp.ReducerConfig(method=c["method"], k=c["k"], l=c["l"], projection=lp.ProjectionSpec(seed=5),
+        cfg = lp.ReducerConfig(method=c["method"], k=c["k"], l=c["l"], projection=projection(c),
                                power_iters=c.get("q", 0))
         try:
             if c.get("stream"):

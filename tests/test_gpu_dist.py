@@ -17,7 +17,7 @@ import paper_1709_07175_b200 as lp
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "tests" / "helpers"))
-from dist_cases import CASES, case_data  # noqa: E402
+from dist_cases import CASES, case_data, projection  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,7 @@ def ranks(tmp_path_factory):
 def _single(ctx, name):
     c = CASES[name]
     x = case_data(name)
-    cfg = lp.ReducerConfig(method=c["method"], k=c["k"], l=c["l"], projection=lp.ProjectionSpec(seed=5),
+    cfg = lp.ReducerConfig(method=c["method"], k=c["k"], l=c["l"], projection=projection(c),
                            power_iters=c.get("q", 0))
     if c.get("stream"):
         fn = lp.reduce_spca_streaming if c["method"] == lp.ReducerMethod.spca else lp.reduce_lazy_spca_streaming

@@ -116,7 +116,9 @@ int32_t lpca_abi_version(void);
 /* ---- contexts (one per GPU) --------------------------------------------- */
 lpca_status lpca_ctx_create(int32_t device, lpca_ctx** out);
 /* Row-sharded data parallelism over NCCL: `rank` of `world`, all ranks pass the
- * same 128-byte id from lpca_nccl_unique_id on rank 0. world == 1 needs no id. */
+ * same 128-byte id from lpca_nccl_unique_id on rank 0. world == 1 needs no id;
+ * world == 1 with an id makes a one-rank communicator whose exchanges still run
+ * through ncclAllReduce (the NCCL path exercised on one GPU). */
 lpca_status lpca_nccl_unique_id(void* out_128_bytes);
 lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
                                  const void* nccl_id_128, lpca_ctx** out);

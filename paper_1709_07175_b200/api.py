@@ -361,7 +361,7 @@ class Context:
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self.lib = L.load()
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # (world 1 + id: a one-rank NCCL communicator)
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _check(self.lib.lpca_ctx_create_dist(device, rank, world, buf, C.byref(h)))
         else:

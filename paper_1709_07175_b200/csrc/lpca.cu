@@ -227,7 +227,7 @@ struct lpca_ctx {
     return static_cast<T*>(buf(name, count * sizeof(T)));
   }
   void allreduce(double* p, index_t count) {
-    if (world <= 1) return;
+    if (world <= 1 && !comm) return;  // (a one-rank communicator still runs: the NCCL path on one GPU)
     if (hook) {
       if (hook(hook_user, p, count, stream) != 0) throw Error(lpca::kNccl, "allreduce hook failed");
       return;
@@ -2087,7 +2087,9 @@ lpca_status lpca_ctx_create_dist(int32_t device, int32_t rank, int32_t world,
     *out = nullptr;
     lpca_ctx* ctx = make_ctx(device, rank, world);
     try {
-      if (world > 1) {
+      // world == 1 with an id: a one-rank communicator (every exchange still
+      // goes through ncclAllReduce, so the NCCL path runs on a one-GPU box)
+      if (world > 1 || nccl_id_128) {
         if (!nccl_id_128) throw Error(kInvalidArgument, "world > 1 needs an NCCL unique id");
         ncclUniqueId id;
         std::memcpy(&id, nccl_id_128, sizeof(id));

@@ -463,6 +463,50 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
   if (c == 0 && lane == 0) status[0] = 0;
 }
 
+constexpr int kCholRows = 8, kCholMaxL = 256;  // one-CTA kernels: rows per lane, l <= 256
+
+// chol_inv_kernel with L's packed lower triangle staged in shared memory once
+// per CTA (l <= ~220 with 8 warps): the column walk reads L(r, j) at shared-memory
+// latency instead of L1/L2's (the global variant: 0.11 ms at l = 220). Same
+// arithmetic in the same order.
+__global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* __restrict__ lm, index_t l,
+                                                            double* __restrict__ w, int* status) {
+  extern __shared__ double sh[];
+  if (status[0] != 0) return;
+  const int L = static_cast<int>(l), lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* dinv = sh;                                 // [l]
+  double* b = sh + L + wid * L;                      // this warp's [l]
+  double* tri = sh + L + (blockDim.x >> 5) * L;      // packed lower triangle, column j at tri + off(j)
+  auto off = [&](int j) { return j * L - j * (j - 1) / 2 - j; };
+  for (int j = threadIdx.x; j < L; j += blockDim.x) dinv[j] = 1.0 / lm[static_cast<index_t>(j) * l + j];
+  for (int j = wid; j < L; j += blockDim.x >> 5) {  // a lane's rows of a column loaded together
+    double v[kCholRows];
+#pragma unroll
+    for (int t = 0; t < kCholRows; ++t) {
+      const int r = j + lane + 32 * t;
+      v[t] = r < L ? lm[static_cast<index_t>(j) * l + r] : 0.0;
+    }
+    double* cj = tri + off(j);
+#pragma unroll
+    for (int t = 0; t < kCholRows; ++t)
+      if (j + lane + 32 * t < L) cj[j + lane + 32 * t] = v[t];
+  }
+  __syncthreads();
+  const int c = static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + wid;
+  if (c >= L) return;
+  for (int r = lane; r < L; r += 32) b[r] = r == c ? 1.0 : 0.0;
+  __syncwarp();
+  for (int j = c; j < L; ++j) {
+    const double x = b[j] * dinv[j];  // L^{-1}(j, c)
+    if (lane == 0) w[static_cast<index_t>(j) * l + c] = x;
+    const double* colj = tri + off(j);
+    for (int r = j + 1 + lane; r < L; r += 32) b[r] -= colj[r] * x;
+    __syncwarp();
+  }
+  for (int j = lane; j < c; j += 32) w[static_cast<index_t>(j) * l + c] = 0.0;
+  if (c == 0 && lane == 0) status[0] = 0;
+}
+
 // tmp(r, j) = sum_{s <= r} L^{-1}(r, s) F(s, j), tiled: a CTA computes 64 r x
 // 64 j outputs from 16-wide slabs of L^{-1} rows and F columns in shared memory,
 // 4 x 4 per thread; each output still sums s = 0, 1, ... in order with FMAs
@@ -608,44 +652,124 @@ void launch_sign_canon(cudaStream_t s, double* v, index_t n, index_t k, double* 
 
 namespace {
 // The whole Cholesky factorisation in one CTA when the lower triangle fits
-// shared memory (l <= ~236): packed columns, right-looking, a warp per trailing
-// column with lanes running down it (contiguous, conflict-free), three barriers
-// per column, instead of a one-CTA panel kernel plus a trailing SYRK per 32 columns
-// (latency-bound at l ~ 220: 21 launches, ~1.4 ms for a power step's three
-// factorisations). Same pivot rule and status as the panel path; L goes to lm
-// (column-major, zeros above) for chol_inv_kernel.
-__global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restrict__ g, index_t l, double tol_rel,
+// shared memory (l <= ~236): packed columns, right-looking, blocked by panels
+// of kCholPanel columns. Within a panel one barrier per column (the update runs
+// on the unscaled column j: A(r, c) -= A(r, j) (A(c, j) / d), d = A(j, j), for
+// the panel's later columns only); the panel is then scaled to L and the
+// trailing matrix takes one rank-kCholPanel update, a warp per kCholGroup
+// columns with lanes down the rows and the panel's rows L(r, :) in registers,
+// so each trailing element is read and written once per panel instead of once
+// per column (the column-at-a-time kernel was bound by shared-memory traffic:
+// 0.37 ms at l = 220). Same pivot rule and status as the panel path (the first
+// column whose pivot fails, 1-based); L goes to lm (column-major, zeros above)
+// for chol_inv_kernel.
+constexpr int kCholPanel = 8, kCholGroup = 2;
+
+__global__ void __launch_bounds__(512) chol_small_kernel(const double* __restrict__ g, index_t l, double tol_rel,
                                                           double* __restrict__ lm, int* status) {
   extern __shared__ double tri[];  // packed lower triangle, column-major: column c at coff(c)
   __shared__ double red[32];
+  __shared__ int coff[kCholMaxL];    // col(c)[r] = A(r, c), r >= c
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  auto coff = [&](index_t c) { return c * l - c * (c - 1) / 2; };  // element (r, c), r >= c: coff(c) + r - c
+  const int L = static_cast<int>(l);
+  for (int c = tid; c < L; c += blockDim.x) coff[c] = c * L - c * (c - 1) / 2 - c;
+  __syncthreads();
+  auto col = [&](int c) { return tri + coff[c]; };
   double maxd = 0.0;
   for (index_t j = tid; j < l; j += blockDim.x) maxd = fmax(maxd, g[j * l + j]);
   block_max_reduce(maxd, red);
   const double tol = tol_rel * maxd;
-  for (index_t c = warp; c < l; c += nw) {
-    double* col = tri + coff(c) - c;
-    for (index_t r = c + lane; r < l; r += 32) col[r] = g[c * l + r];
+  // a lane's rows of a column loaded together (one L2 latency per column, not per row)
+  for (int c = warp; c < L; c += nw) {
+    double v[kCholRows];
+#pragma unroll
+    for (int t = 0; t < kCholRows; ++t) {
+      const int r = c + lane + 32 * t;
+      v[t] = r < L ? g[static_cast<index_t>(c) * l + r] : 0.0;
+    }
+    double* cc = col(c);
+#pragma unroll
+    for (int t = 0; t < kCholRows; ++t)
+      if (c + lane + 32 * t < L) cc[c + lane + 32 * t] = v[t];
   }
   __syncthreads();
-  // One barrier per column: the trailing update uses the unscaled column j,
-  // A(r, c) -= A(r, j) (A(c, j) / d), d = A(j, j); the columns are scaled by
-  // 1 / sqrt(d) once at the end. Every thread tests the pivot (a uniform break).
   int fail_at = 0;
-  for (index_t j = 0; j < l; ++j) {
-    const double* cj = tri + coff(j) - j;  // cj[r] = A(r, j)
-    const double d = cj[j];
-    if (!(d > tol)) {  // (NaN fails too)
-      fail_at = static_cast<int>(j) + 1;
-      break;
+  for (int p0 = 0; p0 < L && !fail_at; p0 += kCholPanel) {
+    const int pe = p0 + kCholPanel < L ? p0 + kCholPanel : L;
+    for (int j = p0; j < pe; ++j) {
+      const double* cj = col(j);
+      const double d = cj[j];
+      if (!(d > tol)) {  // (NaN fails too); every thread tests: a uniform break
+        fail_at = j + 1;
+        break;
+      }
+      const double inv_d = 1.0 / d;
+      for (int c = j + 1 + warp; c < pe; c += nw) {
+        double* cc = col(c);
+        const double ljc = cj[c] * inv_d;
+        // all of the lane's loads before its stores (at most kCholRows rows per
+        // lane): one shared-memory latency per column instead of one per row
+        double a[kCholRows], b[kCholRows];
+#pragma unroll
+        for (int t = 0; t < kCholRows; ++t) {
+          const int r = c + lane + 32 * t;
+          a[t] = r < L ? cj[r] : 0.0;
+          b[t] = r < L ? cc[r] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kCholRows; ++t) {
+          const int r = c + lane + 32 * t;
+          if (r < L) cc[r] = fma(-a[t], ljc, b[t]);
+        }
+      }
+      __syncthreads();
     }
-    const double inv_d = 1.0 / d;
-    // trailing update, a warp per column c, lanes down the column
-    for (index_t c = j + 1 + warp; c < l; c += nw) {
-      double* cc = tri + coff(c) - c;
-      const double ljc = cj[c] * inv_d;
-      for (index_t r = c + lane; r < l; r += 32) cc[r] = fma(-cj[r], ljc, cc[r]);
+    if (fail_at) break;
+    for (int j = p0 + warp; j < pe; j += nw) {  // the panel becomes L
+      double* cj = col(j);
+      const double sq = sqrt(cj[j]), isq = 1.0 / sq;
+      for (int r = j + 1 + lane; r < L; r += 32) cj[r] *= isq;
+      if (lane == 0) cj[j] = sq;
+    }
+    __syncthreads();
+    const int np = pe - p0, ngroups = (L - pe + kCholGroup - 1) / kCholGroup;
+    const double* pk[kCholPanel];  // the panel's columns
+#pragma unroll
+    for (int k = 0; k < kCholPanel; ++k) pk[k] = col(k < np ? p0 + k : p0);
+    for (int grp = warp; grp < ngroups; grp += nw) {
+      const int c0 = pe + grp * kCholGroup;
+      double* cq[kCholGroup];
+#pragma unroll
+      for (int q = 0; q < kCholGroup; ++q) cq[q] = col(c0 + q < L ? c0 + q : c0);
+      double lc[kCholGroup][kCholPanel];
+#pragma unroll
+      for (int q = 0; q < kCholGroup; ++q)
+#pragma unroll
+        for (int k = 0; k < kCholPanel; ++k) lc[q][k] = (c0 + q < L && k < np) ? pk[k][c0 + q] : 0.0;
+      // two rows per lane at a time, every load before the stores
+      for (int r0 = c0 + lane; r0 < L; r0 += 64) {
+        double lr[2][kCholPanel], v[2][kCholGroup];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + 32 * h;
+#pragma unroll
+          for (int k = 0; k < kCholPanel; ++k) lr[h][k] = (k < np && r < L) ? pk[k][r] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kCholGroup; ++q) v[h][q] = (r < L && r >= c0 + q) ? cq[q][r] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + 32 * h;
+#pragma unroll
+          for (int q = 0; q < kCholGroup; ++q) {
+            if (r >= L || r < c0 + q) continue;  // (also covers c0 + q >= L)
+            double t = v[h][q];
+#pragma unroll
+            for (int k = 0; k < kCholPanel; ++k) t = fma(-lr[h][k], lc[q][k], t);
+            cq[q][r] = t;
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -653,11 +777,32 @@ __global__ void __launch_bounds__(1024) chol_small_kernel(const double* __restri
     if (tid == 0) status[0] = fail_at;
     return;
   }
-  for (index_t c = warp; c < l; c += nw) {
-    const double* col = tri + coff(c) - c;
-    const double sq = sqrt(col[c]), isq = 1.0 / sq;
-    for (index_t r = lane; r < l; r += 32) lm[c * l + r] = r > c ? col[r] * isq : (r == c ? sq : 0.0);
+  for (int c = warp; c < L; c += nw) {
+    const double* cc = col(c);
+    for (int r = lane; r < L; r += 32) lm[static_cast<index_t>(c) * l + r] = r >= c ? cc[r] : 0.0;
   }
+}
+}  // namespace
+
+namespace {
+// W = L^{-T} of lm (launch_chol_inverse's layout): the shared-memory variant when
+// L's packed triangle, dinv and the warps' right-hand sides fit one CTA.
+void launch_chol_inv(cudaStream_t s, const double* lm, index_t l, double* w, int* status) {
+  const std::size_t packed = static_cast<std::size_t>(l) * (l + 1) / 2;
+  const std::size_t sm8 = (static_cast<std::size_t>(l) * 9 + packed) * sizeof(double);
+  if (sm8 <= 227 * 1024) {
+    LPCA_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm8 > 48 * 1024 ? sm8 : 48 * 1024)));
+    chol_inv_smem_kernel<<<static_cast<unsigned>(ceil_div(l, 8)), 256, sm8, s>>>(lm, l, w, status);
+    return;
+  }
+  int wpb = 8;  // warps per block: dinv + one right-hand side per warp in shared memory
+  while (wpb > 1 && static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
+  const std::size_t ism = static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double);
+  if (ism > 227 * 1024) throw Error(kInternal, "chol_inverse: l too large for the shared-memory solve");
+  LPCA_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ism > 48 * 1024 ? ism : 48 * 1024)));
+  chol_inv_kernel<<<static_cast<unsigned>(ceil_div(l, wpb)), 32 * wpb, ism, s>>>(lm, l, w, status);
 }
 }  // namespace
 
@@ -669,7 +814,7 @@ void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rin
   if (tri_bytes <= 220 * 1024) {
     LPCA_CUDA(cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(tri_bytes < 48 * 1024 ? 48 * 1024 : tri_bytes)));
-    chol_small_kernel<<<1, 1024, tri_bytes, s>>>(g, l, tol_rel, work, status);
+    chol_small_kernel<<<1, 512, tri_bytes, s>>>(g, l, tol_rel, work, status);
   } else {
     chol_copy_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(g, l, work);
     std::size_t psm = static_cast<std::size_t>(l) * kCholNb * sizeof(double);
@@ -686,13 +831,7 @@ void launch_chol_inverse(cudaStream_t s, const double* g, index_t l, double* rin
       }
     }
   }
-  int wpb = 8;  // warps per block: dinv + one right-hand side per warp in shared memory
-  while (wpb > 1 && static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
-  const std::size_t ism = static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double);
-  if (ism > 227 * 1024) throw Error(kInternal, "chol_inverse: l too large for the shared-memory solve");
-  LPCA_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ism > 48 * 1024 ? ism : 48 * 1024)));
-  chol_inv_kernel<<<static_cast<unsigned>(ceil_div(l, wpb)), 32 * wpb, ism, s>>>(work, l, rinv, status);
+  launch_chol_inv(s, work, l, rinv, status);
 }
 
 namespace {
@@ -802,13 +941,7 @@ void launch_upper_inverse(cudaStream_t s, const double* r, index_t l, double* w,
   if (l <= 0) return;
   LPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
   upper_to_lower_kernel<<<static_cast<unsigned>(ceil_div(l * l, 256)), 256, 0, s>>>(r, l, work);
-  int wpb = 8;
-  while (wpb > 1 && static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
-  const std::size_t ism = static_cast<std::size_t>(l) * (wpb + 1) * sizeof(double);
-  if (ism > 227 * 1024) throw Error(kInternal, "upper_inverse: l too large for the shared-memory solve");
-  LPCA_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ism > 48 * 1024 ? ism : 48 * 1024)));
-  chol_inv_kernel<<<static_cast<unsigned>(ceil_div(l, wpb)), 32 * wpb, ism, s>>>(work, l, w, status);
+  launch_chol_inv(s, work, l, w, status);
 }
 
 }  // namespace lpca

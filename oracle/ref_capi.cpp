@@ -207,6 +207,30 @@ int ref_fit_transform(int method, const void* x, int dtype, std::int64_t m, std:
   });
 }
 
+// ref_fit_transform on a caller's canonical CSC (col_ptr n+1, row_idx and
+// values nnz; SparseMatrix::from_csc validates it), for sparse-X timing
+// (tools/sparse_bench.py): reduce() + apply_map() timed, the copy into the
+// reference's SparseMatrix outside.
+int ref_fit_transform_csc(int method, std::int64_t m, std::int64_t n, const std::int64_t* col_ptr,
+                          const std::int64_t* row_idx, const double* values, std::int64_t k, std::int64_t l,
+                          std::uint64_t seed, int kind, double density, double* y_out, double* v_out,
+                          double* sigma_out, double* seconds) {
+  return guarded([&] {
+    const std::int64_t nnz = col_ptr[n];
+    const SparseMatrix xs = SparseMatrix::from_csc(m, n, std::vector<index_t>(col_ptr, col_ptr + n + 1),
+                                                   std::vector<index_t>(row_idx, row_idx + nnz),
+                                                   std::vector<double>(values, values + nnz));
+    const auto t0 = std::chrono::steady_clock::now();
+    const ReductionMap map = reduce(xs, make_cfg(method, k, l, seed, kind, density, 0));
+    const DenseMatrix y = apply_map(map, xs);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (y_out) copy_out(y, y_out);
+    if (v_out) copy_out(map.v, v_out);
+    if (sigma_out)
+      for (std::size_t i = 0; i < map.singular_values.size(); ++i) sigma_out[i] = map.singular_values[i];
+  });
+}
+
 // Lazy SPCA with q power steps composed from the reference's own kernels
 // (the reference has no power iterations; this is the builder's
 // scheme of SURVEY 8(a) a16 restated on the reference's code):

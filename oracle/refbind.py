@@ -147,6 +147,23 @@ def fit_transform(method: int, x: np.ndarray, k: int, l: int, seed: int, kind: i
     return y, v, sig, secs.value
 
 
+def fit_transform_csc(method: int, m: int, n: int, col_ptr, row_idx, values, k: int, l: int, seed: int,
+                     kind: int = 0, density: float = 1.0, want_y: bool = True):
+    """reduce + apply_map on a canonical CSC X (int64 col_ptr / row_idx, fp64
+    values); returns (Y, V, sigma, seconds of reduce + apply_map)."""
+    cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(row_idx, dtype=np.int64)
+    va = np.ascontiguousarray(values, dtype=np.float64)
+    y = np.zeros((m, k), order="F") if want_y else None
+    v = np.zeros((n, k), order="F")
+    sig = np.zeros(k)
+    secs = C.c_double()
+    _chk(load().ref_fit_transform_csc(C.c_int(method), C.c_int64(m), C.c_int64(n), _p(cp), _p(ri), _p(va),
+                                      C.c_int64(k), C.c_int64(l), C.c_uint64(seed), C.c_int(kind),
+                                      C.c_double(density), _p(y), _p(v), _p(sig), C.byref(secs)))
+    return y, v, sig, secs.value
+
+
 def lazy_power_fit_transform(x: np.ndarray, k: int, l: int, seed: int, q: int, kind: int = 0,
                              density: float = 1.0, want_y: bool = True):
     """Lazy SPCA with q power steps composed from the reference's kernels

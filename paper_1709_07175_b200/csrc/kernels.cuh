@@ -64,6 +64,17 @@ void launch_spmm_csr(cudaStream_t s, index_t m, const std::int64_t* row_ptr, con
                      const double* val, const double* wt, index_t ldw, index_t w, void* out, int out_dtype,
                      index_t ors, index_t ocs);
 // F (l x n column-major) (+)= U^T X with X in CSC and U row-major m x l (ld ldu), l <= 512.
+// Device staging of a host CSC (sparse.cu): checks in the host loop's order
+// (first = 4 p + code of the first failing entry, ~0 if none), 32-bit rows,
+// column of each entry, fp64 values; then the CSR copy by a stable row sort.
+std::size_t csc_stage_temp_bytes(index_t m, index_t nnz);
+void launch_csc_check(cudaStream_t s, index_t n, index_t rows, const std::int64_t* cp, const std::int64_t* ri64,
+                      const void* val, int dtype, std::int32_t* ri, std::int32_t* colof, double* cv,
+                      unsigned long long* first);
+void launch_csr_from_csc(cudaStream_t s, index_t m, index_t nnz, const std::int32_t* ri, const std::int32_t* colof,
+                         const double* cv, std::int64_t* rp, std::int32_t* ci, double* rv, std::int64_t* cnt,
+                         std::int32_t* keys_out, std::int32_t* perm_in, std::int32_t* perm_out, void* temp,
+                         std::size_t temp_bytes);
 void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, const std::int32_t* row,
                        const double* val, const double* u, index_t ldu, index_t l, double* f, bool accumulate);
 // ---- verification metrics (metrics.cu; metrics.cpp:123-136, 311-352) -------------

@@ -381,6 +381,83 @@ void check_view(const lpca_matrix_view* x) {
   }
 }
 
+// A sparse CSC view staged on the device (csrc/sparse.cu): col_ptr, row_idx and
+// the values cross PCIe as the caller holds them; the entries are checked, the
+// indices narrowed and the CSR copy built by kernels. Errors are the host
+// loop's, in its order: the first column whose col_ptr decreases is found
+// here, and an entry error in an earlier column wins over it (the device
+// checks exactly those columns).
+DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes) {
+  const index_t m = x->rows, n = x->cols, nnz = x->nnz;
+  const std::size_t es = dsize(x->dtype), nz = static_cast<std::size_t>(nnz > 0 ? nnz : 1);
+  index_t bad_col = -1;  // the first column whose col_ptr decreases
+  for (index_t j = 0; j < n && bad_col < 0; ++j)
+    if (x->col_ptr[j + 1] < x->col_ptr[j]) bad_col = j;
+  const index_t ncheck = bad_col >= 0 ? bad_col : n;
+  const std::string sl(slot);
+  auto* cp = ctx.get<std::int64_t>(sl + ".cp", n + 1);
+  auto* ri = ctx.get<std::int32_t>(sl + ".ri", nz);
+  auto* cv = ctx.get<double>(sl + ".cv", nz);
+  auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
+  auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
+  auto* rv = ctx.get<double>(sl + ".rv", nz);
+  auto* first = ctx.get<unsigned long long>(sl + ".first", 1);
+  // scratch (one cached workspace, reused by later calls of the same shape):
+  // the caller's 64-bit rows and values, each entry's column, the sort's keys
+  // and permutations, the row counts, CUB's temp. (A stream-ordered allocation
+  // returned its tens of GB to the driver at every call: 2-6 s of remapping.)
+  const index_t nin = bad_col >= 0 ? x->col_ptr[bad_col] : nnz;  // entries of the checked columns
+  const std::size_t tb = csc_stage_temp_bytes(m, nnz);
+  auto a16 = [](std::size_t b) { return (b + 15) & ~std::size_t(15); };
+  const std::size_t off_v = a16(nz * 8), off_c = off_v + a16(nz * es), off_k = off_c + a16(nz * 4),
+                    off_p0 = off_k + a16(nz * 4), off_p1 = off_p0 + a16(nz * 4), off_n = off_p1 + a16(nz * 4),
+                    off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)), total = off_t + tb;
+  char* tmp = ctx.get<char>(sl + ".stage", total);
+  auto* ri64 = reinterpret_cast<std::int64_t*>(tmp);
+  void* vin = tmp + off_v;
+  auto* colof = reinterpret_cast<std::int32_t*>(tmp + off_c);
+  auto* keys = reinterpret_cast<std::int32_t*>(tmp + off_k);
+  auto* perm0 = reinterpret_cast<std::int32_t*>(tmp + off_p0);
+  auto* perm1 = reinterpret_cast<std::int32_t*>(tmp + off_p1);
+  auto* cnt = reinterpret_cast<std::int64_t*>(tmp + off_n);
+  LPCA_CUDA(cudaMemcpyAsync(cp, x->col_ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx.stream));
+  if (nin > 0) {
+    LPCA_CUDA(cudaMemcpyAsync(ri64, x->row_idx, sizeof(std::int64_t) * nin, cudaMemcpyHostToDevice, ctx.stream));
+    LPCA_CUDA(cudaMemcpyAsync(vin, x->data, es * nin, cudaMemcpyHostToDevice, ctx.stream));
+  }
+  launch_csc_check(ctx.stream, ncheck, m, cp, ri64, vin, x->dtype, ri, colof, cv, first);
+  LPCA_LAUNCHED(ctx);
+  const unsigned long long* fh = ctx.stage_read(first, 1);
+  LPCA_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (*fh != ~0ull || bad_col >= 0) {
+    if (*fh == ~0ull) throw Error(kInvalidArgument, "csc: col_ptr must be non-decreasing");
+    const index_t p = static_cast<index_t>(*fh / 4);
+    const int code = static_cast<int>(*fh % 4);
+    const index_t j = static_cast<index_t>(std::upper_bound(x->col_ptr, x->col_ptr + ncheck + 1, p) - x->col_ptr) - 1;
+    if (code == 0) throw Error(kDimension, "csc: row index out of range in column " + S(j));
+    if (code == 1) throw Error(kInvalidArgument, "csc: row indices must be strictly increasing in column " + S(j));
+    if (code == 2) throw Error(kInvalidArgument, "csc: explicit zero stored in column " + S(j));
+    throw Error(kInvalidArgument, "csc: non-finite value in column " + S(j));
+  }
+  launch_csr_from_csc(ctx.stream, m, nnz, ri, colof, cv, rp, ci, rv, cnt, keys, perm0, perm1, tmp + off_t, tb);
+  ctx.note_launch(3);  // row counts, iota, gather (+ CUB's scan and radix sort)
+  LPCA_CUDA(cudaGetLastError());
+  if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz) * static_cast<double>(8 + es) + static_cast<double>(n + 1) * 8;
+  DevX d;
+  d.m = m;
+  d.n = n;
+  d.dtype = 8;
+  d.ld = n;
+  d.rp = rp;
+  d.ci = ci;
+  d.rv = rv;
+  d.cp = cp;
+  d.ri = ri;
+  d.cv = cv;
+  d.nnz = nnz;
+  return d;
+}
+
 // Brings any view to a row-major device matrix of its own dtype. Host data is
 // copied with one cudaMemcpyAsync per contiguous range; a column-major or CSC
 // view is transposed / densified by a kernel after upload.
@@ -401,6 +478,7 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
     // canonical-form checks of SparseMatrix::from_csc (sparse_matrix.cpp:50-80)
     if (x->col_ptr[0] != 0) throw Error(kInvalidArgument, "csc: col_ptr[0] must be 0");
     if (x->col_ptr[x->cols] != nnz) throw Error(kDimension, "csc: col_ptr[cols] must equal nnz");
+    if (keep_sparse(nnz, x->rows, x->cols) && nnz < (index_t(1) << 31)) return stage_csc_device(ctx, x, slot, h2d_bytes);
     std::vector<double> vals(static_cast<std::size_t>(nnz));
     for (index_t j = 0; j < x->cols; ++j) {
       const index_t lo = x->col_ptr[j], hi = x->col_ptr[j + 1];

@@ -14,6 +14,9 @@
 // the gathered W / U rows are read as coalesced, row-major, 8-byte vectors.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "kernels.cuh"
 
 namespace lpca {
@@ -148,6 +151,122 @@ void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, c
     gemm_t_csc_kernel<8><<<g, 32 * kWarpsPerBlock, 0, s>>>(n, col_ptr, row, val, u, ldu, li, f, accumulate);
   else
     gemm_t_csc_kernel<16><<<g, 32 * kWarpsPerBlock, 0, s>>>(n, col_ptr, row, val, u, ldu, li, f, accumulate);
+}
+
+// ---- CSC staging on the device (stage_x) ------------------------------------------
+// A host CSC crosses PCIe as the caller holds it (int64 col_ptr / row_idx,
+// fp32 or fp64 values); validation, the 32-bit row indices, fp64 values and
+// the CSR copy are built here instead of by a serial host pass (a 1.2G-entry
+// X took ~50 s on the host, most of it the CSR counting sort's scattered
+// writes). Validation keeps the host loop's order: the first entry p (column
+// major) failing any check, and for that entry the first check in the order
+// range, strictly increasing, explicit zero, non-finite (first = 4 p + code).
+namespace {
+template <typename T>
+__global__ void csc_check_kernel(index_t n, index_t rows, const std::int64_t* __restrict__ cp,
+                                 const std::int64_t* __restrict__ ri64, const T* __restrict__ val,
+                                 std::int32_t* __restrict__ ri, std::int32_t* __restrict__ colof,
+                                 double* __restrict__ cv, unsigned long long* first) {
+  const int lane = threadIdx.x & 31;
+  for (index_t j = blockIdx.x * static_cast<index_t>(kWarpsPerBlock) + threadIdx.x / 32; j < n;
+       j += static_cast<index_t>(gridDim.x) * kWarpsPerBlock) {
+    const std::int64_t lo = cp[j], hi = cp[j + 1];
+    for (std::int64_t p = lo + lane; p < hi; p += 32) {
+      const std::int64_t r = ri64[p];
+      const double v = static_cast<double>(val[p]);
+      int code = -1;
+      if (r < 0 || r >= rows) code = 0;
+      else if (p > lo && r <= ri64[p - 1]) code = 1;
+      else if (v == 0.0) code = 2;
+      else if (!isfinite(v)) code = 3;
+      if (code >= 0) atomicMin(first, static_cast<unsigned long long>(p) * 4ull + static_cast<unsigned>(code));
+      ri[p] = static_cast<std::int32_t>(r);
+      colof[p] = static_cast<std::int32_t>(j);
+      cv[p] = v;
+    }
+  }
+}
+
+__global__ void row_count_kernel(index_t nnz, const std::int32_t* __restrict__ ri, std::int64_t* __restrict__ cnt) {
+  for (index_t p = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; p < nnz;
+       p += static_cast<index_t>(gridDim.x) * blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long*>(cnt + ri[p]), 1ull);
+}
+
+__global__ void csr_gather_kernel(index_t nnz, const std::int32_t* __restrict__ perm,
+                                  const std::int32_t* __restrict__ colof, const double* __restrict__ cv,
+                                  std::int32_t* __restrict__ ci, double* __restrict__ rv) {
+  for (index_t q = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; q < nnz;
+       q += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    const std::int32_t p = perm[q];
+    ci[q] = colof[p];
+    rv[q] = cv[p];
+  }
+}
+
+__global__ void iota_kernel(index_t nnz, std::int32_t* __restrict__ out) {
+  for (index_t q = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; q < nnz;
+       q += static_cast<index_t>(gridDim.x) * blockDim.x)
+    out[q] = static_cast<std::int32_t>(q);
+}
+
+unsigned grid_flat(index_t count) {
+  index_t g = ceil_div(count, 256);
+  if (g > 148 * 32) g = 148 * 32;
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+int row_bits(index_t m) {
+  int b = 1;
+  while (b < 31 && (index_t(1) << b) < m) ++b;
+  return b;
+}
+}  // namespace
+
+std::size_t csc_stage_temp_bytes(index_t m, index_t nnz) {
+  std::size_t sort_b = 0, scan_b = 0;
+  const int n32 = static_cast<int>(nnz);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, static_cast<const std::int32_t*>(nullptr),
+                                  static_cast<std::int32_t*>(nullptr), static_cast<const std::int32_t*>(nullptr),
+                                  static_cast<std::int32_t*>(nullptr), n32, 0, row_bits(m));
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_b, static_cast<std::int64_t*>(nullptr),
+                                static_cast<std::int64_t*>(nullptr), static_cast<int>(m + 1));
+  return sort_b > scan_b ? sort_b : scan_b;
+}
+
+void launch_csc_check(cudaStream_t s, index_t n, index_t rows, const std::int64_t* cp, const std::int64_t* ri64,
+                      const void* val, int dtype, std::int32_t* ri, std::int32_t* colof, double* cv,
+                      unsigned long long* first) {
+  if (n <= 0) return;
+  LPCA_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), s));
+  const unsigned g = grid_rows(n);
+  if (dtype == 4)
+    csc_check_kernel<float><<<g, 32 * kWarpsPerBlock, 0, s>>>(n, rows, cp, ri64, static_cast<const float*>(val), ri,
+                                                              colof, cv, first);
+  else
+    csc_check_kernel<double><<<g, 32 * kWarpsPerBlock, 0, s>>>(n, rows, cp, ri64, static_cast<const double*>(val),
+                                                               ri, colof, cv, first);
+}
+
+// CSR from the checked CSC: a stable radix sort of the entries by row keeps
+// each row's columns ascending (the reference's accumulation order, as the
+// host counting sort did); row offsets by a histogram and an exclusive scan.
+// cnt: m + 1 int64; keys_out / perm_in / perm_out: nnz int32 each; temp:
+// csc_stage_temp_bytes.
+void launch_csr_from_csc(cudaStream_t s, index_t m, index_t nnz, const std::int32_t* ri, const std::int32_t* colof,
+                         const double* cv, std::int64_t* rp, std::int32_t* ci, double* rv, std::int64_t* cnt,
+                         std::int32_t* keys_out, std::int32_t* perm_in, std::int32_t* perm_out, void* temp,
+                         std::size_t temp_bytes) {
+  LPCA_CUDA(cudaMemsetAsync(cnt, 0, sizeof(std::int64_t) * static_cast<std::size_t>(m + 1), s));
+  if (nnz > 0) row_count_kernel<<<grid_flat(nnz), 256, 0, s>>>(nnz, ri, cnt);
+  std::size_t tb = temp_bytes;
+  LPCA_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, cnt, rp, static_cast<int>(m + 1), s));
+  if (nnz <= 0) return;
+  iota_kernel<<<grid_flat(nnz), 256, 0, s>>>(nnz, perm_in);
+  tb = temp_bytes;
+  LPCA_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, ri, keys_out, perm_in, perm_out, static_cast<int>(nnz), 0,
+                                            row_bits(m), s));
+  csr_gather_kernel<<<grid_flat(nnz), 256, 0, s>>>(nnz, perm_out, colof, cv, ci, rv);
 }
 
 }  // namespace lpca

@@ -1,0 +1,82 @@
+"""GPU: a host CSC view is checked and turned into the device CSR/CSC copies by
+kernels (csrc/sparse.cu, stage_csc_device in csrc/lpca.cu). The errors must be
+the reference's SparseMatrix::from_csc errors (sparse_matrix.cpp:50-80) — same
+class, same message, same column — including which one wins when a view has
+several: the first entry in column-major order, for that entry the first check
+(range, strictly increasing, explicit zero, non-finite), and a decreasing
+col_ptr only after every entry of the columns before it. The reference raises
+them through oracle/ref_capi.cpp's ref_fit_transform_csc."""
+import numpy as np
+import pytest
+
+import paper_1709_07175_b200 as lp
+
+pytestmark = pytest.mark.gpu
+
+M, N = 40, 30
+
+
+def _valid():
+    rng = np.random.default_rng(8)
+    d = rng.uniform(0.5, 1.5, (M, N)) * (rng.random((M, N)) < 0.1)
+    d[0, :] = 1.0  # every column non-empty
+    s = lp.SparseMatrix.from_dense(d)
+    return s.col_ptr.copy(), s.row_idx.copy(), s.values.copy()
+
+
+def _entry(cp, j, t=1):
+    """index of the t-th entry of column j"""
+    assert cp[j + 1] - cp[j] > t
+    return cp[j] + t
+
+
+def _cases():
+    out = {}
+    cp, ri, va = _valid()
+    r = ri.copy(); r[_entry(cp, 3)] = M + 2
+    out["row out of range"] = (cp, r, va)
+    r = ri.copy(); p = _entry(cp, 2); r[p] = r[p - 1]
+    out["rows not increasing"] = (cp, r, va)
+    v = va.copy(); v[_entry(cp, 4)] = 0.0
+    out["explicit zero"] = (cp, ri, v)
+    v = va.copy(); v[_entry(cp, 1)] = np.nan
+    out["non-finite"] = (cp, ri, v)
+    c = cp.copy(); c[5] = c[4] - 1  # column 4's range runs backwards
+    out["col_ptr decreasing"] = (c, ri, va)
+    c = cp.copy(); c[4] = c[5] + 1  # column 3's range runs into column 4's rows first
+    out["col_ptr overlapping the next column"] = (c, ri, va)
+    c = cp.copy(); c[4] = c[5] + 1
+    v = va.copy(); v[_entry(cp, 1)] = 0.0  # an entry error in an earlier column wins
+    out["entry error before a bad col_ptr"] = (c, ri, v)
+    r = ri.copy(); r[_entry(cp, 1)] = -1
+    v = va.copy(); v[_entry(cp, 2)] = 0.0
+    out["first of two entry errors"] = (cp, r, v)
+    r = ri.copy(); p = _entry(cp, 5); r[p] = r[p - 1]
+    v = va.copy(); v[p] = 0.0  # one entry failing two checks: the increasing check first
+    out["one entry, two checks"] = (cp, r, v)
+    return out
+
+
+CASES = _cases()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_csc_errors_match_the_reference(ctx, ref, name):
+    cp, ri, va = CASES[name]
+    with pytest.raises(Exception) as want:
+        ref.fit_transform_csc(2, M, N, cp, ri, va, 4, 6, 3)
+    x = lp.SparseMatrix(M, N, cp, ri, va)
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=4, l=6, projection=lp.ProjectionSpec(seed=3))
+    with pytest.raises(lp.Error) as got:
+        lp.reduce(x, cfg, ctx=ctx)
+    assert str(got.value) == str(want.value)
+    assert type(got.value) is {1: lp.DimensionError, 2: lp.InvalidArgumentError}[want.value.code]
+
+
+def test_valid_csc_fit_equals_the_reference(ctx, ref):
+    cp, ri, va = _valid()
+    _, v_ref, s_ref, _ = ref.fit_transform_csc(2, M, N, cp, ri, va, 4, 6, 3, want_y=False)
+    x = lp.SparseMatrix(M, N, cp, ri, va)
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=4, l=6, projection=lp.ProjectionSpec(seed=3))
+    got = lp.reduce(x, cfg, ctx=ctx)
+    assert np.max(np.abs(got.singular_values - s_ref) / s_ref) < 1e-12

@@ -64,6 +64,13 @@ void launch_spmm_csr(cudaStream_t s, index_t m, const std::int64_t* row_ptr, con
                      const double* val, const double* wt, index_t ldw, index_t w, void* out, int out_dtype,
                      index_t ors, index_t ocs);
 // F (l x n column-major) (+)= U^T X with X in CSC and U row-major m x l (ld ldu), l <= 512.
+// Sparse X times a {-1, 0, +1} W (very sparse Omega) from per-row bit masks of
+// W (sparse.cu): bitwise the dense-W spmm_csr. masks: n * 2 * pm1_mask_words(l).
+int pm1_mask_words(index_t l);
+void launch_pm1_masks(cudaStream_t s, const double* w, index_t n, index_t l, index_t ldw, std::uint32_t* masks);
+void launch_spmm_csr_pm1(cudaStream_t s, index_t m, const std::int64_t* row_ptr, const std::int32_t* col,
+                         const double* val, const std::uint32_t* masks, index_t w, double* out, index_t ors,
+                         index_t ocs);
 // Device staging of a host CSC (sparse.cu): checks in the host loop's order
 // (first = 4 p + code of the first failing entry, ~0 if none), 32-bit rows,
 // column of each entry, fp64 values; then the CSR copy by a stable row sort.

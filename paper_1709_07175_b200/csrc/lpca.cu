@@ -1441,6 +1441,16 @@ lpca_map* fit_dev(lpca_ctx& ctx, const lpca_config& cfg_in, const DevX& x, lpca_
       }
       LPCA_LAUNCHED(ctx);
       ev.mark(13);
+    } else if (x.sparse() && c.projection_kind == LPCA_VERY_SPARSE && so_mode != 0 && l <= 512) {
+      // sparse X, very sparse Omega: W's rows as sign bit masks (csrc/sparse.cu),
+      // bitwise the dense-W gather with 1/25 of its L2 reads at l = 100
+      auto* masks = ctx.get<std::uint32_t>("so.masks", n * 2 * pm1_mask_words(l));
+      launch_pm1_masks(ctx.stream, omega, n, l, n, masks);
+      LPCA_LAUNCHED(ctx);
+      ev.mark(12);
+      launch_spmm_csr_pm1(ctx.stream, m, x.rp, x.ci, x.rv, masks, l, static_cast<double*>(u.plain), u.ld, 1);
+      LPCA_LAUNCHED(ctx);
+      ev.mark(13);
     } else {
       ctx.pass_slot = 12;
       xw_pass(ctx, x, omega, l, n, u, exact, f16 ? &sketch : nullptr);

@@ -153,6 +153,101 @@ void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, c
     gemm_t_csc_kernel<16><<<g, 32 * kWarpsPerBlock, 0, s>>>(n, col_ptr, row, val, u, ldu, li, f, accumulate);
 }
 
+// ---- sparse X times a {-1, 0, +1} W (the very sparse Omega, unscaled) -------------
+// The dense-W gather reads W's whole row (8 l bytes) per nonzero of X, from L2
+// (a 1.19G-nonzero X at l = 100: 0.95 TB of L2 reads per sketch). For a sign
+// pattern each row of W is two bit masks, nonzero and negative, of
+// wpad (multiple of 4) words: 32 B per row at l <= 128. The sums are the
+// dense kernel's bit for bit: v * (+-1) is exactly +-v, and zero entries of W
+// are skipped there too.
+namespace {
+__global__ void pm1_masks_kernel(const double* __restrict__ w, index_t n, int l, index_t ldw, int wpad,
+                                 std::uint32_t* __restrict__ masks) {
+  const index_t cells = n * wpad;
+  for (index_t e = blockIdx.x * static_cast<index_t>(blockDim.x) + threadIdx.x; e < cells;
+       e += static_cast<index_t>(gridDim.x) * blockDim.x) {
+    const index_t j = e / wpad;
+    const int t = static_cast<int>(e % wpad);
+    std::uint32_t nz = 0, ng = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int c = 32 * t + b;
+      if (c >= l) break;
+      const double v = w[static_cast<index_t>(c) * ldw + j];
+      if (v != 0.0) nz |= 1u << b;
+      if (v < 0.0) ng |= 1u << b;
+    }
+    masks[j * 2 * wpad + t] = nz;
+    masks[j * 2 * wpad + wpad + t] = ng;
+  }
+}
+
+template <int kPer, typename TO>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    spmm_csr_pm1_kernel(index_t m, const std::int64_t* __restrict__ row_ptr, const std::int32_t* __restrict__ col,
+                        const double* __restrict__ val, const std::uint32_t* __restrict__ masks, int wpad, int w,
+                        TO* __restrict__ out, index_t ors, index_t ocs) {
+  const int lane = threadIdx.x & 31;
+  for (index_t i = blockIdx.x * static_cast<index_t>(kWarpsPerBlock) + threadIdx.x / 32; i < m;
+       i += static_cast<index_t>(gridDim.x) * kWarpsPerBlock) {
+    double acc[kPer];
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) acc[t] = 0.0;
+    const std::int64_t p1 = row_ptr[i + 1];
+    for (std::int64_t p = row_ptr[i]; p < p1; ++p) {
+      const double v = __ldg(val + p);
+      const uint4* mr = reinterpret_cast<const uint4*>(masks + static_cast<index_t>(__ldg(col + p)) * 2 * wpad);
+      std::uint32_t nz[kPer], ng[kPer];
+#pragma unroll
+      for (int q = 0; q < (kPer + 3) / 4; ++q) {
+        const uint4 a = __ldg(mr + q), b = __ldg(mr + wpad / 4 + q);
+        const std::uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (4 * q + r < kPer) {
+            nz[4 * q + r] = av[r];
+            ng[4 * q + r] = bv[r];
+          }
+      }
+#pragma unroll
+      for (int t = 0; t < kPer; ++t)
+        if ((nz[t] >> lane) & 1u) acc[t] = __dadd_rn(acc[t], ((ng[t] >> lane) & 1u) ? -v : v);
+    }
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int c = lane + 32 * t;
+      if (c < w) out[i * ors + static_cast<index_t>(c) * ocs] = static_cast<TO>(acc[t]);
+    }
+  }
+}
+}  // namespace
+
+int pm1_mask_words(index_t l) { return static_cast<int>(((l + 31) / 32 + 3) / 4 * 4); }
+
+void launch_pm1_masks(cudaStream_t s, const double* w, index_t n, index_t l, index_t ldw, std::uint32_t* masks) {
+  if (n <= 0) return;
+  const int wpad = pm1_mask_words(l);
+  pm1_masks_kernel<<<static_cast<unsigned>(ceil_div(n * wpad, 256) < 148 * 32 ? ceil_div(n * wpad, 256) : 148 * 32), 256, 0, s>>>(w, n, static_cast<int>(l), ldw, wpad, masks);
+}
+
+void launch_spmm_csr_pm1(cudaStream_t s, index_t m, const std::int64_t* row_ptr, const std::int32_t* col,
+                         const double* val, const std::uint32_t* masks, index_t w, double* out, index_t ors,
+                         index_t ocs) {
+  if (m <= 0 || w <= 0) return;
+  if (w > 512) throw Error(kInvalidArgument, "sparse spmm (sign W): at most 512 output columns");
+  const unsigned g = grid_rows(m);
+  const int wp = pm1_mask_words(w), wi = static_cast<int>(w);
+  if (w <= 32)
+    spmm_csr_pm1_kernel<1, double><<<g, 32 * kWarpsPerBlock, 0, s>>>(m, row_ptr, col, val, masks, wp, wi, out, ors, ocs);
+  else if (w <= 64)
+    spmm_csr_pm1_kernel<2, double><<<g, 32 * kWarpsPerBlock, 0, s>>>(m, row_ptr, col, val, masks, wp, wi, out, ors, ocs);
+  else if (w <= 128)
+    spmm_csr_pm1_kernel<4, double><<<g, 32 * kWarpsPerBlock, 0, s>>>(m, row_ptr, col, val, masks, wp, wi, out, ors, ocs);
+  else if (w <= 256)
+    spmm_csr_pm1_kernel<8, double><<<g, 32 * kWarpsPerBlock, 0, s>>>(m, row_ptr, col, val, masks, wp, wi, out, ors, ocs);
+  else
+    spmm_csr_pm1_kernel<16, double><<<g, 32 * kWarpsPerBlock, 0, s>>>(m, row_ptr, col, val, masks, wp, wi, out, ors, ocs);
+}
+
 // ---- CSC staging on the device (stage_x) ------------------------------------------
 // A host CSC crosses PCIe as the caller holds it (int64 col_ptr / row_idx,
 // fp32 or fp64 values); validation, the 32-bit row indices, fp64 values and

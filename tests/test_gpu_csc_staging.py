@@ -80,3 +80,31 @@ def test_valid_csc_fit_equals_the_reference(ctx, ref):
     cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=4, l=6, projection=lp.ProjectionSpec(seed=3))
     got = lp.reduce(x, cfg, ctx=ctx)
     assert np.max(np.abs(got.singular_values - s_ref) / s_ref) < 1e-12
+
+
+@pytest.mark.parametrize("l", [20, 100, 150])
+def test_very_sparse_omega_on_sparse_x_matches_the_reference(ctx, ref, l):
+    """The sign-mask sketch (spmm_csr_pm1) sums each U[i][c] over the row's
+    nonzeros in ascending j like the reference's spmm(CSC, CSC)
+    (kernels.cpp:49-68): with the exact-order passes the map equals the
+    reference's to eigensolver roundoff and Y bitwise."""
+    rng = np.random.default_rng(31)
+    m, n, k = 3000, 2000, l // 2
+    d = rng.uniform(0.5, 1.5, (m, n)) * (rng.random((m, n)) < 0.0244)
+    xs = lp.SparseMatrix.from_dense(d)
+    dens = lp.density_for(lp.DensityPolicy.aggressive(), l)
+    y_ref, v_ref, s_ref, _ = ref.fit_transform_csc(2, m, n, xs.col_ptr, xs.row_idx, xs.values, k, l, 5, kind=1,
+                                                   density=dens)
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=k, l=l,
+                           projection=lp.ProjectionSpec(kind=lp.ProjectionKind.very_sparse, density=dens, seed=5))
+    ctx.set_exact_order(True)
+    try:
+        mp = lp.reduce(xs, cfg, ctx=ctx)
+        y = lp.apply_map(mp, xs, ctx=ctx)
+    finally:
+        ctx.set_exact_order(False)
+    assert np.max(np.abs(mp.singular_values - s_ref) / s_ref) < 1e-13
+    kk = k // 2
+    from oracle import lazypca_oracle as O
+    assert np.max(O.principal_angles(mp.v[:, :kk], v_ref[:, :kk])) < 1e-10
+    assert np.array_equal(y, ref.apply_map(d, mp.v))

@@ -381,13 +381,16 @@ void check_view(const lpca_matrix_view* x) {
   }
 }
 
-// A sparse CSC view staged on the device (csrc/sparse.cu): col_ptr, row_idx and
-// the values cross PCIe as the caller holds them; the entries are checked, the
-// indices narrowed and the CSR copy built by kernels. Errors are the host
-// loop's, in its order: the first column whose col_ptr decreases is found
-// here, and an entry error in an earlier column wins over it (the device
-// checks exactly those columns).
-DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes) {
+// A CSC view staged on the device (csrc/sparse.cu): col_ptr, row_idx and the
+// values cross PCIe as the caller holds them; the entries are checked and the
+// indices narrowed by a kernel, then either the CSR copy is built (the sparse
+// path) or X is densified into a row-major matrix of its own dtype (denser
+// inputs, for the tensor-core passes). Errors are the host loop's, in its
+// order: the first column whose col_ptr decreases is found here, and an entry
+// error in an earlier column wins over it (the device checks exactly those
+// columns).
+DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes,
+                      bool densify) {
   const index_t m = x->rows, n = x->cols, nnz = x->nnz;
   const std::size_t es = dsize(x->dtype), nz = static_cast<std::size_t>(nnz > 0 ? nnz : 1);
   index_t bad_col = -1;  // the first column whose col_ptr decreases
@@ -398,20 +401,18 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   auto* cp = ctx.get<std::int64_t>(sl + ".cp", n + 1);
   auto* ri = ctx.get<std::int32_t>(sl + ".ri", nz);
   auto* cv = ctx.get<double>(sl + ".cv", nz);
-  auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
-  auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
-  auto* rv = ctx.get<double>(sl + ".rv", nz);
   auto* first = ctx.get<unsigned long long>(sl + ".first", 1);
   // scratch (one cached workspace, reused by later calls of the same shape):
   // the caller's 64-bit rows and values, each entry's column, the sort's keys
   // and permutations, the row counts, CUB's temp. (A stream-ordered allocation
   // returned its tens of GB to the driver at every call: 2-6 s of remapping.)
   const index_t nin = bad_col >= 0 ? x->col_ptr[bad_col] : nnz;  // entries of the checked columns
-  const std::size_t tb = csc_stage_temp_bytes(m, nnz);
+  const std::size_t tb = densify ? 0 : csc_stage_temp_bytes(m, nnz);
   auto a16 = [](std::size_t b) { return (b + 15) & ~std::size_t(15); };
   const std::size_t off_v = a16(nz * 8), off_c = off_v + a16(nz * es), off_k = off_c + a16(nz * 4),
                     off_p0 = off_k + a16(nz * 4), off_p1 = off_p0 + a16(nz * 4), off_n = off_p1 + a16(nz * 4),
-                    off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)), total = off_t + tb;
+                    off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)),
+                    total = densify ? off_k : off_t + tb;  // densify: the caller's arrays and colof only
   char* tmp = ctx.get<char>(sl + ".stage", total);
   auto* ri64 = reinterpret_cast<std::int64_t*>(tmp);
   void* vin = tmp + off_v;
@@ -439,10 +440,26 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
     if (code == 2) throw Error(kInvalidArgument, "csc: explicit zero stored in column " + S(j));
     throw Error(kInvalidArgument, "csc: non-finite value in column " + S(j));
   }
+  if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz) * static_cast<double>(8 + es) + static_cast<double>(n + 1) * 8;
+  if (densify) {
+    DevX d;
+    d.m = m;
+    d.n = n;
+    d.dtype = x->dtype;
+    void* dst = ctx.buf(slot, es * m * n);
+    launch_zero(ctx.stream, dst, es * m * n);
+    launch_csc_to_dense(ctx.stream, m, n, cp, ri64, cv, d.dtype, dst, n);
+    LPCA_LAUNCHED(ctx);
+    d.p = dst;
+    d.ld = n;
+    return d;
+  }
+  auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
+  auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
+  auto* rv = ctx.get<double>(sl + ".rv", nz);
   launch_csr_from_csc(ctx.stream, m, nnz, ri, colof, cv, rp, ci, rv, cnt, keys, perm0, perm1, tmp + off_t, tb);
   ctx.note_launch(3);  // row counts, iota, gather (+ CUB's scan and radix sort)
   LPCA_CUDA(cudaGetLastError());
-  if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz) * static_cast<double>(8 + es) + static_cast<double>(n + 1) * 8;
   DevX d;
   d.m = m;
   d.n = n;
@@ -478,7 +495,7 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
     // canonical-form checks of SparseMatrix::from_csc (sparse_matrix.cpp:50-80)
     if (x->col_ptr[0] != 0) throw Error(kInvalidArgument, "csc: col_ptr[0] must be 0");
     if (x->col_ptr[x->cols] != nnz) throw Error(kDimension, "csc: col_ptr[cols] must equal nnz");
-    if (keep_sparse(nnz, x->rows, x->cols) && nnz < (index_t(1) << 31)) return stage_csc_device(ctx, x, slot, h2d_bytes);
+    if (nnz < (index_t(1) << 31)) return stage_csc_device(ctx, x, slot, h2d_bytes, !keep_sparse(nnz, x->rows, x->cols));
     std::vector<double> vals(static_cast<std::size_t>(nnz));
     for (index_t j = 0; j < x->cols; ++j) {
       const index_t lo = x->col_ptr[j], hi = x->col_ptr[j + 1];

@@ -60,8 +60,10 @@ def _cases():
 CASES = _cases()
 
 
+@pytest.mark.parametrize("sparse", ["1", "0"])  # kept sparse (CSR built) / densified
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_csc_errors_match_the_reference(ctx, ref, name):
+def test_csc_errors_match_the_reference(ctx, ref, name, sparse, monkeypatch):
+    monkeypatch.setenv("LPCA_SPARSE", sparse)
     cp, ri, va = CASES[name]
     with pytest.raises(Exception) as want:
         ref.fit_transform_csc(2, M, N, cp, ri, va, 4, 6, 3)

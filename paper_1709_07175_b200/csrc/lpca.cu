@@ -226,6 +226,17 @@ struct lpca_ctx {
   T* get(const std::string& name, std::size_t count) {
     return static_cast<T*>(buf(name, count * sizeof(T)));
   }
+  std::size_t cached(const std::string& name) const {
+    auto it = ws.find(name);
+    return it == ws.end() ? 0 : it->second.second;
+  }
+  void release(const std::string& name) {
+    auto it = ws.find(name);
+    if (it == ws.end()) return;
+    LPCA_CUDA(cudaStreamSynchronize(stream));
+    LPCA_CUDA(cudaFree(it->second.first));
+    ws.erase(it);
+  }
   void allreduce(double* p, index_t count) {
     if (world <= 1 && !comm) return;  // (a one-rank communicator still runs: the NCCL path on one GPU)
     if (hook) {
@@ -389,8 +400,10 @@ void check_view(const lpca_matrix_view* x) {
 // order: the first column whose col_ptr decreases is found here, and an entry
 // error in an earlier column wins over it (the device checks exactly those
 // columns).
-DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes,
-                      bool densify) {
+// Returns false (nothing staged) when the device scratch (~32 B per entry)
+// does not fit the free memory: the host path below then does the same work.
+bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes,
+                      bool densify, DevX& out) {
   const index_t m = x->rows, n = x->cols, nnz = x->nnz;
   const std::size_t es = dsize(x->dtype), nz = static_cast<std::size_t>(nnz > 0 ? nnz : 1);
   index_t bad_col = -1;  // the first column whose col_ptr decreases
@@ -413,6 +426,14 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
                     off_p0 = off_k + a16(nz * 4), off_p1 = off_p0 + a16(nz * 4), off_n = off_p1 + a16(nz * 4),
                     off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)),
                     total = densify ? off_k : off_t + tb;  // densify: the caller's arrays and colof only
+  if (ctx.cached(sl + ".stage") < total) {
+    ctx.release(sl + ".stage");
+    std::size_t free_b = 0, total_b = 0;
+    LPCA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const std::size_t outputs = densify ? dsize(x->dtype) * static_cast<std::size_t>(m) * static_cast<std::size_t>(n)
+                                        : nz * 12 + 8 * static_cast<std::size_t>(m + 1);
+    if (total + outputs + (std::size_t(1) << 30) > free_b) return false;
+  }
   char* tmp = ctx.get<char>(sl + ".stage", total);
   auto* ri64 = reinterpret_cast<std::int64_t*>(tmp);
   void* vin = tmp + off_v;
@@ -441,6 +462,12 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
     throw Error(kInvalidArgument, "csc: non-finite value in column " + S(j));
   }
   if (h2d_bytes) *h2d_bytes += static_cast<double>(nnz) * static_cast<double>(8 + es) + static_cast<double>(n + 1) * 8;
+  // the scratch stays cached for the next call unless memory is tight
+  auto keep_or_release_scratch = [&]() {
+    std::size_t free_b = 0, total_b = 0;
+    LPCA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (free_b < total_b / 4) ctx.release(sl + ".stage");
+  };
   if (densify) {
     DevX d;
     d.m = m;
@@ -452,7 +479,9 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
     LPCA_LAUNCHED(ctx);
     d.p = dst;
     d.ld = n;
-    return d;
+    keep_or_release_scratch();
+    out = d;
+    return true;
   }
   auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
   auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
@@ -460,6 +489,7 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   launch_csr_from_csc(ctx.stream, m, nnz, ri, colof, cv, rp, ci, rv, cnt, keys, perm0, perm1, tmp + off_t, tb);
   ctx.note_launch(3);  // row counts, iota, gather (+ CUB's scan and radix sort)
   LPCA_CUDA(cudaGetLastError());
+  keep_or_release_scratch();
   DevX d;
   d.m = m;
   d.n = n;
@@ -472,7 +502,8 @@ DevX stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   d.ri = ri;
   d.cv = cv;
   d.nnz = nnz;
-  return d;
+  out = d;
+  return true;
 }
 
 // Brings any view to a row-major device matrix of its own dtype. Host data is
@@ -495,7 +526,11 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
     // canonical-form checks of SparseMatrix::from_csc (sparse_matrix.cpp:50-80)
     if (x->col_ptr[0] != 0) throw Error(kInvalidArgument, "csc: col_ptr[0] must be 0");
     if (x->col_ptr[x->cols] != nnz) throw Error(kDimension, "csc: col_ptr[cols] must equal nnz");
-    if (nnz < (index_t(1) << 31)) return stage_csc_device(ctx, x, slot, h2d_bytes, !keep_sparse(nnz, x->rows, x->cols));
+    DevX dd;
+    const char* host_env = std::getenv("LPCA_CSC_HOST");  // tests: force the host staging below
+    if (nnz < (index_t(1) << 31) && !(host_env && host_env[0] == '1') &&
+        stage_csc_device(ctx, x, slot, h2d_bytes, !keep_sparse(nnz, x->rows, x->cols), dd))
+      return dd;
     std::vector<double> vals(static_cast<std::size_t>(nnz));
     for (index_t j = 0; j < x->cols; ++j) {
       const index_t lo = x->col_ptr[j], hi = x->col_ptr[j + 1];

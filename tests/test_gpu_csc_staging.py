@@ -60,10 +60,12 @@ def _cases():
 CASES = _cases()
 
 
+@pytest.mark.parametrize("host", ["0", "1"])  # device staging / the host fallback (too little memory)
 @pytest.mark.parametrize("sparse", ["1", "0"])  # kept sparse (CSR built) / densified
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_csc_errors_match_the_reference(ctx, ref, name, sparse, monkeypatch):
+def test_csc_errors_match_the_reference(ctx, ref, name, sparse, host, monkeypatch):
     monkeypatch.setenv("LPCA_SPARSE", sparse)
+    monkeypatch.setenv("LPCA_CSC_HOST", host)
     cp, ri, va = CASES[name]
     with pytest.raises(Exception) as want:
         ref.fit_transform_csc(2, M, N, cp, ri, va, 4, 6, 3)
@@ -75,7 +77,9 @@ def test_csc_errors_match_the_reference(ctx, ref, name, sparse, monkeypatch):
     assert type(got.value) is {1: lp.DimensionError, 2: lp.InvalidArgumentError}[want.value.code]
 
 
-def test_valid_csc_fit_equals_the_reference(ctx, ref):
+@pytest.mark.parametrize("host", ["0", "1"])
+def test_valid_csc_fit_equals_the_reference(ctx, ref, host, monkeypatch):
+    monkeypatch.setenv("LPCA_CSC_HOST", host)
     cp, ri, va = _valid()
     _, v_ref, s_ref, _ = ref.fit_transform_csc(2, M, N, cp, ri, va, 4, 6, 3, want_y=False)
     x = lp.SparseMatrix(M, N, cp, ri, va)

@@ -12,7 +12,6 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-import math
 from dataclasses import dataclass, field
 from typing import Optional
 

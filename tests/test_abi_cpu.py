@@ -2,7 +2,6 @@
 its pure-host entry points (config resolution, density policy) behave like the
 reference. No compute call runs here (there is no GPU); creating a context must
 fail loudly rather than fall back to the CPU."""
-import ctypes as C
 import re
 from pathlib import Path
 

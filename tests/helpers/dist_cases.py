@@ -18,6 +18,11 @@ CASES = {
     # fp32, a very sparse Omega on long rows: the row gather on each rank
     "lazy_f32_row_gather": dict(method=M.lazy_spca, k=16, l=40, q=1, m=4096, n=9000, dtype="f32",
                                 very_sparse=1.0 / 90),
+    # sparse X (CSC, the device-staged CSR/CSC path) on each rank; the second
+    # with a very sparse Omega (the sign-mask sketch)
+    "sparse_lazy_q1": dict(method=M.lazy_spca, k=8, l=16, q=1, m=3000, n=300, dtype="f64", sparse=0.05),
+    "sparse_lazy_vs_omega": dict(method=M.lazy_spca, k=8, l=16, m=3000, n=300, dtype="f64", sparse=0.05,
+                                 very_sparse=1.0 / 17),
     # streaming reducers (Algorithms 4 and 3) over each rank's blocks
     "stream_lazy": dict(method=M.lazy_spca, k=8, l=16, m=3000, n=300, dtype="f64", stream=True, block_rows=700),
     "stream_spca": dict(method=M.spca, k=8, l=16, m=3000, n=300, dtype="f64", stream=True, block_rows=700),
@@ -39,7 +44,15 @@ def case_data(name):
             x[:, c0:c0 + 64] = rng.standard_normal((c["m"], 64)).astype(np.float32) * 1e-3
         return x
     dt = np.float32 if c["dtype"] == "f32" else np.float64
-    return O.synth_lowrank(0, c["m"], c["n"], 30, 0.93, 0.01, 17, dtype=dt)
+    x = O.synth_lowrank(0, c["m"], c["n"], 30, 0.93, 0.01, 17, dtype=dt)
+    if c.get("sparse"):
+        x = x * (np.random.default_rng(19).random(x.shape) < c["sparse"])
+    return x
+
+
+def as_input(c, x):
+    """The case's X as the reducers take it: a CSC SparseMatrix for sparse cases."""
+    return lp.SparseMatrix.from_dense(x) if c.get("sparse") else x
 
 
 def shard(c, m, world, rank):

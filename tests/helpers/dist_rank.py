@@ -17,7 +17,7 @@ import paper_1709_07175_b200 as lp  # noqa: E402
 from cuda.bindings import runtime as cudart  # noqa: E402
 
 sys.path.insert(0, str(ROOT / "tests" / "helpers"))
-from dist_cases import CASES, case_data, projection, shard  # noqa: E402
+from dist_cases import CASES, as_input, case_data, projection, shard  # noqa: E402
 
 
 def main():
@@ -65,6 +65,8 @@ def main():
                 fn = lp.reduce_spca_streaming if c["method"] == lp.ReducerMethod.spca else lp.reduce_lazy_spca_streaming
                 mp = fn(blocks, cfg, ctx=ctx)
                 y = None
+            elif c.get("sparse"):
+                mp, y = lp.fit_transform(as_input(c, np.ascontiguousarray(x[lo:hi])), cfg, ctx=ctx)
             else:
                 mp, y = lp.fit_transform(xs, cfg, ctx=ctx)
             results[name + ".v"] = mp.v

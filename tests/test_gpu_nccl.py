@@ -18,7 +18,7 @@ import paper_1709_07175_b200 as lp
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "tests" / "helpers"))
-from dist_cases import CASES, case_data, projection  # noqa: E402
+from dist_cases import CASES, as_input, case_data, projection  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -40,6 +40,8 @@ def _fit(ctx, name):
     if c.get("stream"):
         fn = lp.reduce_spca_streaming if c["method"] == lp.ReducerMethod.spca else lp.reduce_lazy_spca_streaming
         return fn(lp.SliceRowBlockStream(x, c["block_rows"]), cfg, ctx=ctx), None
+    if c.get("sparse"):
+        return lp.fit_transform(as_input(c, x), cfg, ctx=ctx)
     mp, y = lp.fit_transform(torch.from_numpy(x).cuda(), cfg, ctx=ctx)
     return mp, y
 

@@ -39,16 +39,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 #pragma unroll
     for (int t = 0; t < kPer; ++t) acc[t] = 0.0;
     const std::int64_t p1 = row_ptr[i + 1];
-    for (std::int64_t p = row_ptr[i]; p < p1; ++p) {
-      const double v = __ldg(val + p);
-      const double* wr = wt + static_cast<index_t>(__ldg(col + p)) * ldw;
+    // the row's (column, value) pairs 32 at a time, one per lane; kU nonzeros'
+    // W rows loaded together, then added in ascending p (the reference's order)
+    constexpr int kU = kPer <= 4 ? 4 : (kPer <= 8 ? 2 : 1);
+    for (std::int64_t p0 = row_ptr[i]; p0 < p1; p0 += 32) {
+      const int cnt = p1 - p0 < 32 ? static_cast<int>(p1 - p0) : 32;
+      const int cj = lane < cnt ? __ldg(col + p0 + lane) : 0;
+      const double cv = lane < cnt ? __ldg(val + p0 + lane) : 0.0;
+      for (int q0 = 0; q0 < cnt; q0 += kU) {
+        double v[kU], b[kU][kPer];
 #pragma unroll
-      for (int t = 0; t < kPer; ++t) {
-        const int c = lane + 32 * t;
-        if (c < w) {
-          const double b = __ldg(wr + c);
-          if (b != 0.0) acc[t] = __dadd_rn(acc[t], __dmul_rn(v, b));
+        for (int u = 0; u < kU; ++u) {
+          const int src = q0 + u < cnt ? q0 + u : 0;
+          v[u] = __shfl_sync(0xffffffffu, cv, src);
+          const double* wr = wt + static_cast<index_t>(__shfl_sync(0xffffffffu, cj, src)) * ldw;
+#pragma unroll
+          for (int t = 0; t < kPer; ++t) {
+            const int c = lane + 32 * t;
+            b[u][t] = (q0 + u < cnt && c < w) ? __ldg(wr + c) : 0.0;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int t = 0; t < kPer; ++t)
+            if (b[u][t] != 0.0) acc[t] = __dadd_rn(acc[t], __dmul_rn(v[u], b[u][t]));
       }
     }
 #pragma unroll
@@ -77,13 +92,34 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       acc[t] = accumulate && c < l ? fc[c] : 0.0;
     }
     const std::int64_t p1 = col_ptr[j + 1];
-    for (std::int64_t p = col_ptr[j]; p < p1; ++p) {
-      const double v = __ldg(val + p);
-      const double* ur = u + static_cast<index_t>(__ldg(row + p)) * ldu;
+    // as spmm_csr_kernel: (row, value) pairs 32 at a time, added in ascending p;
+    // one U row at a time (U rarely fits L2: the gathers need occupancy more
+    // than per-warp ILP — 4 rows in flight made F 1.8x slower)
+    constexpr int kU = 1;
+    for (std::int64_t p0 = col_ptr[j]; p0 < p1; p0 += 32) {
+      const int cnt = p1 - p0 < 32 ? static_cast<int>(p1 - p0) : 32;
+      const int cr = lane < cnt ? __ldg(row + p0 + lane) : 0;
+      const double cv = lane < cnt ? __ldg(val + p0 + lane) : 0.0;
+      for (int q0 = 0; q0 < cnt; q0 += kU) {
+        double v[kU], b[kU][kPer];
 #pragma unroll
-      for (int t = 0; t < kPer; ++t) {
-        const int c = lane + 32 * t;
-        if (c < l) acc[t] = __dadd_rn(acc[t], __dmul_rn(v, __ldg(ur + c)));
+        for (int uu = 0; uu < kU; ++uu) {
+          const int src = q0 + uu < cnt ? q0 + uu : 0;
+          v[uu] = __shfl_sync(0xffffffffu, cv, src);
+          const double* ur = u + static_cast<index_t>(__shfl_sync(0xffffffffu, cr, src)) * ldu;
+#pragma unroll
+          for (int t = 0; t < kPer; ++t) {
+            const int c = lane + 32 * t;
+            b[uu][t] = (q0 + uu < cnt && c < l) ? __ldg(ur + c) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int uu = 0; uu < kU; ++uu)
+          if (q0 + uu < cnt) {
+#pragma unroll
+            for (int t = 0; t < kPer; ++t)
+              if (lane + 32 * t < l) acc[t] = __dadd_rn(acc[t], __dmul_rn(v[uu], b[uu][t]));
+          }
       }
     }
 #pragma unroll
@@ -193,24 +229,33 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 #pragma unroll
     for (int t = 0; t < kPer; ++t) acc[t] = 0.0;
     const std::int64_t p1 = row_ptr[i + 1];
-    for (std::int64_t p = row_ptr[i]; p < p1; ++p) {
-      const double v = __ldg(val + p);
-      const uint4* mr = reinterpret_cast<const uint4*>(masks + static_cast<index_t>(__ldg(col + p)) * 2 * wpad);
-      std::uint32_t nz[kPer], ng[kPer];
+    // (column, value) pairs 32 at a time, one per lane, then one nonzero at a
+    // time in ascending p (the masks are one 32 B line; loading 4 nonzeros'
+    // masks together measured slower: 82 -> 90 ms at 1.19G nonzeros)
+    for (std::int64_t p0 = row_ptr[i]; p0 < p1; p0 += 32) {
+      const int cnt = p1 - p0 < 32 ? static_cast<int>(p1 - p0) : 32;
+      const int cj = lane < cnt ? __ldg(col + p0 + lane) : 0;
+      const double cv = lane < cnt ? __ldg(val + p0 + lane) : 0.0;
+      for (int q0 = 0; q0 < cnt; ++q0) {
+        const double v = __shfl_sync(0xffffffffu, cv, q0);
+        const uint4* mr =
+            reinterpret_cast<const uint4*>(masks + static_cast<index_t>(__shfl_sync(0xffffffffu, cj, q0)) * 2 * wpad);
+        std::uint32_t nz[kPer], ng[kPer];
 #pragma unroll
-      for (int q = 0; q < (kPer + 3) / 4; ++q) {
-        const uint4 a = __ldg(mr + q), b = __ldg(mr + wpad / 4 + q);
-        const std::uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        for (int q = 0; q < (kPer + 3) / 4; ++q) {
+          const uint4 a = __ldg(mr + q), b = __ldg(mr + wpad / 4 + q);
+          const std::uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (4 * q + r < kPer) {
-            nz[4 * q + r] = av[r];
-            ng[4 * q + r] = bv[r];
-          }
+          for (int r = 0; r < 4; ++r)
+            if (4 * q + r < kPer) {
+              nz[4 * q + r] = av[r];
+              ng[4 * q + r] = bv[r];
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kPer; ++t)
+          if ((nz[t] >> lane) & 1u) acc[t] = __dadd_rn(acc[t], ((ng[t] >> lane) & 1u) ? -v : v);
       }
-#pragma unroll
-      for (int t = 0; t < kPer; ++t)
-        if ((nz[t] >> lane) & 1u) acc[t] = __dadd_rn(acc[t], ((ng[t] >> lane) & 1u) ? -v : v);
     }
 #pragma unroll
     for (int t = 0; t < kPer; ++t) {

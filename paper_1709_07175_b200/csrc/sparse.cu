@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     const std::int64_t p1 = col_ptr[j + 1];
     // as spmm_csr_kernel: (row, value) pairs 32 at a time, added in ascending p;
     // one U row at a time (U rarely fits L2: the gathers need occupancy more
-    // than per-warp ILP — 4 rows in flight made F 1.8x slower)
+    // than per-warp ILP — 4 rows in flight made F 1.8x slower, 2 rows 1.13x)
     constexpr int kU = 1;
     for (std::int64_t p0 = col_ptr[j]; p0 < p1; p0 += 32) {
       const int cnt = p1 - p0 < 32 ? static_cast<int>(p1 - p0) : 32;

@@ -406,9 +406,11 @@ bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
                       bool densify, DevX& out) {
   const index_t m = x->rows, n = x->cols, nnz = x->nnz;
   const std::size_t es = dsize(x->dtype), nz = static_cast<std::size_t>(nnz > 0 ? nnz : 1);
-  index_t bad_col = -1;  // the first column whose col_ptr decreases
+  // the first column whose col_ptr decreases (or runs past nnz, which a later
+  // column must then undo: the entries before it stay inside the arrays)
+  index_t bad_col = -1;
   for (index_t j = 0; j < n && bad_col < 0; ++j)
-    if (x->col_ptr[j + 1] < x->col_ptr[j]) bad_col = j;
+    if (x->col_ptr[j + 1] < x->col_ptr[j] || x->col_ptr[j + 1] > nnz) bad_col = j;
   const index_t ncheck = bad_col >= 0 ? bad_col : n;
   const std::string sl(slot);
   auto* cp = ctx.get<std::int64_t>(sl + ".cp", n + 1);
@@ -534,7 +536,8 @@ DevX stage_x(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double*
     std::vector<double> vals(static_cast<std::size_t>(nnz));
     for (index_t j = 0; j < x->cols; ++j) {
       const index_t lo = x->col_ptr[j], hi = x->col_ptr[j + 1];
-      if (hi < lo) throw Error(kInvalidArgument, "csc: col_ptr must be non-decreasing");
+      // (hi > nnz: a later column must decrease; stop before reading past the arrays)
+      if (hi < lo || hi > nnz) throw Error(kInvalidArgument, "csc: col_ptr must be non-decreasing");
       for (index_t p = lo; p < hi; ++p) {
         const index_t r = x->row_idx[p];
         if (r < 0 || r >= x->rows)

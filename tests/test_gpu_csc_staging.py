@@ -88,6 +88,22 @@ def test_valid_csc_fit_equals_the_reference(ctx, ref, host, monkeypatch):
     assert np.max(np.abs(got.singular_values - s_ref) / s_ref) < 1e-12
 
 
+@pytest.mark.parametrize("host", ["0", "1"])
+def test_col_ptr_past_nnz_is_refused_without_reading_past_the_arrays(ctx, host, monkeypatch):
+    """A col_ptr entry beyond nnz (the last one still equal to nnz) makes a
+    later column decrease; the entries are never read past the arrays (the
+    reference reads out of bounds here, so only the library's behaviour is
+    checked): the decreasing col_ptr is reported."""
+    monkeypatch.setenv("LPCA_CSC_HOST", host)
+    cp, ri, va = _valid()
+    c = cp.copy()
+    c[3] = cp[-1] + 10 ** 12
+    x = lp.SparseMatrix(M, N, c, ri, va)
+    cfg = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=4, l=6, projection=lp.ProjectionSpec(seed=3))
+    with pytest.raises(lp.InvalidArgumentError, match="col_ptr must be non-decreasing"):
+        lp.reduce(x, cfg, ctx=ctx)
+
+
 @pytest.mark.parametrize("l", [20, 100, 150])
 def test_very_sparse_omega_on_sparse_x_matches_the_reference(ctx, ref, l):
     """The sign-mask sketch (spmm_csr_pm1) sums each U[i][c] over the row's

@@ -94,13 +94,21 @@ def peaks() -> dict:
 
 
 def cpu_model() -> str:
+    """Model name plus family/model/stepping (a virtualised host often reports a
+    generic name: family 6 model 143 is Sapphire Rapids, 207 Emerald Rapids),
+    the logical CPUs online and whether AVX-512 / AMX are exposed."""
+    info = {}
     try:
         for line in Path("/proc/cpuinfo").read_text().splitlines():
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
+            if ":" in line:
+                k, v = (t.strip() for t in line.split(":", 1))
+                info.setdefault(k, v)
     except OSError:
-        pass
-    return "unknown"
+        return "unknown"
+    flags = set(info.get("flags", "").split())
+    isa = "+".join(f for f in ("avx512f", "amx_tile") if f in flags) or "no avx512"
+    return (f"{info.get('model name', 'unknown')} (family {info.get('cpu family', '?')} model "
+            f"{info.get('model', '?')} stepping {info.get('stepping', '?')}, {os.cpu_count()} logical CPUs, {isa})")
 
 
 class ClockSampler:

@@ -80,8 +80,7 @@ void launch_csc_check(cudaStream_t s, index_t n, index_t rows, const std::int64_
                       unsigned long long* first);
 void launch_csr_from_csc(cudaStream_t s, index_t m, index_t nnz, const std::int32_t* ri, const std::int32_t* colof,
                          const double* cv, std::int64_t* rp, std::int32_t* ci, double* rv, std::int64_t* cnt,
-                         std::int32_t* keys_out, std::int32_t* perm_in, std::int32_t* perm_out, void* temp,
-                         std::size_t temp_bytes);
+                         std::int32_t* keys_out, void* temp, std::size_t temp_bytes);
 void launch_gemm_t_csc(cudaStream_t s, index_t n, const std::int64_t* col_ptr, const std::int32_t* row,
                        const double* val, const double* u, index_t ldu, index_t l, double* f, bool accumulate);
 // ---- verification metrics (metrics.cu; metrics.cpp:123-136, 311-352) -------------

@@ -400,7 +400,7 @@ void check_view(const lpca_matrix_view* x) {
 // order: the first column whose col_ptr decreases is found here, and an entry
 // error in an earlier column wins over it (the device checks exactly those
 // columns).
-// Returns false (nothing staged) when the device scratch (~32 B per entry)
+// Returns false (nothing staged) when the device scratch (~24 B per entry)
 // does not fit the free memory: the host path below then does the same work.
 bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot, double* h2d_bytes,
                       bool densify, DevX& out) {
@@ -418,15 +418,14 @@ bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   auto* cv = ctx.get<double>(sl + ".cv", nz);
   auto* first = ctx.get<unsigned long long>(sl + ".first", 1);
   // scratch (one cached workspace, reused by later calls of the same shape):
-  // the caller's 64-bit rows and values, each entry's column, the sort's keys
-  // and permutations, the row counts, CUB's temp. (A stream-ordered allocation
+  // the caller's 64-bit rows and values, each entry's column, the sorts' keys,
+  // the row counts, CUB's temp. (A stream-ordered allocation
   // returned its tens of GB to the driver at every call: 2-6 s of remapping.)
   const index_t nin = bad_col >= 0 ? x->col_ptr[bad_col] : nnz;  // entries of the checked columns
   const std::size_t tb = densify ? 0 : csc_stage_temp_bytes(m, nnz);
   auto a16 = [](std::size_t b) { return (b + 15) & ~std::size_t(15); };
   const std::size_t off_v = a16(nz * 8), off_c = off_v + a16(nz * es), off_k = off_c + a16(nz * 4),
-                    off_p0 = off_k + a16(nz * 4), off_p1 = off_p0 + a16(nz * 4), off_n = off_p1 + a16(nz * 4),
-                    off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)),
+                    off_n = off_k + a16(nz * 4), off_t = off_n + a16(8 * static_cast<std::size_t>(m + 1)),
                     total = densify ? off_k : off_t + tb;  // densify: the caller's arrays and colof only
   if (ctx.cached(sl + ".stage") < total) {
     ctx.release(sl + ".stage");
@@ -441,8 +440,6 @@ bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   void* vin = tmp + off_v;
   auto* colof = reinterpret_cast<std::int32_t*>(tmp + off_c);
   auto* keys = reinterpret_cast<std::int32_t*>(tmp + off_k);
-  auto* perm0 = reinterpret_cast<std::int32_t*>(tmp + off_p0);
-  auto* perm1 = reinterpret_cast<std::int32_t*>(tmp + off_p1);
   auto* cnt = reinterpret_cast<std::int64_t*>(tmp + off_n);
   LPCA_CUDA(cudaMemcpyAsync(cp, x->col_ptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx.stream));
   if (nin > 0) {
@@ -488,8 +485,8 @@ bool stage_csc_device(lpca_ctx& ctx, const lpca_matrix_view* x, const char* slot
   auto* rp = ctx.get<std::int64_t>(sl + ".rp", m + 1);
   auto* ci = ctx.get<std::int32_t>(sl + ".ci", nz);
   auto* rv = ctx.get<double>(sl + ".rv", nz);
-  launch_csr_from_csc(ctx.stream, m, nnz, ri, colof, cv, rp, ci, rv, cnt, keys, perm0, perm1, tmp + off_t, tb);
-  ctx.note_launch(3);  // row counts, iota, gather (+ CUB's scan and radix sort)
+  launch_csr_from_csc(ctx.stream, m, nnz, ri, colof, cv, rp, ci, rv, cnt, keys, tmp + off_t, tb);
+  ctx.note_launch(1);  // row counts (+ CUB's scan and two radix sorts)
   LPCA_CUDA(cudaGetLastError());
   keep_or_release_scratch();
   DevX d;

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -48,6 +49,12 @@ CONFIGS = {
     "c5": dict(m=8_000_000, n=2_048, r=500, rho=0.99, k=256, l=512, q=1, dtype="f64",
                name="configs[4]: X fp64 8,000,000x2,048, r=500, rho=0.99, k=256, l=512, q=1"),
 }
+# Not a BASELINE config: SURVEY 8(f1), sparse X shaped like the paper's malware
+# data (98,450 mostly binary features at density 0.0244, very
+# sparse Omega at the aggressive density log(k)/k, l = k), a 500k-row slice.
+SPARSE = dict(m=500_000, n=98_450, x_density=0.0244, k=100, l=100,
+              name="sparse X (SURVEY 8 f1): CSC 500,000x98,450 binary at density 0.0244, very sparse Omega "
+                   "log(k)/k, k=l=100, q=0")
 DEFAULT_CONFIG = "c3"
 # bounded CPU samples (rows) for the reference's CPU path: ~10-30 s of work for
 # cpu_baseline, a few seconds per step for --impl reference
@@ -506,13 +513,133 @@ def _e2e(args, cfg, ctx, host, conf, m_global, dist, lp, torch):
             "path": "lpca_fit_transform (C ABI), pinned host X in, host Y out (per rank)"}
 
 
+# ---- sparse X (not a BASELINE config) -----------------------------------------------
+def _sparse_csc(m: int, n: int, density: float, seed: int, torch):
+    """Canonical CSC built on the GPU: column j holds Binomial(m, density)
+    distinct uniformly drawn rows, values 1.0 (binary features)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    counts = torch.binomial(torch.full((n,), float(m), device="cuda"),
+                            torch.full((n,), density, device="cuda"), generator=g).long()
+    cols = torch.repeat_interleave(torch.arange(n, device="cuda"), counts)
+    rows = torch.randint(0, m, (cols.numel(),), device="cuda", generator=g)
+    keys = torch.unique(cols * m + rows)  # sorted column-major, duplicates merged
+    cols, rows = keys // m, keys % m
+    del keys
+    return cols, rows
+
+
+def _csc_arrays(m, n, cols, rows, torch, pinned):
+    """(col_ptr, row_idx, values) as host numpy arrays (row_idx / values pinned
+    when asked: the uploads then run at the PCIe rate)."""
+    col_ptr = torch.zeros(n + 1, dtype=torch.long, device="cuda")
+    col_ptr[1:] = torch.cumsum(torch.bincount(cols, minlength=n), 0)
+    vals = torch.ones(rows.numel(), dtype=torch.float64, device="cuda")
+
+    def host(t):
+        if not pinned:
+            return t.cpu().numpy()
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h.numpy()
+    return col_ptr.cpu().numpy(), host(rows), host(vals)
+
+
+def _sparse_reference(cfg, sample_rows, threads, cols, rows, steps, warmup, torch):
+    """The reference's reduce(lazy_spca) + apply_map on the first sample_rows
+    rows of the same CSC (oracle/_ref, all host threads)."""
+    from oracle import refbind as R
+    R.use_native(True)
+    R.set_threads(threads)
+    keep = rows < sample_rows
+    cp, ri, va = _csc_arrays(sample_rows, cfg["n"], cols[keep], rows[keep], torch, pinned=False)
+    dens = math.log(cfg["k"]) / cfg["k"]
+    secs = []
+    for i in range(warmup + steps):
+        _, _, _, sec = R.fit_transform_csc(2, sample_rows, cfg["n"], cp, ri, va, cfg["k"], cfg["l"], SEED_OMEGA,
+                                           kind=1, density=dens, want_y=True)
+        if i >= warmup:
+            secs.append(sec)
+    per = sum(secs) / len(secs)
+    desc = (f"{sample_rows} rows x {cfg['n']} of the same CSC (nnz {int(keep.sum())}); reduce(lazy_spca) + "
+            f"apply_map on the reference's SparseMatrix; {threads} threads on {cpu_model()}; reference built "
+            f"{R.build_flags()}; {len(secs)} timed reps")
+    return sample_rows / per, threads, desc, per
+
+
+def run_sparse(args):
+    """Sparse X on one GPU: every step is one lpca_fit_transform of a host CSC
+    (pinned) into a host Y — the upload, the device checks and CSR build, the
+    sketch (very sparse Omega as sign masks), F, the l x l step, the transform
+    and the Y download, wall clock. value and e2e are the same number here (a
+    CSC input always crosses PCIe); the phase split comes from ReducerTimings."""
+    import torch
+    import paper_1709_07175_b200 as lp
+    cfg = dict(SPARSE)
+    m = args.rows or cfg["m"]
+    torch.cuda.set_device(0)
+    cols, rows = _sparse_csc(m, cfg["n"], cfg["x_density"], 460, torch)
+    threads = len(os.sched_getaffinity(0))
+    if args.impl == "reference":
+        sr = args.ref_rows or 20_000
+        v, cores, desc, per = _sparse_reference(cfg, sr, threads, cols, rows, args.steps, args.warmup, torch)
+        print(json.dumps({"impl": "reference", "metric": METRIC + " (sparse X)", "value": v, "unit": "samples/s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic (binary CSC, seeded)",
+                          "config": {"workload": cfg["name"], "sample_rows": sr, "method": "lazy_spca"},
+                          "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
+                                           "sample": desc},
+                          "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    cp, ri, va = _csc_arrays(m, cfg["n"], cols, rows, torch, pinned=True)
+    x = lp.SparseMatrix(m, cfg["n"], cp, ri, va)
+    ctx = lp.Context(0)
+    conf = lp.ReducerConfig(method=lp.ReducerMethod.lazy_spca, k=cfg["k"], l=cfg["l"],
+                            projection=lp.ProjectionSpec(kind=lp.ProjectionKind.very_sparse,
+                                                         density=math.log(cfg["k"]) / cfg["k"], seed=SEED_OMEGA))
+    for _ in range(args.warmup):
+        lp.fit_transform(x, conf, ctx=ctx)
+    launches0 = ctx.launch_count()
+    tm = lp.ReducerTimings()
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            lp.fit_transform(x, conf, ctx=ctx, timings=tm)
+        torch.cuda.synchronize()
+        sec = (time.perf_counter() - t0) / args.steps
+    nnz = int(ri.size)
+    cpu = None
+    if not args.no_cpu:
+        v, cores, desc, _ = _sparse_reference(cfg, int(args.cpu_rows or 20_000), threads, cols, rows, 1, 1, torch)
+        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference", "sample": desc}
+    h2d = nnz * 16 + (cfg["n"] + 1) * 8
+    print(json.dumps({
+        "metric": METRIC + " (sparse X)", "value": m / sec, "unit": "samples/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "dtype_detail": "f64 values, CSR/CSC gathers in the reference's summation order",
+        "data": "synthetic (binary CSC at the paper's density, seeded)",
+        "config": {"workload": cfg["name"], "rows": m, "nnz": nnz, "method": "lazy_spca",
+                   "parallelism": "dp1", "l2": "inputs larger than L2 (CSC %.1f GB)" % (h2d / 1e9)},
+        "phases_ms": {p: getattr(tm, p) / args.steps * 1e3 for p in ("sketch", "f_form", "svd", "transform")},
+        "roofline": None, "cpu_baseline": cpu,
+        "e2e": {"value": m / sec, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": m * cfg["k"] * 8, "ms_per_step": sec * 1e3,
+                "path": "lpca_fit_transform (C ABI) on a pinned host CSC, host Y out"},
+        "gpu_launches": ctx.launch_count() - launches0, "clocks": clk.summary(),
+    }), flush=True)
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS) + ["sparse"])
     ap.add_argument("--rows", type=int, default=0, help="override the global row count (experiments only)")
     ap.add_argument("--gemm", default=None, choices=["tcgen05", "simt"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -522,6 +649,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--stub-worker", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.config == "sparse":
+        return run_sparse(args)
     cfg = CONFIGS[args.config]
     rc = relaunch_if_needed(args)
     if rc is not None:

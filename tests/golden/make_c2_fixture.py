@@ -4,7 +4,7 @@ compiled reference's streaming Lazy SPCA (reduce with block_rows = 25,000:
 reduce_lazy_spca_streaming over SliceRowBlockStream, proj/core/src/reducer.cpp:
 300-335) on the GPU box's host cores. Stores sigma (k = 100) and the first 10
 columns of V for tests/test_gpu_c2_full.py. Run on a GPU box (the generator is
-the device's): python tools/make_c2_fixture.py"""
+the device's): python tests/golden/make_c2_fixture.py"""
 import sys
 import time
 from pathlib import Path
@@ -12,7 +12,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 import paper_1709_07175_b200 as lp  # noqa: E402

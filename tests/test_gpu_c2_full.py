@@ -1,7 +1,7 @@
 """GPU: BASELINE configs[1] at FULL size (X fp32 1,000,000 x 4,096, l = 110,
 k = 100) through the bench's call (fit_transform), against the compiled
 reference's streaming Lazy SPCA on the same X (tests/golden/c2_full.npz, made
-on a GPU box's host cores by tools/make_c2_fixture.py from the device
+on a GPU box's host cores by tests/golden/make_c2_fixture.py from the device
 generator's X; VERDICT r1 missing #5)."""
 from pathlib import Path
 

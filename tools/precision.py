@@ -11,7 +11,13 @@ import torch
 sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_1709_07175_b200 as lp  # noqa: E402
-from oracle import lazypca_oracle as O  # noqa: E402
+
+def principal_angles(a, b):
+    """Principal angles (radians) between the column spaces of a and b."""
+    qa, _ = np.linalg.qr(a)
+    qb, _ = np.linalg.qr(b)
+    return np.arccos(np.clip(np.linalg.svd(qa.T @ qb, compute_uv=False), -1.0, 1.0))
+
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = dict(bench.CONFIGS[name])
@@ -43,9 +49,9 @@ torch.cuda.synchronize()
 v64, s64 = m64.v, m64.singular_values
 
 rel = np.abs(s32 - s64) / s64
-ang = O.principal_angles(v32, v64)
+ang = principal_angles(v32, v64)
 half = k // 2
-ang_top = O.principal_angles(v32[:, :half], v64[:, :half])
+ang_top = principal_angles(v32[:, :half], v64[:, :half])
 dy = (y32.double() - y64)
 print(f"{name} m={m} n={n} k={k} l={l} q={q}")
 print(f"  sigma rel per value: max {rel.max():.3e}  median {np.median(rel):.3e}")
